@@ -1,0 +1,369 @@
+"""FastFCA IP+EM fit throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+A step is one full fastfca_fit (all `iters` IP+EM iterations) over the
+config's synthetic mixture(s) -- SURVEY §8(d): the work unit is one TF-bin EM
+update, throughput = B*F*T*iters / t.  Under torchrun (N > 1) the flattened
+(mixture, bin) problems are split into contiguous balanced ranges, one per
+rank (frequency sharding: no exchange during the fit); the per-bin NLL slots
+are all-gathered over NCCL after the timed region to assemble the trace.
+
+value : device-resident inputs (x, H, W, L already in HBM), one fit kernel per
+        step timed with CUDA events on the launching stream, L2 flushed
+        between steps (a 256 MiB write), max over ranks.
+e2e   : the reference-facing C-ABI call ffca_fit with pinned HOST buffers in
+        the reference's Eigen layout (complex<double> x, double W/L/H): H2D,
+        boundary pack, fit, unpack, D2H -- host clock around the synchronous
+        call, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TF-bin EM updates/sec (F*T*iters/s) and % of HBM roofline, 1/2/4/8 B200"
+UNIT = "TF-bin-updates/s"
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def shard(P: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced range of the flattened problem index p = b*F + f."""
+    base, rem = divmod(P, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_inputs(cfg, lo: int, hi: int):
+    """Host inputs for problems [lo, hi) of the flattened (mixture, bin) index."""
+    from paper_2101_08563_b200 import synth
+    xs, Ws, Ls, Hs = [], [], [], []
+    F = cfg.F
+    for b in range(lo // F, (hi - 1) // F + 1):
+        f0 = max(lo - b * F, 0)
+        f1 = min(hi - b * F, F)
+        x = synth.mixture(cfg, b)
+        W, L, H = synth.init_params(cfg, b)
+        xs.append(x[f0:f1]); Ws.append(W[f0:f1]); Ls.append(L[f0:f1]); Hs.append(H[f0:f1])
+    return (np.concatenate(xs), np.concatenate(Ws), np.concatenate(Ls), np.concatenate(Hs))
+
+
+def cpu_baseline(cfg, args) -> dict:
+    """The oracle (fp64 restatement of the reference, all host threads) on a
+    bounded sample of the same workload: the first S bins of mixture 0, all
+    frames and iterations."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # test infrastructure: the CPU baseline leg only
+    cores = oracle.default_workers()
+    S = min(cfg.F, max(1, args.cpu_bins or 2 * cores))
+    from paper_2101_08563_b200 import synth
+    x = synth.mixture(cfg, 0)[:S].astype(np.complex128)
+    W, L, H = synth.init_params(cfg, 0)
+    _, _, _, _, _, secs = oracle.fit(x, W[:S], L[:S], H[:S], cfg.iters, record_trace=True,
+                                     workers=cores)
+    units = S * cfg.T * cfg.iters
+    return {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, "
+                      f"{cfg.iters} iters, fastfca_fit only ({secs:.2f} s)"}
+
+
+def run_reference(cfg, args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # the reference's CPU path (oracle port; reference unbuildable here)
+    from paper_2101_08563_b200 import synth
+    cores = oracle.default_workers()
+    S = min(cfg.F, max(1, args.cpu_bins or 2 * cores))
+    x = synth.mixture(cfg, 0)[:S].astype(np.complex128)
+    W, L, H = synth.init_params(cfg, 0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        _, _, _, _, _, secs = oracle.fit(x, W[:S], L[:S], H[:S], cfg.iters, record_trace=True,
+                                         workers=cores)
+        if i >= args.warmup:
+            times.append(secs)
+    units = S * cfg.T * cfg.iters
+    tot = sum(times)
+    v = units * len(times) / tot
+    sample = (f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, {cfg.iters} "
+              f"iters per step (oracle port of the reference; the reference needs Eigen3, absent)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config shapes)",
+        "config": {"workload": cfg.name, "M": cfg.M, "N": cfg.N, "F": cfg.F, "T": cfg.T,
+                   "iters": cfg.iters, "batch": cfg.batch, "sample_bins": S},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c1"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-bins", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2101_08563_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(cfg, args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2101_08563_b200 import _lib
+
+    P = cfg.batch * cfg.F
+    lo, hi = shard(P, world, rank)
+    Pl = hi - lo
+    M, N, T, iters = cfg.M, cfg.N, cfg.T, cfg.iters
+    x, W0, L0, H0 = build_inputs(cfg, lo, hi)
+    dev = torch.device("cuda", local)
+    fp64 = args.precision == "fp64"
+    cdt = torch.complex128 if fp64 else torch.complex64
+    rdt = torch.float64 if fp64 else torch.float32
+    x_d = torch.from_numpy(x).to(dev, cdt).contiguous()                     # [P, M, T]
+    H_init = torch.from_numpy(H0).to(dev, rdt).contiguous()                 # [P, N, T]
+    W_init = torch.from_numpy(np.ascontiguousarray(np.swapaxes(W0, -1, -2))).to(dev)  # col-major
+    L_init = torch.from_numpy(np.ascontiguousarray(np.swapaxes(L0, -1, -2))).to(dev)
+    H_d, W_d, L_d = H_init.clone(), W_init.clone(), L_init.clone()
+    power = torch.empty(Pl, dtype=torch.float64, device=dev)
+    slots = torch.zeros((iters + 1, Pl), dtype=torch.float64, device=dev)
+    status = torch.zeros(Pl, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ctx = _lib.Context(local)
+    L_ = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    prec = _lib.PREC_FP64 if fp64 else _lib.PREC_FP32
+    _lib.check(L_.ffca_power_scale_device(ctx.handle, Pl, M, T, prec, _lib.ptr(x_d),
+                                          _lib.ptr(power), sp))
+    opts = _lib.FitOpts(_lib.FLAVOR_EM, iters, 1, 0, 1, 0, prec)
+
+    def reset():
+        H_d.copy_(H_init); W_d.copy_(W_init); L_d.copy_(L_init)
+
+    def fit_once():
+        _lib.check(L_.ffca_fit_device(ctx.handle, Pl, cfg.F, lo, M, N, T, opts, _lib.ptr(x_d),
+                                      _lib.ptr(power), _lib.ptr(W_d), _lib.ptr(L_d),
+                                      _lib.ptr(H_d), _lib.ptr(slots), _lib.ptr(status), sp))
+        return ctx.launches()
+
+    for _ in range(args.warmup):
+        reset(); fit_once()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            reset()
+            flush.fill_(s & 0xff)  # evict L2 (126 MB) between timed steps
+            ev[s][0].record(stream)
+            launches += fit_once()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    units = P * T * iters * args.steps
+    value = units / (tot_ms / 1e3)
+
+    # Trace assembly: all-gather the per-bin slots (NCCL), bin-order sums.
+    st = status.cpu().numpy()
+    bad = int((st >= 2).sum())
+    if dist:
+        sizes = [shard(P, world, r)[1] - shard(P, world, r)[0] for r in range(world)]
+        mx = max(sizes)
+        pad = torch.zeros((iters + 1, mx), dtype=torch.float64, device=dev)
+        pad[:, :Pl] = slots
+        gath = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(gath, pad)
+        all_slots = torch.cat([g[:, :n] for g, n in zip(gath, sizes)], dim=1).cpu().numpy()
+        badt = torch.tensor([bad], device=dev)
+        dist.all_reduce(badt)
+        bad = int(badt.item())
+    else:
+        all_slots = slots.cpu().numpy()
+    trace = all_slots.reshape(iters + 1, cfg.batch, cfg.F).sum(axis=2)  # [iters+1, batch]
+    monotone = bool((trace[1:] <= trace[:-1] + 1e-5 * np.abs(trace[:-1])).all())
+
+    # e2e through the reference-facing C-ABI with pinned host buffers.
+    e2e = None
+    if not args.no_e2e:
+        xr = torch.from_numpy(np.ascontiguousarray(np.swapaxes(x, -1, -2)).astype(np.complex128)).pin_memory()
+        Wr = torch.from_numpy(np.ascontiguousarray(np.swapaxes(W0, -1, -2))).pin_memory()
+        Lr = torch.from_numpy(np.ascontiguousarray(np.swapaxes(L0, -1, -2))).pin_memory()
+        Hr0 = np.ascontiguousarray(np.swapaxes(H0, -1, -2))
+        Hr = torch.from_numpy(Hr0.copy()).pin_memory()
+        Wpin, Lpin = Wr.clone().pin_memory(), Lr.clone().pin_memory()
+        nll_h = torch.zeros(iters + 1, dtype=torch.float64).pin_memory()
+        d = _lib.Dims(1, Pl, M, N, T)
+        eopts = _lib.FitOpts(_lib.FLAVOR_EM, iters, 1, 0, 1, 0, prec)
+        ectx = _lib.Context(local)
+        times = []
+        for i in range(args.warmup + args.steps):
+            Hr.copy_(torch.from_numpy(Hr0)); Wpin.copy_(Wr); Lpin.copy_(Lr)
+            flush.fill_(i & 0xff)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _lib.check(L_.ffca_fit(ectx.handle, d, eopts, _lib.ptr(xr), None, _lib.ptr(Wpin),
+                                   _lib.ptr(Lpin), _lib.ptr(Hr), _lib.ptr(nll_h), None, None))
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                times.append(t1 - t0)
+        et = sum(times)
+        if dist:
+            t = torch.tensor([et], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        h2d = xr.numel() * 16 + Hr.numel() * 8 + Wpin.numel() * 16 + Lpin.numel() * 8
+        d2h = Hr.numel() * 8 + Wpin.numel() * 16 + Lpin.numel() * 8 + nll_h.numel() * 8
+        e2e = {"value": P * T * iters * len(times) / et, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": 1e3 * et / len(times)}
+
+    if rank == 0:
+        pk = peaks()
+        b_alg = 8 * M + 8 * N  # bytes per TF-bin-iteration
+        kern_s = (tot_ms / 1e3) / args.steps
+        achieved = (Pl * world) * T * iters * b_alg / kern_s / 1e9  # GB/s (whole job / world)
+        per_gpu = achieved / world
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get(cfg.name)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, args)
+        clocks = clk.summary()
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if cfg.batch == 1 else "weak",
+            "vs_baseline": None, "dtype": "f32" if not fp64 else "f64",
+            "data": "synthetic (seeded, BASELINE.json config shapes; paper data unavailable)",
+            "config": {"workload": cfg.name, "M": M, "N": N, "F": cfg.F, "T": T,
+                       "iters": iters, "batch": cfg.batch, "flavor": "em",
+                       "record_trace": True, "parallelism": f"freq-shard x{world}",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": per_gpu / pk["hbm_gbs"], "traffic": traffic,
+                         "peak_source": pk["source"],
+                         "algorithmic_bytes_per_unit": b_alg,
+                         "note": "algorithmic bytes (8M+8N per TF-bin-iteration) / kernel time;"
+                                 " x and H stay in shared memory across iterations, so DRAM"
+                                 " traffic is far below the algorithmic bytes"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "trace": {"nll_first": float(trace[0].sum()), "nll_last": float(trace[-1].sum()),
+                      "monotone": monotone, "failed_bins": bad},
+            "step_ms": step_ms,
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

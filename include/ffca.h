@@ -1,0 +1,134 @@
+/* ffca.h -- C ABI of the B200-native FastFCA hot path (libffca.so).
+ *
+ * Drop-in boundary for the reference's fit / separate entry points
+ * (reference proj/include/fastfca/fastfca.hpp:55-66, sigmodel.hpp:58,104).
+ * The reference is a C++ library with no FFI of its own; these entry points
+ * are what its C++ API (re-exposed in include/fastfca/*.hpp, implemented in
+ * paper_2101_08563_b200/csrc/shim.cpp on top of this ABI) and any ctypes /
+ * cgo / JNI binding call.  Plain pointers and sizes only.
+ *
+ * Host layouts are the reference containers' (Eigen column-major):
+ *   x       [batch][bins][frames][dim]   complex (re, im doubles)  Spectrogram::f[i]
+ *   W       [batch][bins][dim*dim]       complex, W(r,c) at r + c*dim  FastFcaParams::decorr
+ *   L       [batch][bins][dim*sources]   real,    L(m,n) at m + n*dim  FastFcaParams::loading
+ *   H       [batch][bins][sources*frames] real,   H(n,j) at n + j*sources  FastFcaParams::act
+ *   images  [sources][batch][bins][frames][dim] complex              fastfca_separate output
+ *
+ * Every function returns a status: FFCA_OK, FFCA_INVALID_ARGUMENT (the
+ * reference's std::invalid_argument), FFCA_NUMERICAL (NumericalError,
+ * types.hpp:21-24) or FFCA_CUDA_ERROR.  ffca_last_error() returns the message
+ * of the calling thread's last failure.  There is no CPU fallback: without a
+ * usable sm_100 device every compute entry point fails with FFCA_CUDA_ERROR.
+ */
+#ifndef FFCA_H_
+#define FFCA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFCA_OK 0
+#define FFCA_INVALID_ARGUMENT 1
+#define FFCA_NUMERICAL 2
+#define FFCA_CUDA_ERROR 3
+
+#define FFCA_FLAVOR_EM 0 /* LhFlavor::em (fastfca.hpp:16) */
+#define FFCA_FLAVOR_MM 1 /* LhFlavor::mm */
+
+#define FFCA_PREC_FP32 0 /* complex64 / fp32 data path, fp64 reductions and solves */
+#define FFCA_PREC_FP64 1 /* fp64 check mode */
+
+/* Per-bin status words written by the fit. */
+#define FFCA_BIN_OK 0
+#define FFCA_BIN_SILENT 1       /* power(i) <= 0: init kept (fastfca.cpp:165-170) */
+#define FFCA_BIN_IP_SINGULAR 2  /* ip_update_w failed after its restart (fastfca.cpp:63-65); column in bits 8.. */
+#define FFCA_BIN_SINGULAR_W 3   /* log_abs_det2 on a singular W (sigmodel.cpp:124-125) */
+
+typedef struct ffca_ctx ffca_ctx;
+
+typedef struct {
+  int batch;   /* independent mixtures (1 for the reference API) */
+  int bins;    /* F */
+  int dim;     /* M, 1..8 */
+  int sources; /* N, 1..16 */
+  int frames;  /* T */
+} ffca_dims;
+
+typedef struct {
+  int flavor;           /* FFCA_FLAVOR_EM / _MM                    (LhFlavor) */
+  int iters;            /* >= 0                                   (fastfca_fit iters) */
+  int record_trace;     /* FitOptions::record_trace (sigmodel.hpp:36) */
+  uint64_t seed;        /* FitOptions::seed (restart seeds only) */
+  int normalize_scales; /* FastFcaOptions::normalize_scales (fastfca.hpp:20) */
+  int fix_loadings;     /* FastFcaOptions::fix_loadings (fastfca.hpp:19) */
+  int precision;        /* FFCA_PREC_FP32 / FFCA_PREC_FP64 */
+} ffca_fit_opts;
+
+/* Library identity / build info. */
+int ffca_version(void);
+const char* ffca_last_error(void);
+int ffca_device_count(void);
+
+/* A context owns one CUDA device's stream and grow-only device buffers.  Not
+ * thread-safe: use one per host thread (the reference's fit is a reentrant
+ * pure function; the C++ shim creates one context per device). */
+int ffca_ctx_create(int device, ffca_ctx** out);
+void ffca_ctx_destroy(ffca_ctx* ctx);
+
+/* fastfca_fit (fastfca.hpp:55-58, fastfca.cpp:146-191) over `batch`
+ * independent mixtures.  W, L, H are the init on entry and the fitted
+ * parameters on return (silent bins and iters == 0 keep the init bit-exactly).
+ * power: SampleCovSet::power_scale [batch][bins], or NULL to compute it from x
+ * (sample_covs, sigmodel.cpp:17-48).  nll: [batch][iters+1] trace (bin-order
+ * sums of the per-bin slots, fastfca.cpp:186-189), required when
+ * record_trace; nll_slots (nullable): [batch][iters+1][bins]; bin_status
+ * (nullable): [batch][bins]. */
+int ffca_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts, const double* x,
+             const double* power, double* W, double* L, double* H, double* nll,
+             double* nll_slots, int32_t* bin_status);
+
+/* fastfca_separate (fastfca.hpp:65-66, fastfca.cpp:205-223). */
+int ffca_separate(ffca_ctx* ctx, const ffca_dims* dims, int precision, const double* x,
+                  const double* W, const double* L, const double* H, double* images);
+
+/* fastfca_nll_freq per bin (sigmodel.cpp:155-162): out [batch][bins]. */
+int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* dims, int precision, const double* x,
+                  const double* W, const double* L, const double* H, double* out);
+
+/* SampleCovSet::power_scale (sigmodel.cpp:43-44): out [batch][bins]. */
+int ffca_power_scale(ffca_ctx* ctx, const ffca_dims* dims, const double* x, double* out);
+
+/* ---- device-resident entry points (inputs already in HBM; used for the
+ * frequency-sharded multi-GPU path and the device-timed benchmark) ----
+ * x_soa  : [P][dim][frames] complex64 (fp32) or complex128 (fp64), t fastest
+ * H_soa  : [P][sources][frames] fp32 / fp64, in/out
+ * W, L   : [P][dim*dim] complex128, [P][dim*sources] fp64, in/out
+ * power  : [P] fp64;  nll_slots: [(iters+1)][P] fp64 or NULL;  status: [P]
+ * P = batch*bins problems; prob_offset = global index of problem 0 (only the
+ * restart seed uses it: bin index i = (prob_offset + p) % bins_per_mixture).
+ * stream: a cudaStream_t (NULL = the context's stream).  Asynchronous. */
+int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset, int dim,
+                    int sources, int frames, const ffca_fit_opts* opts, const void* x_soa,
+                    const double* power, double* W, double* L, void* H_soa, double* nll_slots,
+                    int32_t* status, void* stream);
+
+/* images_soa: [sources][P][dim][frames] complex64 / complex128. */
+int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int frames,
+                         int precision, const void* x_soa, const double* W, const double* L,
+                         const void* H_soa, void* images_soa, void* stream);
+
+/* power_scale from SoA complex64/complex128 x: out [P]. */
+int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, int precision,
+                            const void* x_soa, double* out, void* stream);
+
+/* Number of kernels the last call on this context launched (bench evidence). */
+int ffca_last_launch_count(const ffca_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFCA_H_ */

@@ -1,0 +1,141 @@
+"""ctypes binding of libffca.so (include/ffca.h).
+
+The product path is the CUDA library; this module only marshals pointers.
+Loading fails loudly if the library is missing, and every compute entry point
+raises if no B200 is present -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libffca.so"
+
+OK, INVALID_ARGUMENT, NUMERICAL, CUDA_ERROR = 0, 1, 2, 3
+FLAVOR_EM, FLAVOR_MM = 0, 1
+PREC_FP32, PREC_FP64 = 0, 1
+BIN_OK, BIN_SILENT, BIN_IP_SINGULAR, BIN_SINGULAR_W = 0, 1, 2, 3
+
+# Every symbol include/ffca.h declares (checked by tests/test_capi_exports.py).
+EXPORTS = (
+    "ffca_version", "ffca_last_error", "ffca_device_count", "ffca_ctx_create",
+    "ffca_ctx_destroy", "ffca_fit", "ffca_separate", "ffca_nll_bins", "ffca_power_scale",
+    "ffca_fit_device", "ffca_separate_device", "ffca_power_scale_device",
+    "ffca_last_launch_count",
+)
+
+
+class FfcaError(RuntimeError):
+    pass
+
+
+class InvalidArgument(FfcaError, ValueError):
+    """The reference's std::invalid_argument (shape / option errors)."""
+
+
+class NumericalError(FfcaError):
+    """The reference's fastfca::NumericalError (types.hpp:21-24)."""
+
+
+class CudaError(FfcaError):
+    pass
+
+
+class Dims(C.Structure):
+    _fields_ = [("batch", C.c_int), ("bins", C.c_int), ("dim", C.c_int),
+                ("sources", C.c_int), ("frames", C.c_int)]
+
+
+class FitOpts(C.Structure):
+    _fields_ = [("flavor", C.c_int), ("iters", C.c_int), ("record_trace", C.c_int),
+                ("seed", C.c_uint64), ("normalize_scales", C.c_int),
+                ("fix_loadings", C.c_int), ("precision", C.c_int)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FfcaError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                            "(no CPU fallback exists)")
+        L = C.CDLL(str(LIB_PATH))
+        P = C.c_void_p
+        dp = C.POINTER(C.c_double)
+        L.ffca_version.restype = C.c_int
+        L.ffca_last_error.restype = C.c_char_p
+        L.ffca_device_count.restype = C.c_int
+        L.ffca_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.ffca_ctx_destroy.argtypes = [P]
+        L.ffca_ctx_destroy.restype = None
+        L.ffca_fit.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
+        L.ffca_separate.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P, P, P]
+        L.ffca_nll_bins.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P, P, P]
+        L.ffca_power_scale.argtypes = [P, C.POINTER(Dims), P, P]
+        L.ffca_fit_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
+        L.ffca_separate_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           P, P, P, P, P, P]
+        L.ffca_power_scale_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]
+        L.ffca_last_launch_count.argtypes = [P]
+        _ = dp
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = lib().ffca_last_error().decode(errors="replace")
+    raise {INVALID_ARGUMENT: InvalidArgument, NUMERICAL: NumericalError}.get(rc, CudaError)(msg)
+
+
+def ptr(a) -> int | None:
+    """Address of a contiguous numpy array or torch tensor (None passes NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+        return a.ctypes.data
+    return int(a.data_ptr())
+
+
+class Context:
+    """One device's stream + buffers (ffca_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().ffca_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().ffca_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self) -> int:
+        return lib().ffca_last_launch_count(self.handle)
+
+
+_ctx_cache: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    if device is None:
+        device = int(os.environ.get("FFCA_DEVICE", "0"))
+    c = _ctx_cache.get(device)
+    if c is None:
+        c = _ctx_cache[device] = Context(device)
+    return c

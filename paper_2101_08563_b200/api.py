@@ -1,0 +1,228 @@
+"""Python mirror of the reference FastFCA API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(proj/include/fastfca/fastfca.hpp:16-66, sigmodel.hpp:34-111, stft.hpp:21-29),
+so parity tests read like the reference's own tests.  Arrays use natural
+numpy indexing (row index first); they are converted to the reference's
+Eigen column-major buffers at the C-ABI boundary (include/ffca.h).  All
+compute runs in libffca.so on the GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import InvalidArgument, NumericalError  # noqa: F401  (re-exported)
+
+
+class LhFlavor:  # fastfca.hpp:16
+    em = _lib.FLAVOR_EM
+    mm = _lib.FLAVOR_MM
+
+
+@dataclass
+class FitOptions:  # sigmodel.hpp:34-38
+    workers: int = 1            # host threads (unused by the GPU path; kept for the API)
+    record_trace: bool = True
+    seed: int = 0
+
+
+@dataclass
+class FastFcaOptions:  # fastfca.hpp:18-21
+    fix_loadings: bool = False
+    normalize_scales: bool = True
+
+
+@dataclass
+class Spectrogram:  # stft.hpp:21-29; f[i] is channels x frames
+    f: np.ndarray  # complex [bins, channels, frames]
+
+    @property
+    def bins(self) -> int:
+        return self.f.shape[0]
+
+    @property
+    def channels(self) -> int:
+        return self.f.shape[1]
+
+    @property
+    def frames(self) -> int:
+        return self.f.shape[2]
+
+    @staticmethod
+    def zero(channels: int, bins: int, frames: int) -> "Spectrogram":
+        return Spectrogram(np.zeros((bins, channels, frames), np.complex128))
+
+
+@dataclass
+class SampleCovSet:  # sigmodel.hpp:48-56, block_size == 1 snapshot branch
+    snapshots: np.ndarray    # complex [bins, dim, frames]
+    power_scale: np.ndarray  # [bins]
+    block_size: int = 1
+
+    @property
+    def dim(self) -> int:
+        return self.snapshots.shape[1]
+
+    @property
+    def bins(self) -> int:
+        return self.snapshots.shape[0]
+
+    @property
+    def frames(self) -> int:
+        return self.snapshots.shape[2]
+
+    blocks = frames
+
+    def power(self, i: int) -> float:
+        return float(self.power_scale[i])
+
+
+@dataclass
+class FastFcaParams:  # sigmodel.hpp:72-78
+    decorr: np.ndarray   # complex [bins, dim, dim]    W_i
+    loading: np.ndarray  # [bins, dim, sources]        L_i
+    act: np.ndarray      # [bins, sources, frames]     H_i
+
+    @property
+    def dim(self) -> int:
+        return self.decorr.shape[1]
+
+    @property
+    def bins(self) -> int:
+        return self.decorr.shape[0]
+
+    @property
+    def sources(self) -> int:
+        return self.loading.shape[2]
+
+    @property
+    def frames(self) -> int:
+        return self.act.shape[2]
+
+    def copy(self) -> "FastFcaParams":
+        return FastFcaParams(self.decorr.copy(), self.loading.copy(), self.act.copy())
+
+
+@dataclass
+class FastFcaFitResult:  # fastfca.hpp:23-26
+    params: FastFcaParams
+    nll: list = field(default_factory=list)
+    bin_status: np.ndarray | None = None
+
+
+# ------------------------------------------------------------ layout glue --
+def _x_ref(snapshots: np.ndarray) -> np.ndarray:
+    """[..., bins, dim, frames] -> reference [..., bins, frames, dim] complex128."""
+    return np.ascontiguousarray(np.swapaxes(snapshots, -1, -2), dtype=np.complex128)
+
+
+def _params_ref(p: FastFcaParams):
+    # Always copies: with a size-1 axis swapaxes is already contiguous, and a
+    # view would let the in/out C buffers alias the caller's arrays (the
+    # reference copies init, fastfca.cpp:153-154).
+    W = np.array(np.swapaxes(p.decorr, -1, -2), dtype=np.complex128, order="C", copy=True)
+    L = np.array(np.swapaxes(p.loading, -1, -2), dtype=np.float64, order="C", copy=True)
+    H = np.array(np.swapaxes(p.act, -1, -2), dtype=np.float64, order="C", copy=True)
+    return W, L, H
+
+
+def _params_from_ref(W, L, H) -> FastFcaParams:
+    return FastFcaParams(np.ascontiguousarray(np.swapaxes(W, -1, -2)),
+                         np.ascontiguousarray(np.swapaxes(L, -1, -2)),
+                         np.ascontiguousarray(np.swapaxes(H, -1, -2)))
+
+
+def _prec(precision: str) -> int:
+    if precision not in ("fp32", "fp64"):
+        raise InvalidArgument(f"precision must be 'fp32' or 'fp64', not {precision!r}")
+    return _lib.PREC_FP64 if precision == "fp64" else _lib.PREC_FP32
+
+
+# ------------------------------------------------------------------- API --
+def sample_covs(spec: Spectrogram, block_size: int = 1, *, device: int | None = None) -> SampleCovSet:
+    """sigmodel.cpp:17-48 for block_size == 1 (snapshots + power_scale)."""
+    if spec.bins == 0 or spec.frames == 0 or spec.channels == 0:
+        raise InvalidArgument("sample_covs: empty spectrogram")
+    if block_size < 1:
+        raise InvalidArgument("sample_covs: block size must be >= 1")
+    if block_size != 1:
+        raise InvalidArgument("sample_covs: block-stationary statistics (block_size > 1) are "
+                              "outside the GPU hot path (SURVEY §8(f) next #4)")
+    x = _x_ref(spec.f)
+    d = _lib.Dims(1, spec.bins, spec.channels, 1, spec.frames)
+    out = np.empty(spec.bins)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_power_scale(ctx.handle, d, _lib.ptr(x), _lib.ptr(out)))
+    return SampleCovSet(np.asarray(spec.f, dtype=np.complex128), out)
+
+
+def _check_shape(covs: SampleCovSet, init: FastFcaParams, what: str) -> None:
+    if (init.dim != covs.dim or init.bins != covs.bins or init.frames != covs.frames
+            or init.loading.shape[:2] != (covs.bins, covs.dim)
+            or init.act.shape[:2] != (covs.bins, init.sources)):
+        raise InvalidArgument(f"{what}: init/covariance shape mismatch")
+
+
+def fastfca_fit(covs: SampleCovSet, init: FastFcaParams, flavor: int, iters: int,
+                fit: FitOptions | None = None, opts: FastFcaOptions | None = None, *,
+                precision: str = "fp32", device: int | None = None) -> FastFcaFitResult:
+    """fastfca.cpp:146-191 on the GPU (one CTA per frequency bin)."""
+    fit = fit or FitOptions()
+    opts = opts or FastFcaOptions()
+    _check_shape(covs, init, "fastfca_fit")
+    if iters < 0:
+        raise InvalidArgument("fastfca_fit: negative iteration count")
+    x = _x_ref(covs.snapshots)
+    W, L, H = _params_ref(init)
+    F = covs.bins
+    d = _lib.Dims(1, F, covs.dim, init.sources, covs.frames)
+    o = _lib.FitOpts(int(flavor), int(iters), int(bool(fit.record_trace)), int(fit.seed),
+                     int(bool(opts.normalize_scales)), int(bool(opts.fix_loadings)),
+                     _prec(precision))
+    nll = np.zeros(iters + 1) if fit.record_trace else None
+    status = np.zeros(F, np.int32)
+    power = np.ascontiguousarray(covs.power_scale, dtype=np.float64)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_fit(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power), _lib.ptr(W),
+                                   _lib.ptr(L), _lib.ptr(H), _lib.ptr(nll), None,
+                                   _lib.ptr(status)))
+    return FastFcaFitResult(_params_from_ref(W, L, H), list(nll) if nll is not None else [],
+                            status)
+
+
+def fastfca_separate(spec: Spectrogram, params: FastFcaParams, *, precision: str = "fp32",
+                     device: int | None = None) -> list[Spectrogram]:
+    """fastfca.cpp:205-223: decorrelate, per-channel Wiener gains, project back."""
+    if spec.channels != params.dim or spec.bins != params.bins or spec.frames != params.frames:
+        raise InvalidArgument("fastfca_separate: shape mismatch")
+    x = _x_ref(spec.f)
+    W, L, H = _params_ref(params)
+    N, F, T, M = params.sources, spec.bins, spec.frames, spec.channels
+    out = np.empty((N, F, T, M), np.complex128)
+    d = _lib.Dims(1, F, M, N, T)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_separate(ctx.handle, d, _prec(precision), _lib.ptr(x),
+                                        _lib.ptr(W), _lib.ptr(L), _lib.ptr(H), _lib.ptr(out)))
+    return [Spectrogram(np.ascontiguousarray(np.swapaxes(out[n], -1, -2))) for n in range(N)]
+
+
+def fastfca_nll_bins(covs: SampleCovSet, params: FastFcaParams, *, precision: str = "fp32",
+                     device: int | None = None) -> np.ndarray:
+    """fastfca_nll_freq for every bin (sigmodel.cpp:155-162)."""
+    _check_shape(covs, params, "nll")
+    x = _x_ref(covs.snapshots)
+    W, L, H = _params_ref(params)
+    out = np.empty(covs.bins)
+    d = _lib.Dims(1, covs.bins, covs.dim, params.sources, covs.frames)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_nll_bins(ctx.handle, d, _prec(precision), _lib.ptr(x),
+                                        _lib.ptr(W), _lib.ptr(L), _lib.ptr(H), _lib.ptr(out)))
+    return out
+
+
+def fastfca_nll(covs: SampleCovSet, params: FastFcaParams, **kw) -> float:
+    """sigmodel.cpp:215-222 (bin-order sum)."""
+    return float(sum(fastfca_nll_bins(covs, params, **kw)))

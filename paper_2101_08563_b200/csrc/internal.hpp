@@ -1,0 +1,74 @@
+// internal.hpp -- host-side internals shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/ffca.h"
+#include "fit_kernel.cuh"
+
+// Set the calling thread's ffca_last_error() message; returns `code`.
+int ffca_set_err(int code, const std::string& msg);
+
+#define FFCA_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return ffca_set_err(FFCA_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct ffca_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int launches = 0;
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+  };
+  Buf bufs[16];
+  // Grow-only device scratch, slot k.
+  void* get(int k, size_t bytes, cudaError_t* err) {
+    Buf& b = bufs[k];
+    *err = cudaSuccess;
+    if (b.n >= bytes && b.p) return b.p;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    *err = cudaMalloc(&b.p, bytes < 256 ? 256 : bytes);
+    if (*err != cudaSuccess) return nullptr;
+    b.n = bytes;
+    return b.p;
+  }
+};
+
+namespace ffca {
+
+enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kNumSlots };
+
+// Threads per fit CTA: about 4 frames per thread, capped at 256; a multiple of
+// 32*M when the weighted-covariance pass is split by channel (M > 4).
+inline int fit_threads(int M, int T) {
+  const int per = (M <= 4) ? 32 : 32 * M;
+  const int want = (T + 3) / 4;
+  int th = ((want + per - 1) / per) * per;
+  const int cap = (256 / per) * per;
+  if (th > cap) th = cap;
+  if (th < per) th = per;
+  if (M <= 4 && th < 64) th = 64;
+  return th;
+}
+
+// Per-dim launchers (fit_m<M>.cu): fp64 selects the check-mode instantiation.
+#define FFCA_DECLARE_FIT_LAUNCHER(M) \
+  int launch_fit_m##M(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool fp64);
+FFCA_DECLARE_FIT_LAUNCHER(1)
+FFCA_DECLARE_FIT_LAUNCHER(2)
+FFCA_DECLARE_FIT_LAUNCHER(3)
+FFCA_DECLARE_FIT_LAUNCHER(4)
+FFCA_DECLARE_FIT_LAUNCHER(5)
+FFCA_DECLARE_FIT_LAUNCHER(6)
+FFCA_DECLARE_FIT_LAUNCHER(7)
+FFCA_DECLARE_FIT_LAUNCHER(8)
+
+}  // namespace ffca
