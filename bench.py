@@ -221,7 +221,10 @@ def main() -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ctx = _lib.Context(local)
     L_ = _lib.lib()
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: every copy, flush, event and fit kernel is ordered on it
+    # (the library launches on the stream it is given).
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     prec = _lib.PREC_FP64 if fp64 else _lib.PREC_FP32
     _lib.check(L_.ffca_power_scale_device(ctx.handle, Pl, M, T, prec, _lib.ptr(x_d),

@@ -145,3 +145,14 @@ template <typename R> __device__ __forceinline__ R narrow_pos(double v) {
   return (v > 0.0 && !(r > R(0))) ? tiny<R>() : r;
 }
 }  // namespace ffca
+
+namespace ffca {
+// Reciprocal on the SFU (MUFU.RCP, ~1 ulp) for the fp32 data path; exact
+// division in the fp64 check mode.
+__device__ __forceinline__ float rcp_fast(float a) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ double rcp_fast(double a) { return 1.0 / a; }
+}  // namespace ffca

@@ -12,15 +12,20 @@
 //            the per-bin NLL of the previous iterate (sigmodel.cpp:155-162)
 //            and all M weighted covariances Q_m (fastfca.cpp:22-34), reduced
 //            once for the whole CTA.
-//   IP       thread 0, fp64: M sequential column solves with the residual
-//            check and the libstdc++-faithful seeded restart (fastfca.cpp:36-72).
+//   IP       one thread, fp64 in registers: M sequential column solves with the
+//            residual check and the libstdc++-faithful seeded restart
+//            (fastfca.cpp:36-72).
 //   EM       N+1 sweeps: sweep n finishes source n-1's H row with the freshly
 //            reduced L column and accumulates source n's L reduction
 //            (em_update_lh, fastfca.cpp:80-99); sweep 0 also forms U = |W^H x|^2
 //            (sigmodel.cpp:93-107).
 //   MM       two sweeps (mm_update_lh, fastfca.cpp:101-117).
-//   balance  thread 0 on the reduced row means (fastfca.cpp:127-142); the H
+//   balance  one thread on the reduced row means (fastfca.cpp:127-142); the H
 //            row scale is applied lazily by the next sweep that touches H.
+// Every reduction is: warp shuffles -> per-warp partials in shared memory ->
+// barrier -> warp 0 sums the partials in a fixed order (fp64) -> lane 0 does
+// the serial update -> barrier.  The order is fixed for a launch shape, so
+// per-bin results do not depend on how bins are sharded over GPUs.
 #pragma once
 
 #include "common.cuh"
@@ -38,7 +43,7 @@ struct FitParams {
   double2* W;       // [nprob][M*M] col-major (r + c*M), in/out
   double* L;        // [nprob][M*N] col-major (m + n*M), in/out
   const double* power;  // [nprob] SampleCovSet::power_scale
-  double* nll;      // slot(t, p) at nll[t * nll_stride + p]; may be null
+  double* nll;      // slot(t, p) at nll[t * nll_stride + prob_offset + p]; may be null
   int nll_stride;
   int* status;      // [nprob]: 0 ok, 1 silent band, 2 IP singular, 3 singular W
   int iters, flavor, record, normalize, fix_loadings, resident;
@@ -57,8 +62,14 @@ struct Split {
   static constexpr int KA = MG * M * M + 1;  // pass-A values per thread
 };
 
+// Occupancy target: CTAs per SM the register budget must allow (256 threads).
+template <int M>
+struct Occ {
+  static constexpr int value = (M <= 3) ? 4 : (M == 4 ? 2 : 1);
+};
+
 // Shared-memory carve-up, identical on host and device.
-template <int M, int NMAX, typename R>
+template <int M, int NT, typename R>
 struct FitSmem {
   int off_wd, off_wr, off_ld, off_lr, off_lold, off_linv, off_hs, off_us, off_hsum, off_num,
       off_den, off_red, off_res, off_scal, off_big, kred, kres, total;
@@ -68,29 +79,31 @@ struct FitSmem {
     kred = S::KA;
     if (M + 1 > kred) kred = M + 1;
     if (2 * M * nc > kred) kred = 2 * M * nc;
-    if (NMAX > kred) kred = NMAX;
+    if (NT > kred) kred = NT;
     kres = M * M * M + 1;
     if (kres < kred) kres = kred;
     int o = 0;
     off_wd = o; o = al(o + M * M * 16);
     off_wr = o; o = al(o + M * M * 2 * (int)sizeof(R));
-    off_ld = o; o = al(o + M * NMAX * 8);
-    off_lr = o; o = al(o + M * NMAX * (int)sizeof(R));
+    off_ld = o; o = al(o + M * NT * 8);
+    off_lr = o; o = al(o + M * NT * (int)sizeof(R));
     off_lold = o; o = al(o + M * (int)sizeof(R));
     off_linv = o; o = al(o + M * (int)sizeof(R));
-    off_hs = o; o = al(o + NMAX * (int)sizeof(R));
+    off_hs = o; o = al(o + NT * (int)sizeof(R));
     off_us = o; o = al(o + M * (int)sizeof(R));
-    off_hsum = o; o = al(o + NMAX * 8);
-    off_num = o; o = al(o + M * NMAX * 8);
-    off_den = o; o = al(o + M * NMAX * 8);
+    off_hsum = o; o = al(o + NT * 8);
+    off_num = o; o = al(o + M * NT * 8);
+    off_den = o; o = al(o + M * NT * 8);
     off_red = o;  // also the restart RNG state during the (serial) IP stage
-    o = al(o + (nwarps * kred * 8 > (int)sizeof(Mt19937_64) ? nwarps * kred * 8 : (int)sizeof(Mt19937_64)));
+    {
+      const int need = nwarps * kred * 8;
+      o = al(o + (need > (int)sizeof(Mt19937_64) ? need : (int)sizeof(Mt19937_64)));
+    }
     off_res = o; o = al(o + kres * 8);
     off_scal = o; o = al(o + 64);
     off_big = o;
     if (resident) o = al(o + T * (M * 2 * (int)sizeof(R) + N * (int)sizeof(R) + M * (int)sizeof(R)));
     total = o;
-    (void)N;
   }
 };
 
@@ -100,79 +113,126 @@ struct Scalars {
 };
 
 // ------------------------------------------------------------- fp64 algebra --
-// In-place LU with partial pivoting (max modulus, Eigen::PartialPivLU order).
+// Everything below runs in one thread on register arrays (M is a compile-time
+// constant, every loop unrolls).  Pivot order follows Eigen::PartialPivLU
+// (largest modulus; compared as squared modulus, the same order).
 template <int M>
-__device__ __noinline__ void lu_factor(double2* a, int* perm) {
+__device__ __forceinline__ void lu_factor(double2 (&a)[M * M], int (&perm)[M]) {
+#pragma unroll
   for (int k = 0; k < M; ++k) perm[k] = k;
+#pragma unroll
   for (int k = 0; k < M; ++k) {
     int p = k;
-    double best = cabs(a[k + k * M]);
+    double best = cabs2(a[k + k * M]);
+#pragma unroll
     for (int r = k + 1; r < M; ++r) {
-      const double v = cabs(a[r + k * M]);
+      const double v = cabs2(a[r + k * M]);
       if (v > best) best = v, p = r;
     }
-    if (p != k) {
-      for (int c = 0; c < M; ++c) {
-        const double2 t = a[k + c * M];
-        a[k + c * M] = a[p + c * M];
-        a[p + c * M] = t;
+    // Swap rows k and p with static indices (p is runtime).
+#pragma unroll
+    for (int r = k + 1; r < M; ++r) {
+      if (r == p) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double2 t = a[k + c * M];
+          a[k + c * M] = a[r + c * M];
+          a[r + c * M] = t;
+        }
+        const int t = perm[k];
+        perm[k] = perm[r];
+        perm[r] = t;
       }
-      const int t = perm[k];
-      perm[k] = perm[p];
-      perm[p] = t;
     }
     if (best != 0.0) {
       const double2 piv = a[k + k * M];
+#pragma unroll
       for (int r = k + 1; r < M; ++r) a[r + k * M] = cdiv(a[r + k * M], piv);
+#pragma unroll
       for (int c = k + 1; c < M; ++c)
+#pragma unroll
         for (int r = k + 1; r < M; ++r)
           a[r + c * M] = csub(a[r + c * M], cmul(a[r + k * M], a[k + c * M]));
     }
   }
 }
 
+// Solve (P^T L U) y = e_col.
 template <int M>
-__device__ __noinline__ void lu_solve(const double2* lu, const int* perm, const double2* b, double2* y) {
-  for (int k = 0; k < M; ++k) y[k] = b[perm[k]];
+__device__ __forceinline__ void lu_solve_unit(const double2 (&lu)[M * M], const int (&perm)[M],
+                                              int col, double2 (&y)[M]) {
+#pragma unroll
+  for (int k = 0; k < M; ++k) y[k] = make_double2(perm[k] == col ? 1.0 : 0.0, 0.0);
+#pragma unroll
   for (int k = 0; k < M; ++k)
+#pragma unroll
     for (int r = k + 1; r < M; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
+#pragma unroll
   for (int k = M - 1; k >= 0; --k) {
     y[k] = cdiv(y[k], lu[k + k * M]);
+#pragma unroll
     for (int r = 0; r < k; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
   }
 }
 
-// sigmodel.cpp:118-129.  Returns false when W is numerically singular.
+// log|det W|^2 (sigmodel.cpp:118-129).  Returns false when W is numerically
+// singular (a zero or non-finite U diagonal).
 template <int M>
-__device__ __noinline__ bool log_abs_det2(const double2* w, double& out) {
+__device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
   double2 a[M * M];
   int perm[M];
+#pragma unroll
   for (int k = 0; k < M * M; ++k) a[k] = w[k];
   lu_factor<M>(a, perm);
   double acc = 0.0;
+#pragma unroll
   for (int k = 0; k < M; ++k) {
-    const double v = cabs(a[k + k * M]);
+    const double v = cabs2(a[k + k * M]);
     if (!(v > 0.0) || !isfinite(v)) return false;
     acc += log(v);
   }
-  out = 2.0 * acc;
+  out = acc;  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
   return true;
+}
+
+// Cold path of ip_update_w: one seeded perturbation of column `col`
+// (fastfca.cpp:66-69).  The generator is seeded lazily on the first restart
+// of the sweep and its state lives in shared scratch.
+static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng, bool* seeded,
+                                        PolarNormal* gauss, unsigned long long seed, int bin) {
+  if (!*seeded) {
+    rng->seed(mix_seed(seed, bin));
+    *seeded = true;
+  }
+  double cn = 0.0;
+  for (int r = 0; r < m; ++r) cn += cabs2(wcol[r]);
+  const double mag = 1e-8 * (sqrt(cn) + 1.0);
+  for (int r = 0; r < m; ++r) {
+    const double im = (*gauss)(*rng);  // g++ evaluates Complex(g(), g()) right to left
+    const double re = (*gauss)(*rng);
+    wcol[r].x += mag * re;
+    wcol[r].y += mag * im;
+  }
 }
 
 // ip_update_w (fastfca.cpp:36-72) on the reduced weighted covariances.
 // qraw[m*M*M + ...] holds sum_t x x^H / sigma2_m packed as: (a,a) real,
 // (a,b) a<b real part at a*M+b and imaginary part at b*M+a.
 template <int M>
-__device__ __noinline__ bool ip_update(double2* w, const double* qraw, int T, unsigned long long seed, int bin, Mt19937_64* rng_state,
-                          int& bad_col) {
-  Mt19937_64* rng = nullptr;  // seeded lazily: draws happen only on restarts
+__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
+                                          unsigned long long seed, int bin, Mt19937_64* rng,
+                                          int& bad_col) {
+  bool seeded = false;
   PolarNormal gauss{0.0, false};
   const double invT = 1.0 / double(T);
+#pragma unroll 1
   for (int col = 0; col < M; ++col) {
     double2 q[M * M];
     const double* p = qraw + col * M * M;
+#pragma unroll
     for (int a = 0; a < M; ++a) {
       q[a + a * M] = make_double2(p[a * M + a] * invT, 0.0);
+#pragma unroll
       for (int b = a + 1; b < M; ++b) {
         const double re = p[a * M + b] * invT, im = p[b * M + a] * invT;
         q[a + b * M] = make_double2(re, im);   // Q(a,b) = sum x_a conj(x_b)
@@ -180,41 +240,52 @@ __device__ __noinline__ bool ip_update(double2* w, const double* qraw, int T, un
       }
     }
     for (int attempt = 0;; ++attempt) {
-      double2 a[M * M], lu[M * M], e[M], wm[M];
+      double2 wr[M * M];
+#pragma unroll
+      for (int k = 0; k < M * M; ++k) wr[k] = w[k];
+      double2 a[M * M], lu[M * M], wm[M];
       int perm[M];
       double anorm = 0.0;
+#pragma unroll
       for (int r = 0; r < M; ++r)
+#pragma unroll
         for (int c = 0; c < M; ++c) {
           double2 s = make_double2(0.0, 0.0);
-          for (int k = 0; k < M; ++k) s = cadd(s, cmulc(w[k + r * M], q[k + c * M]));
+#pragma unroll
+          for (int k = 0; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
           a[r + c * M] = s;  // (W^H Q)(r,c)
           lu[r + c * M] = s;
           anorm += cabs2(s);
         }
-      for (int k = 0; k < M; ++k) e[k] = make_double2(k == col ? 1.0 : 0.0, 0.0);
       lu_factor<M>(lu, perm);
-      lu_solve<M>(lu, perm, e, wm);
+      lu_solve_unit<M>(lu, perm, col, wm);
       double wn = 0.0, rn = 0.0;
       bool fin = true;
+#pragma unroll
       for (int k = 0; k < M; ++k) {
         wn += cabs2(wm[k]);
         fin = fin && isfinite(wm[k].x) && isfinite(wm[k].y);
       }
+#pragma unroll
       for (int r = 0; r < M; ++r) {
-        double2 s = make_double2(0.0, 0.0);
+        double2 s = make_double2(r == col ? -1.0 : 0.0, 0.0);
+#pragma unroll
         for (int c = 0; c < M; ++c) s = cadd(s, cmul(a[r + c * M], wm[c]));
-        rn += cabs2(csub(s, e[r]));
+        rn += cabs2(s);
       }
       const double scale = sqrt(anorm) * sqrt(wn) + 1.0;
       if (fin && sqrt(rn) <= 1e-8 * scale) {
         double en = 0.0;
+#pragma unroll
         for (int r = 0; r < M; ++r) {
           double2 qw = make_double2(0.0, 0.0);
+#pragma unroll
           for (int c = 0; c < M; ++c) qw = cadd(qw, cmul(q[r + c * M], wm[c]));
           en += cmulc(wm[r], qw).x;
         }
         if (en > 0.0 && isfinite(en)) {
           const double s = 1.0 / sqrt(en);
+#pragma unroll
           for (int r = 0; r < M; ++r) w[r + col * M] = make_double2(wm[r].x * s, wm[r].y * s);
           break;
         }
@@ -223,57 +294,24 @@ __device__ __noinline__ bool ip_update(double2* w, const double* qraw, int T, un
         bad_col = col;
         return false;
       }
-      if (!rng) {
-        rng_state->seed(mix_seed(seed, bin));
-        rng = rng_state;
-      }
-      double cn = 0.0;
-      for (int r = 0; r < M; ++r) cn += cabs2(w[r + col * M]);
-      const double mag = 1e-8 * (sqrt(cn) + 1.0);
-      for (int r = 0; r < M; ++r) {
-        const double im = gauss(*rng);  // g++ evaluates Complex(g(), g()) right to left
-        const double re = gauss(*rng);
-        w[r + col * M].x += mag * re;
-        w[r + col * M].y += mag * im;
-      }
+      ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
     }
   }
   return true;
 }
 
-// -------------------------------------------------------------- reductions --
-// Reduce K per-thread values over the CTA: warp shuffles, then an ordered fp64
-// sum over warps (deterministic for a fixed launch shape).
-template <int K, typename T>
-__device__ __forceinline__ void block_reduce(const T (&v)[K], int kact, double* red, double* res,
-                                             int nwarps) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (k < kact) {
-      const T s = warp_sum(v[k]);
-      if (lane == 0) red[warp * K + k] = double(s);
-    }
-  }
-  __syncthreads();
-  for (int o = threadIdx.x; o < kact; o += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nwarps; ++w) s += red[w * K + o];
-    res[o] = s;
-  }
-  __syncthreads();
-}
-
 // ------------------------------------------------------------------ kernel --
-template <int M, int NMAX, typename R>
-__global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kernel(FitParams p) {
+template <int M, int NT, bool EXACT, typename R>
+__global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
-  const int N = p.N, T = p.T;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int N = EXACT ? NT : p.N;
+  const int T = p.T;
   const int b = blockIdx.x;
-  const FitSmem<M, NMAX, R> lay(nwarps, N, T, p.nc, p.resident != 0);
+  const FitSmem<M, NT, R> lay(nwarps, N, T, p.nc, p.resident != 0);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
   double* Ld = reinterpret_cast<double*>(smem + lay.off_ld);
@@ -288,6 +326,9 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
   double* red = reinterpret_cast<double*>(smem + lay.off_red);
   double* res = reinterpret_cast<double*>(smem + lay.off_res);
   Scalars* sc = reinterpret_cast<Scalars*>(smem + lay.off_scal);
+
+  // Source-loop guard: folds away when N is the compile-time NT.
+#define FFCA_NK(k) (EXACT || (k) < N)
 
   const C* xg = reinterpret_cast<const C*>(p.x) + size_t(b) * M * T;
   R* Hg = reinterpret_cast<R*>(p.H) + size_t(b) * N * T;
@@ -316,7 +357,7 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
     Ld[k] = l;
     Lr[k] = R(l);
   }
-  for (int k = tid; k < NMAX; k += nthreads) hs[k] = R(1);
+  for (int k = tid; k < NT; k += nthreads) hs[k] = R(1);
   for (int k = tid; k < M; k += nthreads) us[k] = R(1);
   const double power = p.power[b];
   if (tid == 0) {
@@ -329,10 +370,24 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
   const bool update_loading = !p.fix_loadings;
   const int bin_index = (p.prob_offset + b) % p.F;
 
+  // Warp-0 fixed-order sum of per-warp partials red[w*K + o] -> res[o].
+  auto gather = [&](int K, int kact) {
+    if (warp == 0) {
+      for (int o = lane; o < kact; o += 32) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w * K + o];
+        res[o] = s;
+      }
+      __syncwarp();
+    }
+  };
+
   // ---------------------------------------------------------------- pass A --
   // first: U from x and the current W; else U = stored U * us (balance).
+  // Leaves the reduced Q_m (packed) in res[0, M^3) and the NLL in res[M^3],
+  // visible to warp 0 (the caller's serial section runs on thread 0).
   auto pass_a = [&](bool first, bool want_q, bool want_nll) {
-    constexpr int MSPLIT = S::MSPLIT, MG = S::MG;
+    constexpr int MSPLIT = S::MSPLIT, MG = S::MG, KA = S::KA;
     const int gs = nthreads / MSPLIT;
     const int g = tid / gs, lt = tid - g * gs;
     const int m0 = g * MG;
@@ -344,9 +399,9 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       C xv[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) xv[m] = xs[m * T + t];
-      R h[NMAX];
+      R h[NT];
 #pragma unroll
-      for (int k = 0; k < NMAX; ++k) h[k] = (k < N) ? Hs[k * T + t] * hs[k] : R(0);
+      for (int k = 0; k < NT; ++k) h[k] = FFCA_NK(k) ? Hs[k * T + t] * hs[k] : R(0);
       R P[M * M];
       if (want_q) {
 #pragma unroll
@@ -366,9 +421,9 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
         const int m = m0 + mi;
         R s2 = eps;
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
-          if (k < N) s2 += Lr[m + k * M] * h[k];
-        const R r = rcp(s2);
+        for (int k = 0; k < NT; ++k)
+          if (FFCA_NK(k)) s2 += Lr[m + k * M] * h[k];
+        const R r = rcp_fast(s2);
         if (want_nll) {
           R u;
           if (first) {
@@ -388,9 +443,6 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       }
       nll += double(nll_t);
     }
-    // reduction: per warp, then per group over its warps.
-    const int lane = tid & 31, warp = tid >> 5;
-    constexpr int KA = S::KA;
     if (want_q) {
 #pragma unroll
       for (int k = 0; k < MG * M * M; ++k) {
@@ -403,21 +455,23 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       if (lane == 0) red[warp * KA + KA - 1] = s;
     }
     __syncthreads();
-    const int wpg = nwarps / MSPLIT;  // warps per group
-    const int nout = want_q ? M * M * M : 0;
-    for (int o = tid; o <= nout; o += nthreads) {
-      double s = 0.0;
-      if (o == nout) {
-        for (int w = 0; w < nwarps; ++w) s += red[w * KA + KA - 1];
-        res[M * M * M] = s;
-      } else {
-        const int m = o / (M * M), k = o - m * M * M;
-        const int grp = m / MG, mi = m - grp * MG;
-        for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + mi * M * M + k];
-        res[o] = s;
+    if (warp == 0) {
+      const int wpg = nwarps / MSPLIT;  // warps per channel group
+      const int nout = want_q ? M * M * M : 0;
+      for (int o = lane; o <= nout; o += 32) {
+        double s = 0.0;
+        if (o == nout) {
+          for (int w = 0; w < nwarps; ++w) s += red[w * KA + KA - 1];
+          res[M * M * M] = s;
+        } else {
+          const int m = o / (M * M), k = o - m * M * M;
+          const int grp = m / MG, mi = m - grp * MG;
+          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + mi * M * M + k];
+          res[o] = s;
+        }
       }
+      __syncwarp();
     }
-    __syncthreads();
   };
 
   // ------------------------------------------------- EM sweep n (0..N) --
@@ -429,10 +483,10 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
     for (int k = 0; k <= M; ++k) acc[k] = R(0);
     const int j = n - 1;
     for (int t = tid; t < T; t += nthreads) {
-      R h[NMAX];
+      R h[NT];
 #pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < N) {
+      for (int k = 0; k < NT; ++k) {
+        if (FFCA_NK(k)) {
           R v = Hs[k * T + t];
           if (apply_hs) {
             v *= hs[k];
@@ -463,24 +517,24 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       if (j >= 0) {
         R hj = R(0);
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
+        for (int k = 0; k < NT; ++k)
           if (k == j) hj = h[k];
         R hsum_m = R(0);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           R lh = eps;
 #pragma unroll
-          for (int k = 0; k < NMAX; ++k)
-            if (k < N) lh += ((k == j) ? Lold[m] : Lr[m + k * M]) * h[k];
+          for (int k = 0; k < NT; ++k)
+            if (FFCA_NK(k)) lh += ((k == j) ? Lold[m] : Lr[m + k * M]) * h[k];
           const R lnhn = Lold[m] * hj;
-          const R gg = lnhn * rcp(lh);
+          const R gg = lnhn * rcp_fast(lh);
           const R phi = gg * gg * u[m] + (R(1) - gg) * lnhn;
           hsum_m += Linv[m] * phi;
         }
-        R hn = hsum_m / R(M);
+        R hn = hsum_m * R(1.0 / M);
         hn = hn > tiny<R>() ? hn : tiny<R>();
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
+        for (int k = 0; k < NT; ++k)
           if (k == j) h[k] = hn;
         Hs[j * T + t] = hn;
         acc[M] += hn;
@@ -488,37 +542,44 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       if (n < N) {
         R hn = R(0);
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
+        for (int k = 0; k < NT; ++k)
           if (k == n) hn = h[k];
-        const R ihn = rcp(hn);
+        const R ihn = rcp_fast(hn);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           R lh = eps;
 #pragma unroll
-          for (int k = 0; k < NMAX; ++k)
-            if (k < N) lh += Lr[m + k * M] * h[k];
+          for (int k = 0; k < NT; ++k)
+            if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
           const R lnhn = Lr[m + n * M] * hn;
-          const R gg = lnhn * rcp(lh);
+          const R gg = lnhn * rcp_fast(lh);
           const R phi = gg * gg * u[m] + (R(1) - gg) * lnhn;
           acc[m] += phi * ihn;
         }
       }
     }
-    block_reduce<M + 1>(acc, M + 1, red, res, nwarps);
+#pragma unroll
+    for (int k = 0; k <= M; ++k) {
+      const R s = warp_sum(acc[k]);
+      if (lane == 0) red[warp * (M + 1) + k] = double(s);
+    }
+    __syncthreads();
+    gather(M + 1, M + 1);
   };
 
   // ------------------------------------------------------ MM sweeps --
   // L update: num/den reductions over t for sources [n0, n0+nc).
   auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u, bool apply_hs) {
     constexpr int NCMAX = (16 / M) > 0 ? (16 / M) : 1;
-    R acc[2 * M * NCMAX];
+    constexpr int K = 2 * M * NCMAX;
+    R acc[K];
 #pragma unroll
-    for (int k = 0; k < 2 * M * NCMAX; ++k) acc[k] = R(0);
+    for (int k = 0; k < K; ++k) acc[k] = R(0);
     for (int t = tid; t < T; t += nthreads) {
-      R h[NMAX];
+      R h[NT];
 #pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < N) {
+      for (int k = 0; k < NT; ++k) {
+        if (FFCA_NK(k)) {
           R v = Hs[k * T + t];
           if (apply_hs) {
             v *= hs[k];
@@ -550,16 +611,16 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       for (int m = 0; m < M; ++m) {
         R lh = eps;
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
-          if (k < N) lh += Lr[m + k * M] * h[k];
-        const R il = rcp(lh);
+        for (int k = 0; k < NT; ++k)
+          if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
+        const R il = rcp_fast(lh);
         const R ul2 = u[m] * il * il;
 #pragma unroll
         for (int c = 0; c < NCMAX; ++c) {
           if (c < ncnt) {
             R hn = R(0);
 #pragma unroll
-            for (int k = 0; k < NMAX; ++k)
+            for (int k = 0; k < NT; ++k)
               if (k == n0 + c) hn = h[k];
             acc[(c * M + m) * 2 + 0] += ul2 * hn;
             acc[(c * M + m) * 2 + 1] += il * hn;
@@ -567,18 +628,26 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
         }
       }
     }
-    block_reduce<2 * M * NCMAX>(acc, 2 * M * ncnt, red, res, nwarps);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k < 2 * M * ncnt) {
+        const R s = warp_sum(acc[k]);
+        if (lane == 0) red[warp * K + k] = double(s);
+      }
+    }
+    __syncthreads();
+    gather(K, 2 * M * ncnt);
   };
 
   auto mm_h_sweep = [&](bool compute_u, bool apply_hs) {
-    R acc[NMAX];
+    R acc[NT];
 #pragma unroll
-    for (int k = 0; k < NMAX; ++k) acc[k] = R(0);
+    for (int k = 0; k < NT; ++k) acc[k] = R(0);
     for (int t = tid; t < T; t += nthreads) {
-      R h[NMAX];
+      R h[NT];
 #pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < N) {
+      for (int k = 0; k < NT; ++k) {
+        if (FFCA_NK(k)) {
           R v = Hs[k * T + t];
           if (apply_hs) v *= hs[k];
           h[k] = v;
@@ -608,14 +677,14 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
       for (int m = 0; m < M; ++m) {
         R lh = eps;
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k)
-          if (k < N) lh += Lr[m + k * M] * h[k];
-        il[m] = rcp(lh);
+        for (int k = 0; k < NT; ++k)
+          if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
+        il[m] = rcp_fast(lh);
         ul2[m] = u[m] * il[m] * il[m];
       }
 #pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < N) {
+      for (int k = 0; k < NT; ++k) {
+        if (FFCA_NK(k)) {
           R num = R(0), den = R(0);
 #pragma unroll
           for (int m = 0; m < M; ++m) {
@@ -630,7 +699,15 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
         }
       }
     }
-    block_reduce<NMAX>(acc, N, red, res, nwarps);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      if (FFCA_NK(k)) {
+        const R s = warp_sum(acc[k]);
+        if (lane == 0) red[warp * NT + k] = double(s);
+      }
+    }
+    __syncthreads();
+    gather(NT, N);
   };
 
   // -------------------------------------------------------------- driver --
@@ -655,33 +732,30 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
         for (int t = 0; t < p.iters; ++t)
           p.nll[size_t(t + 1) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
+    if (!sc->stop && p.iters > 0) {
+      // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
+      int bad = -1;
+      if (!ip_update<M>(Wd, res, T, p.seed, bin_index, reinterpret_cast<Mt19937_64*>(red), bad)) {
+        sc->status = kStatusIpSingular | (bad << 8);
+        sc->stop = 1;
+      }
+#pragma unroll
+      for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+    }
   }
   __syncthreads();
   if (!sc->stop) {
     for (int it = 0; it < p.iters; ++it) {
-      // ---- IP sweep over the columns of W (fastfca.cpp:36-72)
-      if (tid == 0) {
-        int bad = -1;
-        if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)it, bin_index,
-                           reinterpret_cast<Mt19937_64*>(red), bad)) {
-          sc->status = kStatusIpSingular | (bad << 8);
-          sc->stop = 1;
-        }
-      }
-      __syncthreads();
-      if (sc->stop) break;
-      for (int k = tid; k < M * M; k += nthreads) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
-      for (int k = tid; k < M; k += nthreads) us[k] = R(1);
-      __syncthreads();
-      // ---- L/H updates
+      // ---- L/H updates (the IP sweep of this iteration already ran)
       if (p.flavor == 0) {
         for (int n = 0; n <= N; ++n) {
           em_sweep(n, n == 0);
           if (tid == 0) {
             if (n == 0)
-              for (int k = 0; k < NMAX; ++k) hs[k] = R(1);
+              for (int k = 0; k < NT; ++k) hs[k] = R(1);
             if (n >= 1) hsumv[n - 1] = res[M];
             if (n < N) {
+#pragma unroll
               for (int m = 0; m < M; ++m) {
                 Lold[m] = Lr[m + n * M];
                 if (update_loading) {
@@ -689,7 +763,7 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
                   Ld[m + n * M] = l;
                   Lr[m + n * M] = narrow_pos<R>(l);
                 }
-                Linv[m] = rcp(Lr[m + n * M]);
+                Linv[m] = rcp_fast(Lr[m + n * M]);
               }
             }
           }
@@ -703,44 +777,46 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
             mm_l_sweep(n0, cnt, first, first);
             if (tid == 0) {
               if (first)
-                for (int k = 0; k < NMAX; ++k) hs[k] = R(1);
+                for (int k = 0; k < NT; ++k) hs[k] = R(1);
               for (int c = 0; c < cnt; ++c)
                 for (int m = 0; m < M; ++m) {
                   numd[m + (n0 + c) * M] = res[(c * M + m) * 2 + 0];
                   dend[m + (n0 + c) * M] = res[(c * M + m) * 2 + 1];
                 }
+              if (n0 + cnt >= N) {
+                for (int k = 0; k < M * N; ++k) {
+                  const double den = fmax(dend[k], 1e-300);
+                  const double l = fmax(Ld[k] * sqrt(numd[k] / den), 1e-300);  // :107-109
+                  Ld[k] = l;
+                  Lr[k] = narrow_pos<R>(l);
+                }
+              }
             }
             __syncthreads();
             first = false;
           }
-          if (tid == 0) {
-            for (int k = 0; k < M * N; ++k) {
-              const double den = fmax(dend[k], 1e-300);
-              const double l = fmax(Ld[k] * sqrt(numd[k] / den), 1e-300);  // :107-109
-              Ld[k] = l;
-              Lr[k] = narrow_pos<R>(l);
-            }
-          }
-          __syncthreads();
         }
         mm_h_sweep(first, first);
         if (tid == 0) {
           if (first)
-            for (int k = 0; k < NMAX; ++k) hs[k] = R(1);
+            for (int k = 0; k < NT; ++k) hs[k] = R(1);
           for (int k = 0; k < N; ++k) hsumv[k] = res[k];
         }
         __syncthreads();
       }
-      // ---- balance_scales (fastfca.cpp:127-142) + log|det W|^2 for the trace
+      // ---- one serial section: balance_scales (fastfca.cpp:127-142),
+      //      log|det W|^2 for the trace, and the R copies of W and L.
       if (tid == 0) {
         if (p.normalize && update_loading) {
           for (int n = 0; n < N; ++n) {
             const double mu = hsumv[n] / double(T);
             if (mu > 0.0 && isfinite(mu)) {
               hs[n] = R(1.0 / mu);
+#pragma unroll
               for (int m = 0; m < M; ++m) Ld[m + n * M] *= mu;
             }
           }
+#pragma unroll
           for (int m = 0; m < M; ++m) {
             double s = 0.0;
             for (int n = 0; n < N; ++n) s += Ld[m + n * M];
@@ -748,6 +824,7 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
             if (s > 0.0 && isfinite(s)) {
               for (int n = 0; n < N; ++n) Ld[m + n * M] /= s;
               const double r = 1.0 / sqrt(s);
+#pragma unroll
               for (int c = 0; c < M; ++c) {
                 Wd[c + m * M].x *= r;
                 Wd[c + m * M].y *= r;
@@ -764,23 +841,39 @@ __global__ void __launch_bounds__(256, (M <= 3) ? 3 : (M == 4 ? 2 : 1)) fit_kern
           }
           sc->logdet = ld;
         }
+        for (int k = 0; k < M * N; ++k) Lr[k] = narrow_pos<R>(Ld[k]);
+#pragma unroll
+        for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
       }
-      __syncthreads();
-      for (int k = tid; k < M * N; k += nthreads) {
-        Lr[k] = narrow_pos<R>(Ld[k]);
-      }
-      for (int k = tid; k < M * M; k += nthreads) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
       __syncthreads();
       if (sc->stop) break;
       const bool more = it + 1 < p.iters;
       if (more || record) {
         pass_a(false, more, record);
-        if (tid == 0 && record)
-          p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
-              -double(T) * sc->logdet + res[M * M * M];
+        if (tid == 0) {
+          if (record)
+            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
+                -double(T) * sc->logdet + res[M * M * M];
+          if (more) {
+            // Next iteration's IP sweep, fused into the pass-A serial section.
+#pragma unroll
+            for (int m = 0; m < M; ++m) us[m] = R(1);
+            int bad = -1;
+            if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)(it + 1), bin_index,
+                              reinterpret_cast<Mt19937_64*>(red), bad)) {
+              sc->status = kStatusIpSingular | (bad << 8);
+              sc->stop = 1;
+            }
+#pragma unroll
+            for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+          }
+        }
+        __syncthreads();
+        if (sc->stop) break;
       }
     }
   }
+#undef FFCA_NK
   __syncthreads();
   // ------------------------------------------------------------- epilogue --
   for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
