@@ -210,8 +210,9 @@ def main() -> None:
     fp64 = args.precision == "fp64"
     cdt = torch.complex128 if fp64 else torch.complex64
     rdt = torch.float64 if fp64 else torch.float32
-    x_d = torch.from_numpy(x).to(dev, cdt).contiguous()                     # [P, M, T]
-    H_init = torch.from_numpy(H0).to(dev, rdt).contiguous()                 # [P, N, T]
+    # Device layouts are the reference's per-bin order: x [P, T, M], H [P, T, N].
+    x_d = torch.from_numpy(np.ascontiguousarray(np.swapaxes(x, -1, -2))).to(dev, cdt).contiguous()
+    H_init = torch.from_numpy(np.ascontiguousarray(np.swapaxes(H0, -1, -2))).to(dev, rdt).contiguous()
     W_init = torch.from_numpy(np.ascontiguousarray(np.swapaxes(W0, -1, -2))).to(dev)  # col-major
     L_init = torch.from_numpy(np.ascontiguousarray(np.swapaxes(L0, -1, -2))).to(dev)
     H_d, W_d, L_d = H_init.clone(), W_init.clone(), L_init.clone()

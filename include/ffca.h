@@ -103,26 +103,28 @@ int ffca_power_scale(ffca_ctx* ctx, const ffca_dims* dims, const double* x, doub
 
 /* ---- device-resident entry points (inputs already in HBM; used for the
  * frequency-sharded multi-GPU path and the device-timed benchmark) ----
- * x_soa  : [P][dim][frames] complex64 (fp32) or complex128 (fp64), t fastest
- * H_soa  : [P][sources][frames] fp32 / fp64, in/out
+ * Device layouts keep the reference's per-bin (frame-major) order, so the
+ * boundary only converts precision:
+ * x_dev  : [P][frames][dim] complex64 (fp32) or complex128 (fp64)
+ * H_dev  : [P][frames][sources] fp32 / fp64, in/out
  * W, L   : [P][dim*dim] complex128, [P][dim*sources] fp64, in/out
  * power  : [P] fp64;  nll_slots: [(iters+1)][P] fp64 or NULL;  status: [P]
  * P = batch*bins problems; prob_offset = global index of problem 0 (only the
  * restart seed uses it: bin index i = (prob_offset + p) % bins_per_mixture).
  * stream: a cudaStream_t (NULL = the context's stream).  Asynchronous. */
 int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset, int dim,
-                    int sources, int frames, const ffca_fit_opts* opts, const void* x_soa,
-                    const double* power, double* W, double* L, void* H_soa, double* nll_slots,
+                    int sources, int frames, const ffca_fit_opts* opts, const void* x_dev,
+                    const double* power, double* W, double* L, void* H_dev, double* nll_slots,
                     int32_t* status, void* stream);
 
-/* images_soa: [sources][P][dim][frames] complex64 / complex128. */
+/* images_dev: [sources][P][frames][dim] complex64 / complex128. */
 int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int frames,
-                         int precision, const void* x_soa, const double* W, const double* L,
-                         const void* H_soa, void* images_soa, void* stream);
+                         int precision, const void* x_dev, const double* W, const double* L,
+                         const void* H_dev, void* images_dev, void* stream);
 
-/* power_scale from SoA complex64/complex128 x: out [P]. */
+/* power_scale from device x (complex64/complex128, [P][frames][dim]): out [P]. */
 int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, int precision,
-                            const void* x_soa, double* out, void* stream);
+                            const void* x_dev, double* out, void* stream);
 
 /* Number of kernels the last call on this context launched (bench evidence). */
 int ffca_last_launch_count(const ffca_ctx* ctx);

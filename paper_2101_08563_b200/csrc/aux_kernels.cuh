@@ -1,85 +1,42 @@
-// aux_kernels.cuh -- layout conversion at the boundary, per-bin power and the
+// aux_kernels.cuh -- boundary precision conversion, per-bin power and the
 // decomposed multichannel Wiener filter output kernel.
+//
+// Device layouts are the reference containers' per-bin order (frame-major):
+// x [p][t][m] complex, H [p][t][n] real, images [n][p][t][m] complex.  The
+// boundary only converts precision (fp64 host buffers -> fp32 compute path).
 #pragma once
 
 #include "common.cuh"
 
 namespace ffca {
 
-// ------------------------------------------------------------------ layout --
-// Reference Spectrogram::f[i] is dim x frames column-major complex<double>,
-// i.e. [p][t][m] (re, im).  The kernels read SoA [p][m][t] in the compute type
-// so that consecutive threads (frames) touch consecutive addresses.
-template <typename R>
-__global__ void pack_x_kernel(const double2* __restrict__ in, cplx_t<R>* __restrict__ out, int P,
-                              int M, int T) {
-  const size_t n = size_t(P) * T;
+// ------------------------------------------------------------ conversion --
+template <typename Src, typename Dst>
+__global__ void convert_kernel(const Src* __restrict__ in, Dst* __restrict__ out, size_t n) {
   for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n;
-       k += size_t(gridDim.x) * blockDim.x) {
-    const size_t p = k / T, t = k - p * T;
-    const double2* src = in + k * M;
-    cplx_t<R>* dst = out + p * M * T + t;
-    for (int m = 0; m < M; ++m) {
-      const double2 v = src[m];
-      dst[size_t(m) * T] = mkc<R>(R(v.x), R(v.y));
-    }
-  }
+       k += size_t(gridDim.x) * blockDim.x)
+    out[k] = Dst(in[k]);
 }
 
-// H(n, j) at n + j*N per problem  ->  [p][n][t]
-template <typename R>
-__global__ void pack_h_kernel(const double* __restrict__ in, R* __restrict__ out, int P, int N,
-                              int T) {
-  const size_t n = size_t(P) * T;
-  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n;
-       k += size_t(gridDim.x) * blockDim.x) {
-    const size_t p = k / T, t = k - p * T;
-    const double* src = in + k * N;
-    R* dst = out + p * N * T + t;
-    for (int s = 0; s < N; ++s) dst[size_t(s) * T] = R(src[s]);
-  }
-}
-
-// Inverse of pack_h; problems whose status is not OK keep the staged init.
+// Compute type -> fp64 for the fitted H; problems whose status is not OK keep
+// the staged fp64 init (silent bands return the init bit-exactly).
 template <typename R>
 __global__ void unpack_h_kernel(const R* __restrict__ in, double* __restrict__ out,
-                                const int* __restrict__ status, int P, int N, int T) {
-  const size_t n = size_t(P) * T;
+                                const int* __restrict__ status, size_t per_problem, size_t n) {
   for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n;
        k += size_t(gridDim.x) * blockDim.x) {
-    const size_t p = k / T, t = k - p * T;
-    if (status[p] != 0) continue;
-    const R* src = in + p * N * T + t;
-    double* dst = out + k * N;
-    for (int s = 0; s < N; ++s) dst[s] = double(src[size_t(s) * T]);
+    if (status[k / per_problem] != 0) continue;
+    out[k] = double(in[k]);
   }
 }
 
-// SampleCovSet::power_scale (sigmodel.cpp:43-44) from the AoS double input:
-// sum_j tr(x_j x_j^H) / (T * M), one CTA per problem, fixed-order reduction.
-__global__ void power_aos_kernel(const double2* __restrict__ x, double* __restrict__ out, int M,
-                                 int T) {
+// SampleCovSet::power_scale (sigmodel.cpp:43-44): sum_j tr(x_j x_j^H) / (T M),
+// one CTA per problem, fixed-order reduction.
+template <typename C>
+__global__ void power_kernel(const C* __restrict__ x, double* __restrict__ out, int M, int T) {
   __shared__ double red[32];
   const int p = blockIdx.x;
-  const double2* xp = x + size_t(p) * T * M;
-  double s = 0.0;
-  for (int k = threadIdx.x; k < T * M; k += blockDim.x) s += cabs2(xp[k]);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) tot += red[w];
-    out[p] = tot / (double(T) * M);
-  }
-}
-
-template <typename R>
-__global__ void power_soa_kernel(const cplx_t<R>* __restrict__ x, double* __restrict__ out, int M,
-                                 int T) {
-  __shared__ double red[32];
-  const int p = blockIdx.x;
-  const cplx_t<R>* xp = x + size_t(p) * T * M;
+  const C* xp = x + size_t(p) * T * M;
   double s = 0.0;
   for (int k = threadIdx.x; k < T * M; k += blockDim.x) s += double(cabs2(xp[k]));
   s = warp_sum(s);
@@ -95,16 +52,15 @@ __global__ void power_soa_kernel(const cplx_t<R>* __restrict__ x, double* __rest
 // ------------------------------------------------------------ separation --
 // fastfca_separate (fastfca.cpp:205-223): y = W^H x; per source
 // g_n = L_n H_n / floor_positive(L H) (source_gain :74-78, sigmodel.cpp:10-15,
-// no eps); c_n = (W^H)^{-1} (g_n .* y).  One CTA per problem.
-//   out_aos: images[n][p][t][m] complex<double> (reference layout), or
-//   out_soa: images[n][p][m][t] in the compute type (device path).
-template <int M, typename R>
+// no eps); c_n = (W^H)^{-1} (g_n .* y).  One CTA per problem; the output is
+// the reference layout images[n][p][t][m] in fp64 (host path) or in the
+// compute type (device path).
+template <int M, typename R, typename OutC>
 __global__ void __launch_bounds__(256) separate_kernel(const cplx_t<R>* __restrict__ x,
                                                        const double2* __restrict__ W,
                                                        const double* __restrict__ L,
                                                        const R* __restrict__ H, int P, int N,
-                                                       int T, double2* __restrict__ out_aos,
-                                                       cplx_t<R>* __restrict__ out_soa) {
+                                                       int T, OutC* __restrict__ out) {
   using C = cplx_t<R>;
   __shared__ C wr[M * M];
   __shared__ C ainv[M * M];
@@ -120,7 +76,7 @@ __global__ void __launch_bounds__(256) separate_kernel(const cplx_t<R>* __restri
     wr[k] = mkc<R>(R(w.x), R(w.y));
   }
   if (tid == 0) {
-    // (W^H)^{-1} in fp64 via Gauss-Jordan with partial pivoting.
+    // (W^H)^{-1} in fp64 by Gauss-Jordan with partial pivoting.
     double2 a[M * M], inv[M * M];
     for (int r = 0; r < M; ++r)
       for (int c = 0; c < M; ++c) {
@@ -130,9 +86,9 @@ __global__ void __launch_bounds__(256) separate_kernel(const cplx_t<R>* __restri
       }
     for (int k = 0; k < M; ++k) {
       int piv = k;
-      double best = cabs(a[k + k * M]);
+      double best = cabs2(a[k + k * M]);
       for (int r = k + 1; r < M; ++r) {
-        const double v = cabs(a[r + k * M]);
+        const double v = cabs2(a[r + k * M]);
         if (v > best) best = v, piv = r;
       }
       if (piv != k)
@@ -159,12 +115,15 @@ __global__ void __launch_bounds__(256) separate_kernel(const cplx_t<R>* __restri
   __syncthreads();
   // floor_positive: rel 1e-12 of the mean of L H over the bin.
   double s = 0.0;
-  for (int t = tid; t < T; t += blockDim.x)
+  for (int t = tid; t < T; t += blockDim.x) {
+    R ssum = R(0);
     for (int m = 0; m < M; ++m) {
       R lh = R(0);
-      for (int n = 0; n < N; ++n) lh += lr[m + n * M] * hp[size_t(n) * T + t];
-      s += double(lh);
+      for (int n = 0; n < N; ++n) lh += lr[m + n * M] * hp[size_t(t) * N + n];
+      ssum += lh;
     }
+    s += double(ssum);
+  }
   s = warp_sum(s);
   if ((tid & 31) == 0) red[tid >> 5] = s;
   __syncthreads();
@@ -180,29 +139,37 @@ __global__ void __launch_bounds__(256) separate_kernel(const cplx_t<R>* __restri
   for (int t = tid; t < T; t += blockDim.x) {
     C xv[M], y[M];
     R lh[M];
-    for (int m = 0; m < M; ++m) xv[m] = xp[size_t(m) * T + t];
+    R hv[16];
+    for (int n = 0; n < N; ++n) hv[n] = hp[size_t(t) * N + n];
+#pragma unroll
+    for (int m = 0; m < M; ++m) xv[m] = xp[size_t(t) * M + m];
+#pragma unroll
     for (int m = 0; m < M; ++m) {
       C acc = mkc<R>(R(0), R(0));
+#pragma unroll
       for (int c = 0; c < M; ++c) acc = cadd(acc, cmulc(wr[c + m * M], xv[c]));
       y[m] = acc;
       R v = R(0);
-      for (int n = 0; n < N; ++n) v += lr[m + n * M] * hp[size_t(n) * T + t];
+      for (int n = 0; n < N; ++n) v += lr[m + n * M] * hv[n];
       lh[m] = v > fl ? v : fl;
     }
     for (int n = 0; n < N; ++n) {
-      const R hn = hp[size_t(n) * T + t];
       C z[M];
+#pragma unroll
       for (int m = 0; m < M; ++m) {
-        const R g = (lr[m + n * M] * hn) / lh[m];
+        const R g = (lr[m + n * M] * hv[n]) / lh[m];
         z[m] = mkc<R>(g * y[m].x, g * y[m].y);
       }
+      OutC* o = out + ((size_t(n) * P + p) * T + t) * M;
+#pragma unroll
       for (int r = 0; r < M; ++r) {
         C c = mkc<R>(R(0), R(0));
+#pragma unroll
         for (int k = 0; k < M; ++k) c = cadd(c, cmul(ainv[r + k * M], z[k]));
-        if (out_aos)
-          out_aos[((size_t(n) * P + p) * T + t) * M + r] = make_double2(double(c.x), double(c.y));
-        else
-          out_soa[((size_t(n) * P + p) * M + r) * T + t] = c;
+        OutC v;
+        v.x = c.x;
+        v.y = c.y;
+        o[r] = v;
       }
     }
   }

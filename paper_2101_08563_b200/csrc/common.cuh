@@ -156,3 +156,8 @@ __device__ __forceinline__ float rcp_fast(float a) {
 }
 __device__ __forceinline__ double rcp_fast(double a) { return 1.0 / a; }
 }  // namespace ffca
+
+namespace ffca {
+__device__ __forceinline__ float flog2(float a) { return __log2f(a); }
+__device__ __forceinline__ double flog2(double a) { return log2(a); }
+}  // namespace ffca

@@ -1,6 +1,6 @@
-// ffca_capi.cu -- the C ABI (include/ffca.h): validation, device buffers,
-// boundary layout conversion and kernel dispatch.  No CPU compute path: every
-// entry point either runs the sm_100a kernels or returns an error.
+// ffca_api.cu -- the C ABI (include/ffca.h): validation, device buffers,
+// boundary precision conversion and kernel dispatch.  No CPU compute path:
+// every entry point either runs the sm_100a kernels or returns an error.
 
 #include <cuda_runtime.h>
 
@@ -9,8 +9,8 @@
 #include <string>
 #include <vector>
 
-#include "internal.hpp"
 #include "aux_kernels.cuh"
+#include "internal.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -21,16 +21,7 @@ int ffca_set_err(int code, const std::string& msg) {
   return code;
 }
 
-using ffca::kX;
-using ffca::kXs;
-using ffca::kH;
-using ffca::kHs;
-using ffca::kW;
-using ffca::kL;
-using ffca::kPow;
-using ffca::kNll;
-using ffca::kStat;
-using ffca::kImg;
+using namespace ffca;
 
 namespace {
 
@@ -47,11 +38,12 @@ struct DeviceGuard {
   }
 };
 
-int check_dims(int problems, int dim, int sources, int frames) {
+int check_dims(long long problems, int dim, int sources, int frames) {
   if (problems < 1 || frames < 1 || dim < 1 || sources < 1)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca: empty shape (sample_covs: empty spectrogram)");
   if (dim > 8) return set_err(FFCA_INVALID_ARGUMENT, "ffca: dim > 8 is not supported");
   if (sources > 16) return set_err(FFCA_INVALID_ARGUMENT, "ffca: sources > 16 is not supported");
+  if (problems > (1LL << 31) - 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca: too many problems");
   return FFCA_OK;
 }
 
@@ -63,75 +55,77 @@ int grid_for(size_t n, int threads) {
 }
 
 template <typename R>
-int launch_fit(ffca_ctx* ctx, int M, ffca::FitParams& fp, cudaStream_t st) {
+int launch_fit(ffca_ctx* ctx, int M, FitParams& fp, cudaStream_t st) {
   const bool fp64 = sizeof(R) == 8;
   switch (M) {
-    case 1: return ffca::launch_fit_m1(ctx, fp, st, fp64);
-    case 2: return ffca::launch_fit_m2(ctx, fp, st, fp64);
-    case 3: return ffca::launch_fit_m3(ctx, fp, st, fp64);
-    case 4: return ffca::launch_fit_m4(ctx, fp, st, fp64);
-    case 5: return ffca::launch_fit_m5(ctx, fp, st, fp64);
-    case 6: return ffca::launch_fit_m6(ctx, fp, st, fp64);
-    case 7: return ffca::launch_fit_m7(ctx, fp, st, fp64);
-    case 8: return ffca::launch_fit_m8(ctx, fp, st, fp64);
+    case 1: return launch_fit_m1(ctx, fp, st, fp64);
+    case 2: return launch_fit_m2(ctx, fp, st, fp64);
+    case 3: return launch_fit_m3(ctx, fp, st, fp64);
+    case 4: return launch_fit_m4(ctx, fp, st, fp64);
+    case 5: return launch_fit_m5(ctx, fp, st, fp64);
+    case 6: return launch_fit_m6(ctx, fp, st, fp64);
+    case 7: return launch_fit_m7(ctx, fp, st, fp64);
+    case 8: return launch_fit_m8(ctx, fp, st, fp64);
   }
   return set_err(FFCA_INVALID_ARGUMENT, "ffca: unsupported dim");
 }
 
-template <int M, typename R>
+template <int M, typename R, typename OutC>
 int launch_sep_m(ffca_ctx* ctx, const void* xs, const double* W, const double* L, const void* Hs,
-                 int P, int N, int T, double* out_aos, void* out_soa, cudaStream_t st) {
-  using C = ffca::cplx_t<R>;
-  ffca::separate_kernel<M, R><<<P, 256, 0, st>>>(
+                 int P, int N, int T, OutC* out, cudaStream_t st) {
+  using C = cplx_t<R>;
+  separate_kernel<M, R, OutC><<<P, 256, 0, st>>>(
       reinterpret_cast<const C*>(xs), reinterpret_cast<const double2*>(W), L,
-      reinterpret_cast<const R*>(Hs), P, N, T, reinterpret_cast<double2*>(out_aos),
-      reinterpret_cast<C*>(out_soa));
+      reinterpret_cast<const R*>(Hs), P, N, T, out);
   ctx->launches++;
   FFCA_CUDA(cudaGetLastError());
   return FFCA_OK;
 }
 
-template <typename R>
+template <typename R, typename OutC>
 int launch_sep(ffca_ctx* ctx, int M, const void* xs, const double* W, const double* L,
-               const void* Hs, int P, int N, int T, double* out_aos, void* out_soa,
-               cudaStream_t st) {
+               const void* Hs, int P, int N, int T, OutC* out, cudaStream_t st) {
   switch (M) {
-    case 1: return launch_sep_m<1, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 2: return launch_sep_m<2, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 3: return launch_sep_m<3, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 4: return launch_sep_m<4, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 5: return launch_sep_m<5, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 6: return launch_sep_m<6, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 7: return launch_sep_m<7, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
-    case 8: return launch_sep_m<8, R>(ctx, xs, W, L, Hs, P, N, T, out_aos, out_soa, st);
+    case 1: return launch_sep_m<1, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 2: return launch_sep_m<2, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 3: return launch_sep_m<3, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 4: return launch_sep_m<4, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 5: return launch_sep_m<5, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 6: return launch_sep_m<6, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 7: return launch_sep_m<7, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
+    case 8: return launch_sep_m<8, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
   }
   return set_err(FFCA_INVALID_ARGUMENT, "ffca: unsupported dim");
 }
 
+// Stage host fp64 x and H on the device and convert them to the compute type.
+// x keeps its fp64 staging copy in slot kX (power_scale reads it).
 template <typename R>
-int pack_inputs(ffca_ctx* ctx, int P, int M, int N, int T, const double* x, const double* H,
-                void** xs_out, void** hs_out, double** hdbl_out, cudaStream_t st) {
-  using C = ffca::cplx_t<R>;
+int stage_inputs(ffca_ctx* ctx, size_t P, int M, int N, int T, const double* x, const double* H,
+                 void** xs_out, void** hs_out, double** hdbl_out, cudaStream_t st) {
   cudaError_t err;
-  const size_t nx = size_t(P) * T * M, nh = size_t(P) * T * N;
+  const size_t nx = P * T * M * 2, nh = P * T * N;
   if (x) {
-    void* dx = ctx->get(kX, nx * 16, &err);
-    void* xs = ctx->get(kXs, nx * sizeof(C), &err);
-    if (!dx || !xs) return set_err(FFCA_CUDA_ERROR, "ffca: x alloc failed");
-    FFCA_CUDA(cudaMemcpyAsync(dx, x, nx * 16, cudaMemcpyHostToDevice, st));
-    ffca::pack_x_kernel<R><<<grid_for(size_t(P) * T, 256), 256, 0, st>>>(
-        reinterpret_cast<const double2*>(dx), reinterpret_cast<C*>(xs), P, M, T);
-    ctx->launches++;
-    FFCA_CUDA(cudaGetLastError());
-    *xs_out = xs;
+    double* dx = static_cast<double*>(ctx->get(kX, nx * 8, &err));
+    if (!dx) return set_err(FFCA_CUDA_ERROR, "ffca: x alloc failed");
+    FFCA_CUDA(cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, st));
+    if (sizeof(R) == 8) {
+      *xs_out = dx;
+    } else {
+      void* xs = ctx->get(kXs, nx * sizeof(R), &err);
+      if (!xs) return set_err(FFCA_CUDA_ERROR, "ffca: x alloc failed");
+      convert_kernel<double, R><<<grid_for(nx, 256), 256, 0, st>>>(dx, static_cast<R*>(xs), nx);
+      ctx->launches++;
+      FFCA_CUDA(cudaGetLastError());
+      *xs_out = xs;
+    }
   }
   if (H) {
     double* dh = static_cast<double*>(ctx->get(kH, nh * 8, &err));
     void* hs = ctx->get(kHs, nh * sizeof(R), &err);
     if (!dh || !hs) return set_err(FFCA_CUDA_ERROR, "ffca: H alloc failed");
     FFCA_CUDA(cudaMemcpyAsync(dh, H, nh * 8, cudaMemcpyHostToDevice, st));
-    ffca::pack_h_kernel<R><<<grid_for(size_t(P) * T, 256), 256, 0, st>>>(
-        dh, reinterpret_cast<R*>(hs), P, N, T);
+    convert_kernel<double, R><<<grid_for(nh, 256), 256, 0, st>>>(dh, static_cast<R*>(hs), nh);
     ctx->launches++;
     FFCA_CUDA(cudaGetLastError());
     *hs_out = hs;
@@ -150,7 +144,7 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   void* xs = nullptr;
   void* hs = nullptr;
   double* hd = nullptr;
-  int rc = pack_inputs<R>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st);
+  int rc = stage_inputs<R>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st);
   if (rc) return rc;
   double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
   double* dL = static_cast<double*>(ctx->get(kL, size_t(P) * M * N * 8, &err));
@@ -165,12 +159,12 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   if (power) {
     FFCA_CUDA(cudaMemcpyAsync(dpow, power, size_t(P) * 8, cudaMemcpyHostToDevice, st));
   } else {
-    ffca::power_aos_kernel<<<P, 256, 0, st>>>(
-        reinterpret_cast<const double2*>(ctx->bufs[kX].p), dpow, M, T);
+    power_kernel<double2><<<P, 256, 0, st>>>(static_cast<const double2*>(ctx->bufs[kX].p), dpow,
+                                             M, T);
     ctx->launches++;
     FFCA_CUDA(cudaGetLastError());
   }
-  ffca::FitParams fp{};
+  FitParams fp{};
   fp.nprob = P;
   fp.N = N;
   fp.T = T;
@@ -202,18 +196,19 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   FFCA_CUDA(cudaStreamSynchronize(st));
   for (int p = 0; p < P; ++p) {
     const int s = stat[p] & 0xff;
-    if (s == ffca::kStatusIpSingular)
+    if (s == kStatusIpSingular)
       return set_err(FFCA_NUMERICAL, "ip_update_w: singular system for column " +
                                          std::to_string(stat[p] >> 8));
-    if (s == ffca::kStatusSingularW) return set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
+    if (s == kStatusSingularW) return set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
   }
   if (bin_status) std::memcpy(bin_status, stat.data(), size_t(P) * 4);
   if (iters > 0) {
-    ffca::unpack_h_kernel<R><<<grid_for(size_t(P) * T, 256), 256, 0, st>>>(
-        reinterpret_cast<const R*>(hs), hd, dstat, P, N, T);
+    const size_t nh = size_t(P) * T * N;
+    unpack_h_kernel<R><<<grid_for(nh, 256), 256, 0, st>>>(static_cast<const R*>(hs), hd, dstat,
+                                                          size_t(T) * N, nh);
     ctx->launches++;
     FFCA_CUDA(cudaGetLastError());
-    FFCA_CUDA(cudaMemcpyAsync(H, hd, size_t(P) * T * N * 8, cudaMemcpyDeviceToHost, st));
+    FFCA_CUDA(cudaMemcpyAsync(H, hd, nh * 8, cudaMemcpyDeviceToHost, st));
     FFCA_CUDA(cudaMemcpyAsync(W, dW, size_t(P) * M * M * 16, cudaMemcpyDeviceToHost, st));
     FFCA_CUDA(cudaMemcpyAsync(L, dL, size_t(P) * M * N * 8, cudaMemcpyDeviceToHost, st));
     FFCA_CUDA(cudaStreamSynchronize(st));
@@ -237,7 +232,7 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
 
 extern "C" {
 
-int ffca_version(void) { return 1; }
+int ffca_version(void) { return 2; }
 
 const char* ffca_last_error(void) { return g_err.c_str(); }
 
@@ -286,9 +281,9 @@ int ffca_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status) {
   if (!ctx || !d || !o) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: null argument");
-  int rc = check_dims(d->batch * d->bins, d->dim, d->sources, d->frames);
-  if (rc) return rc;
   if (d->batch < 1 || d->bins < 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: empty shape");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
+  if (rc) return rc;
   if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
   if (o->flavor != FFCA_FLAVOR_EM && o->flavor != FFCA_FLAVOR_MM)
     return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: unknown flavor");
@@ -310,7 +305,7 @@ int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
                   const double* W, const double* L, const double* H, double* out) {
   if (!ctx || !d || !x || !W || !L || !H || !out)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_nll_bins: null argument");
-  int rc = check_dims(d->batch * d->bins, d->dim, d->sources, d->frames);
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
   if (rc) return rc;
   const int P = d->batch * d->bins;
   // A zero-iteration fit records exactly slot 0 = fastfca_nll_freq at the
@@ -321,6 +316,8 @@ int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
   std::vector<double> slots(P);
   ffca_fit_opts o{FFCA_FLAVOR_EM, 0, 1, 0, 1, 0, precision};
   ffca_dims one = *d;
+  one.batch = 1;
+  one.bins = P;
   ctx->launches = 0;
   DeviceGuard g(ctx->device);
   rc = (precision == FFCA_PREC_FP64)
@@ -335,7 +332,8 @@ int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
 
 int ffca_power_scale(ffca_ctx* ctx, const ffca_dims* d, const double* x, double* out) {
   if (!ctx || !d || !x || !out) return set_err(FFCA_INVALID_ARGUMENT, "ffca_power_scale: null argument");
-  const int P = d->batch * d->bins, M = d->dim, T = d->frames;
+  const long long P = (long long)d->batch * d->bins;
+  const int M = d->dim, T = d->frames;
   if (P < 1 || M < 1 || T < 1) return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: empty spectrogram");
   DeviceGuard g(ctx->device);
   ctx->launches = 0;
@@ -344,7 +342,7 @@ int ffca_power_scale(ffca_ctx* ctx, const ffca_dims* d, const double* x, double*
   double* dp = static_cast<double*>(ctx->get(kPow, size_t(P) * 8, &err));
   if (!dx || !dp) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
   FFCA_CUDA(cudaMemcpyAsync(dx, x, size_t(P) * T * M * 16, cudaMemcpyHostToDevice, ctx->stream));
-  ffca::power_aos_kernel<<<P, 256, 0, ctx->stream>>>(reinterpret_cast<const double2*>(dx), dp, M, T);
+  power_kernel<double2><<<int(P), 256, 0, ctx->stream>>>(static_cast<const double2*>(dx), dp, M, T);
   ctx->launches++;
   FFCA_CUDA(cudaGetLastError());
   FFCA_CUDA(cudaMemcpyAsync(out, dp, size_t(P) * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -356,7 +354,7 @@ int ffca_separate(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
                   const double* W, const double* L, const double* H, double* images) {
   if (!ctx || !d || !x || !W || !L || !H || !images)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_separate: null argument");
-  int rc = check_dims(d->batch * d->bins, d->dim, d->sources, d->frames);
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
   if (rc) return rc;
   const int P = d->batch * d->bins, M = d->dim, N = d->sources, T = d->frames;
   DeviceGuard g(ctx->device);
@@ -366,19 +364,19 @@ int ffca_separate(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
   void* xs = nullptr;
   void* hs = nullptr;
   double* hd = nullptr;
-  rc = (precision == FFCA_PREC_FP64) ? pack_inputs<double>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st)
-                                     : pack_inputs<float>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st);
+  rc = (precision == FFCA_PREC_FP64) ? stage_inputs<double>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st)
+                                     : stage_inputs<float>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st);
   if (rc) return rc;
   double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
   double* dL = static_cast<double*>(ctx->get(kL, size_t(P) * M * N * 8, &err));
   const size_t nimg = size_t(N) * P * T * M;
-  double* dimg = static_cast<double*>(ctx->get(kImg, nimg * 16, &err));
+  double2* dimg = static_cast<double2*>(ctx->get(kImg, nimg * 16, &err));
   if (!dW || !dL || !dimg) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
   FFCA_CUDA(cudaMemcpyAsync(dW, W, size_t(P) * M * M * 16, cudaMemcpyHostToDevice, st));
   FFCA_CUDA(cudaMemcpyAsync(dL, L, size_t(P) * M * N * 8, cudaMemcpyHostToDevice, st));
   rc = (precision == FFCA_PREC_FP64)
-           ? launch_sep<double>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, nullptr, st)
-           : launch_sep<float>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, nullptr, st);
+           ? launch_sep<double>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, st)
+           : launch_sep<float>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, st);
   if (rc) return rc;
   FFCA_CUDA(cudaMemcpyAsync(images, dimg, nimg * 16, cudaMemcpyDeviceToHost, st));
   FFCA_CUDA(cudaStreamSynchronize(st));
@@ -386,27 +384,27 @@ int ffca_separate(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
 }
 
 int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset, int dim,
-                    int sources, int frames, const ffca_fit_opts* o, const void* x_soa,
-                    const double* power, double* W, double* L, void* H_soa, double* nll_slots,
+                    int sources, int frames, const ffca_fit_opts* o, const void* x_dev,
+                    const double* power, double* W, double* L, void* H_dev, double* nll_slots,
                     int32_t* status, void* stream) {
-  if (!ctx || !o || !x_soa || !power || !W || !L || !H_soa || !status)
+  if (!ctx || !o || !x_dev || !power || !W || !L || !H_dev || !status)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_device: null argument");
   int rc = check_dims(problems, dim, sources, frames);
   if (rc) return rc;
-  if (bins_per_mixture < 1 || o->iters < 0)
+  if (bins_per_mixture < 1 || o->iters < 0 || prob_offset < 0)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_device: bad arguments");
   if (o->record_trace && !nll_slots)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_device: record_trace needs nll_slots");
   DeviceGuard g(ctx->device);
   ctx->launches = 0;
-  ffca::FitParams fp{};
+  FitParams fp{};
   fp.nprob = problems;
   fp.N = sources;
   fp.T = frames;
   fp.F = bins_per_mixture;
   fp.prob_offset = prob_offset;
-  fp.x = x_soa;
-  fp.H = H_soa;
+  fp.x = x_dev;
+  fp.H = H_dev;
   fp.W = reinterpret_cast<double2*>(W);
   fp.L = L;
   fp.power = power;
@@ -425,9 +423,9 @@ int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_
 }
 
 int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int frames,
-                         int precision, const void* x_soa, const double* W, const double* L,
-                         const void* H_soa, void* images_soa, void* stream) {
-  if (!ctx || !x_soa || !W || !L || !H_soa || !images_soa)
+                         int precision, const void* x_dev, const double* W, const double* L,
+                         const void* H_dev, void* images_dev, void* stream) {
+  if (!ctx || !x_dev || !W || !L || !H_dev || !images_dev)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_separate_device: null argument");
   int rc = check_dims(problems, dim, sources, frames);
   if (rc) return rc;
@@ -435,26 +433,26 @@ int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int 
   ctx->launches = 0;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   return precision == FFCA_PREC_FP64
-             ? launch_sep<double>(ctx, dim, x_soa, W, L, H_soa, problems, sources, frames, nullptr,
-                                  images_soa, st)
-             : launch_sep<float>(ctx, dim, x_soa, W, L, H_soa, problems, sources, frames, nullptr,
-                                 images_soa, st);
+             ? launch_sep<double>(ctx, dim, x_dev, W, L, H_dev, problems, sources, frames,
+                                  static_cast<double2*>(images_dev), st)
+             : launch_sep<float>(ctx, dim, x_dev, W, L, H_dev, problems, sources, frames,
+                                 static_cast<float2*>(images_dev), st);
 }
 
 int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, int precision,
-                            const void* x_soa, double* out, void* stream) {
-  if (!ctx || !x_soa || !out) return set_err(FFCA_INVALID_ARGUMENT, "ffca_power_scale_device: null");
+                            const void* x_dev, double* out, void* stream) {
+  if (!ctx || !x_dev || !out) return set_err(FFCA_INVALID_ARGUMENT, "ffca_power_scale_device: null");
   if (problems < 1 || dim < 1 || frames < 1)
     return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: empty spectrogram");
   DeviceGuard g(ctx->device);
   ctx->launches = 0;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   if (precision == FFCA_PREC_FP64)
-    ffca::power_soa_kernel<double><<<problems, 256, 0, st>>>(
-        reinterpret_cast<const double2*>(x_soa), out, dim, frames);
+    power_kernel<double2><<<problems, 256, 0, st>>>(static_cast<const double2*>(x_dev), out, dim,
+                                                     frames);
   else
-    ffca::power_soa_kernel<float><<<problems, 256, 0, st>>>(
-        reinterpret_cast<const float2*>(x_soa), out, dim, frames);
+    power_kernel<float2><<<problems, 256, 0, st>>>(static_cast<const float2*>(x_dev), out, dim,
+                                                    frames);
   ctx->launches++;
   FFCA_CUDA(cudaGetLastError());
   return FFCA_OK;

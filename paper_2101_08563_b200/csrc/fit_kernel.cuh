@@ -3,25 +3,34 @@
 // One CTA owns one frequency problem (bin i of mixture b) for ALL iterations
 // of fastfca_fit (reference src/fastfca.cpp:158-184): the CTA grid replaces
 // parallel_for over bins (src/parallel.cpp:16-45).  When the per-bin working
-// set (x: M*T complex, H: N*T, U: M*T) fits in shared memory the CTA keeps it
-// on chip for the whole fit, so HBM sees x and H once; otherwise the same code
-// streams them from global memory (L2/HBM) and keeps U in a global scratch.
+// set fits in shared memory the CTA keeps it on chip for the whole fit, so HBM
+// sees x and H once; otherwise the same code streams it from global memory
+// (L2/HBM) with the per-frame scratch in a global buffer.
 //
-// Per iteration (fastfca.cpp:172-183), with T the frame count:
-//   pass A   one sweep over T: balance-pending scales, sigma^2 = L H + eps,
-//            the per-bin NLL of the previous iterate (sigmodel.cpp:155-162)
-//            and all M weighted covariances Q_m (fastfca.cpp:22-34), reduced
-//            once for the whole CTA.
+// Data layout (frame-major records, the reference's own per-bin order):
+//   x   [t][m]  complex   (Spectrogram::f[i] column-major, stft.hpp:21-29)
+//   H   [t][n]  real      (FastFcaParams::act[i] column-major, sigmodel.hpp:76)
+//   wk  [t][2M] real      U(m) = |w_m^H x_t|^2, then Phi(m) of the current source
+// so one thread reads a frame's record with a few vector loads.
+//
+// Per iteration (fastfca.cpp:172-183):
+//   pass A   sigma^2 = L H + eps; the per-bin NLL of the previous iterate
+//            (sigmodel.cpp:155-162) and all M weighted covariances Q_m
+//            (fastfca.cpp:22-34), one CTA reduction.
 //   IP       one thread, fp64 in registers: M sequential column solves with the
 //            residual check and the libstdc++-faithful seeded restart
 //            (fastfca.cpp:36-72).
-//   EM       N+1 sweeps: sweep n finishes source n-1's H row with the freshly
-//            reduced L column and accumulates source n's L reduction
-//            (em_update_lh, fastfca.cpp:80-99); sweep 0 also forms U = |W^H x|^2
-//            (sigmodel.cpp:93-107).
+//   EM       N+1 sweeps: sweep n stores U (n = 0), finishes source n-1's H row
+//            from the stored Phi and the freshly reduced L column, then forms
+//            Phi for source n and reduces its L column (em_update_lh,
+//            fastfca.cpp:80-99).
 //   MM       two sweeps (mm_update_lh, fastfca.cpp:101-117).
-//   balance  one thread on the reduced row means (fastfca.cpp:127-142); the H
-//            row scale is applied lazily by the next sweep that touches H.
+//   balance  one thread on the reduced row means (fastfca.cpp:127-142).  The H
+//            row scale 1/mu_n is kept as a per-source factor hsc[n] (H_true =
+//            H_stored * hsc) and folded into the effective loadings
+//            Le = L * hsc used by every product, so no sweep rescales H; the
+//            next H update stores true values and resets hsc[n] = 1.  The W
+//            column scale is folded the same way into the stored U (us[m]).
 // Every reduction is: warp shuffles -> per-warp partials in shared memory ->
 // barrier -> warp 0 sums the partials in a fixed order (fp64) -> lane 0 does
 // the serial update -> barrier.  The order is fixed for a launch shape, so
@@ -37,9 +46,9 @@ struct FitParams {
   int N, T;         // sources, frames
   int F;            // bins per mixture (restart seed index i = global % F)
   int prob_offset;  // global problem index of blockIdx.x == 0
-  const void* x;    // R2 [nprob][M][T]   SoA, t fastest
-  void* H;          // R  [nprob][N][T]   in/out
-  void* U;          // R  [nprob][M][T]   scratch (streaming mode only)
+  const void* x;    // R2 [nprob][T][M]
+  void* H;          // R  [nprob][T][N]   in/out
+  void* work;       // R  [nprob][T][2M]  scratch (streaming mode only)
   double2* W;       // [nprob][M*M] col-major (r + c*M), in/out
   double* L;        // [nprob][M*N] col-major (m + n*M), in/out
   const double* power;  // [nprob] SampleCovSet::power_scale
@@ -59,7 +68,8 @@ struct Split {
   // M  > 4: the CTA splits into M groups of warps, group g owns Q_g (M^2).
   static constexpr int MSPLIT = (M <= 4) ? 1 : M;
   static constexpr int MG = M / MSPLIT;
-  static constexpr int KA = MG * M * M + 1;  // pass-A values per thread
+  static constexpr int KQ = MG * M * M;          // Q values per thread
+  static constexpr int KA = KQ + MG + 1;         // + sum U r per channel + sum log2 s2
 };
 
 // Occupancy target: CTAs per SM the register budget must allow (256 threads).
@@ -71,7 +81,7 @@ struct Occ {
 // Shared-memory carve-up, identical on host and device.
 template <int M, int NT, typename R>
 struct FitSmem {
-  int off_wd, off_wr, off_ld, off_lr, off_lold, off_linv, off_hs, off_us, off_hsum, off_num,
+  int off_wd, off_wr, off_ld, off_le, off_linv, off_hsc, off_hscr, off_us, off_hsum, off_num,
       off_den, off_red, off_res, off_scal, off_big, kred, kres, total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
@@ -80,17 +90,17 @@ struct FitSmem {
     if (M + 1 > kred) kred = M + 1;
     if (2 * M * nc > kred) kred = 2 * M * nc;
     if (NT > kred) kred = NT;
-    kres = M * M * M + 1;
+    kres = M * M * M + M + 1;
     if (kres < kred) kres = kred;
     int o = 0;
     off_wd = o; o = al(o + M * M * 16);
     off_wr = o; o = al(o + M * M * 2 * (int)sizeof(R));
     off_ld = o; o = al(o + M * NT * 8);
-    off_lr = o; o = al(o + M * NT * (int)sizeof(R));
-    off_lold = o; o = al(o + M * (int)sizeof(R));
+    off_le = o; o = al(o + M * NT * (int)sizeof(R));
     off_linv = o; o = al(o + M * (int)sizeof(R));
-    off_hs = o; o = al(o + NT * (int)sizeof(R));
-    off_us = o; o = al(o + M * (int)sizeof(R));
+    off_hsc = o; o = al(o + NT * 8);
+    off_hscr = o; o = al(o + NT * (int)sizeof(R));
+    off_us = o; o = al(o + M * 8);
     off_hsum = o; o = al(o + NT * 8);
     off_num = o; o = al(o + M * NT * 8);
     off_den = o; o = al(o + M * NT * 8);
@@ -102,7 +112,10 @@ struct FitSmem {
     off_res = o; o = al(o + kres * 8);
     off_scal = o; o = al(o + 64);
     off_big = o;
-    if (resident) o = al(o + T * (M * 2 * (int)sizeof(R) + N * (int)sizeof(R) + M * (int)sizeof(R)));
+    // x, H and work records, each region 16-byte aligned.
+    if (resident)
+      o = al(al(al(o + T * 2 * M * (int)sizeof(R)) + T * N * (int)sizeof(R)) +
+             T * 2 * M * (int)sizeof(R));
     total = o;
   }
 };
@@ -111,6 +124,48 @@ struct Scalars {
   double eps, logdet, nll0;
   int stop, status;
 };
+
+// --------------------------------------------------------- vector records --
+template <int K, typename R>
+__device__ __forceinline__ void ld_rec(const R* p, R (&v)[K]) {
+  if constexpr (sizeof(R) == 4 && K % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < K; k += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + k);
+      v[k] = q.x, v[k + 1] = q.y, v[k + 2] = q.z, v[k + 3] = q.w;
+    }
+  } else if constexpr (K % 2 == 0) {
+    using V2 = typename Cplx<R>::type;
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      const V2 q = *reinterpret_cast<const V2*>(p + k);
+      v[k] = q.x, v[k + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = p[k];
+  }
+}
+
+template <int K, typename R>
+__device__ __forceinline__ void st_rec(R* p, const R (&v)[K]) {
+  if constexpr (sizeof(R) == 4 && K % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < K; k += 4)
+      *reinterpret_cast<float4*>(p + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+  } else if constexpr (K % 2 == 0) {
+    using V2 = typename Cplx<R>::type;
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      V2 q;
+      q.x = v[k], q.y = v[k + 1];
+      *reinterpret_cast<V2*>(p + k) = q;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = v[k];
+  }
+}
 
 // ------------------------------------------------------------- fp64 algebra --
 // Everything below runs in one thread on register arrays (M is a compile-time
@@ -129,7 +184,6 @@ __device__ __forceinline__ void lu_factor(double2 (&a)[M * M], int (&perm)[M]) {
       const double v = cabs2(a[r + k * M]);
       if (v > best) best = v, p = r;
     }
-    // Swap rows k and p with static indices (p is runtime).
 #pragma unroll
     for (int r = k + 1; r < M; ++r) {
       if (r == p) {
@@ -146,8 +200,10 @@ __device__ __forceinline__ void lu_factor(double2 (&a)[M * M], int (&perm)[M]) {
     }
     if (best != 0.0) {
       const double2 piv = a[k + k * M];
+      const double s = 1.0 / best;
+      const double2 ipiv = make_double2(piv.x * s, -piv.y * s);  // 1 / piv
 #pragma unroll
-      for (int r = k + 1; r < M; ++r) a[r + k * M] = cdiv(a[r + k * M], piv);
+      for (int r = k + 1; r < M; ++r) a[r + k * M] = cmul(a[r + k * M], ipiv);
 #pragma unroll
       for (int c = k + 1; c < M; ++c)
 #pragma unroll
@@ -179,27 +235,45 @@ __device__ __forceinline__ void lu_solve_unit(const double2 (&lu)[M * M], const 
 // singular (a zero or non-finite U diagonal).
 template <int M>
 __device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
-  double2 a[M * M];
-  int perm[M];
-#pragma unroll
-  for (int k = 0; k < M * M; ++k) a[k] = w[k];
-  lu_factor<M>(a, perm);
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < M; ++k) {
-    const double v = cabs2(a[k + k * M]);
+  if constexpr (M == 1) {
+    const double v = cabs2(w[0]);
     if (!(v > 0.0) || !isfinite(v)) return false;
-    acc += log(v);
+    out = log(v);
+    return true;
+  } else if constexpr (M == 2) {
+    // |u00 u11|^2 of the pivoted LU equals |det W|^2; a vanishing pivot is
+    // the singular case the reference rejects.
+    const double2 w00 = w[0], w10 = w[1], w01 = w[2], w11 = w[3];
+    const double a0 = cabs2(w00), a1 = cabs2(w10);
+    const double2 det = csub(cmul(w00, w11), cmul(w01, w10));
+    const double d = cabs2(det);
+    if (!((a0 > 0.0 || a1 > 0.0) && d > 0.0) || !isfinite(d)) return false;
+    out = log(d);
+    return true;
+  } else {
+    double2 a[M * M];
+    int perm[M];
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) a[k] = w[k];
+    lu_factor<M>(a, perm);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double v = cabs2(a[k + k * M]);
+      if (!(v > 0.0) || !isfinite(v)) return false;
+      acc += log(v);
+    }
+    out = acc;  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
+    return true;
   }
-  out = acc;  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
-  return true;
 }
 
-// Cold path of ip_update_w: one seeded perturbation of column `col`
+// Cold path of ip_update_w: one seeded perturbation of a column
 // (fastfca.cpp:66-69).  The generator is seeded lazily on the first restart
 // of the sweep and its state lives in shared scratch.
-static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng, bool* seeded,
-                                        PolarNormal* gauss, unsigned long long seed, int bin) {
+static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng,
+                                               bool* seeded, PolarNormal* gauss,
+                                               unsigned long long seed, int bin) {
   if (!*seeded) {
     rng->seed(mix_seed(seed, bin));
     *seeded = true;
@@ -243,8 +317,7 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
       double2 wr[M * M];
 #pragma unroll
       for (int k = 0; k < M * M; ++k) wr[k] = w[k];
-      double2 a[M * M], lu[M * M], wm[M];
-      int perm[M];
+      double2 a[M * M], wm[M];
       double anorm = 0.0;
 #pragma unroll
       for (int r = 0; r < M; ++r)
@@ -254,11 +327,30 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
 #pragma unroll
           for (int k = 0; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
           a[r + c * M] = s;  // (W^H Q)(r,c)
-          lu[r + c * M] = s;
           anorm += cabs2(s);
         }
-      lu_factor<M>(lu, perm);
-      lu_solve_unit<M>(lu, perm, col, wm);
+      if constexpr (M == 1) {
+        wm[0] = cdiv(make_double2(1.0, 0.0), a[0]);
+      } else if constexpr (M == 2) {
+        // Closed-form inverse column; same solution as the pivoted LU.
+        const double2 det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
+        const double s = 1.0 / cabs2(det);
+        const double2 idet = make_double2(det.x * s, -det.y * s);
+        if (col == 0) {
+          wm[0] = cmul(a[3], idet);
+          wm[1] = cmul(make_double2(-a[1].x, -a[1].y), idet);
+        } else {
+          wm[0] = cmul(make_double2(-a[2].x, -a[2].y), idet);
+          wm[1] = cmul(a[0], idet);
+        }
+      } else {
+        double2 lu[M * M];
+        int perm[M];
+#pragma unroll
+        for (int k = 0; k < M * M; ++k) lu[k] = a[k];
+        lu_factor<M>(lu, perm);
+        lu_solve_unit<M>(lu, perm, col, wm);
+      }
       double wn = 0.0, rn = 0.0;
       bool fin = true;
 #pragma unroll
@@ -273,8 +365,8 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
         for (int c = 0; c < M; ++c) s = cadd(s, cmul(a[r + c * M], wm[c]));
         rn += cabs2(s);
       }
-      const double scale = sqrt(anorm) * sqrt(wn) + 1.0;
-      if (fin && sqrt(rn) <= 1e-8 * scale) {
+      const double scale = sqrt(anorm * wn) + 1.0;
+      if (fin && rn <= 1e-16 * scale * scale) {
         double en = 0.0;
 #pragma unroll
         for (int r = 0; r < M; ++r) {
@@ -284,7 +376,7 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
           en += cmulc(wm[r], qw).x;
         }
         if (en > 0.0 && isfinite(en)) {
-          const double s = 1.0 / sqrt(en);
+          const double s = rsqrt(en);
 #pragma unroll
           for (int r = 0; r < M; ++r) w[r + col * M] = make_double2(wm[r].x * s, wm[r].y * s);
           break;
@@ -305,6 +397,8 @@ template <int M, int NT, bool EXACT, typename R>
 __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
+  constexpr int XR = 2 * M;  // reals per x record
+  constexpr int WR = 2 * M;  // reals per work record: U[M], Phi[M]
   extern __shared__ __align__(16) unsigned char smem[];
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
   const int lane = tid & 31, warp = tid >> 5;
@@ -315,11 +409,11 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
   double* Ld = reinterpret_cast<double*>(smem + lay.off_ld);
-  R* Lr = reinterpret_cast<R*>(smem + lay.off_lr);
-  R* Lold = reinterpret_cast<R*>(smem + lay.off_lold);
-  R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);
-  R* hs = reinterpret_cast<R*>(smem + lay.off_hs);
-  R* us = reinterpret_cast<R*>(smem + lay.off_us);
+  R* Le = reinterpret_cast<R*>(smem + lay.off_le);      // L * hsc, compute type
+  R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);  // 1 / L(:, n) of the new column
+  double* hsc = reinterpret_cast<double*>(smem + lay.off_hsc);
+  R* hscr = reinterpret_cast<R*>(smem + lay.off_hscr);  // hsc in the compute type (MM)
+  double* us = reinterpret_cast<double*>(smem + lay.off_us);
   double* hsumv = reinterpret_cast<double*>(smem + lay.off_hsum);
   double* numd = reinterpret_cast<double*>(smem + lay.off_num);
   double* dend = reinterpret_cast<double*>(smem + lay.off_den);
@@ -330,22 +424,29 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   // Source-loop guard: folds away when N is the compile-time NT.
 #define FFCA_NK(k) (EXACT || (k) < N)
 
-  const C* xg = reinterpret_cast<const C*>(p.x) + size_t(b) * M * T;
+  const R* xg = reinterpret_cast<const R*>(p.x) + size_t(b) * XR * T;
   R* Hg = reinterpret_cast<R*>(p.H) + size_t(b) * N * T;
-  const C* xs;
+  const R* xs;
   R* Hs;
-  R* Us;
+  R* wk;
   if (p.resident) {
-    C* xsm = reinterpret_cast<C*>(smem + lay.off_big);
-    Hs = reinterpret_cast<R*>(xsm + M * T);
-    Us = Hs + N * T;
-    for (int k = tid; k < M * T; k += nthreads) xsm[k] = xg[k];
+    const int ox = lay.off_big;
+    const int oh = FitSmem<M, NT, R>::al(ox + T * XR * (int)sizeof(R));
+    const int ow = FitSmem<M, NT, R>::al(oh + T * N * (int)sizeof(R));
+    R* xsm = reinterpret_cast<R*>(smem + ox);
+    Hs = reinterpret_cast<R*>(smem + oh);
+    wk = reinterpret_cast<R*>(smem + ow);
+    {
+      const C* src = reinterpret_cast<const C*>(xg);
+      C* dst = reinterpret_cast<C*>(xsm);
+      for (int k = tid; k < M * T; k += nthreads) dst[k] = src[k];
+    }
     for (int k = tid; k < N * T; k += nthreads) Hs[k] = Hg[k];
     xs = xsm;
   } else {
     xs = xg;
     Hs = Hg;
-    Us = reinterpret_cast<R*>(p.U) + size_t(b) * M * T;
+    wk = reinterpret_cast<R*>(p.work) + size_t(b) * WR * T;
   }
   for (int k = tid; k < M * M; k += nthreads) {
     const double2 w = p.W[size_t(b) * M * M + k];
@@ -355,10 +456,10 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   for (int k = tid; k < M * N; k += nthreads) {
     const double l = p.L[size_t(b) * M * N + k];
     Ld[k] = l;
-    Lr[k] = R(l);
+    Le[k] = R(l);
   }
-  for (int k = tid; k < NT; k += nthreads) hs[k] = R(1);
-  for (int k = tid; k < M; k += nthreads) us[k] = R(1);
+  for (int k = tid; k < NT; k += nthreads) hsc[k] = 1.0;
+  for (int k = tid; k < M; k += nthreads) us[k] = 1.0;
   const double power = p.power[b];
   if (tid == 0) {
     sc->eps = fmax(1e-8 * power, 1e-300);  // var_eps, sigmodel.hpp:29-31
@@ -369,6 +470,15 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   const R eps = R(sc->eps);
   const bool update_loading = !p.fix_loadings;
   const int bin_index = (p.prob_offset + b) % p.F;
+
+  auto load_h = [&](int t, R (&h)[NT]) {
+    if constexpr (EXACT) {
+      ld_rec<NT>(Hs + t * NT, h);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NT; ++k) h[k] = (k < N) ? Hs[t * N + k] : R(0);
+    }
+  };
 
   // Warp-0 fixed-order sum of per-warp partials red[w*K + o] -> res[o].
   auto gather = [&](int K, int kact) {
@@ -382,161 +492,170 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     }
   };
 
+  // y = W^H x and U = |y|^2 of one frame.
+  auto decorrelate = [&](const R (&xv)[XR], R (&u)[M]) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      R yr = R(0), yi = R(0);
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const C w = Wr[c + m * M];
+        yr += w.x * xv[2 * c] + w.y * xv[2 * c + 1];
+        yi += w.x * xv[2 * c + 1] - w.y * xv[2 * c];
+      }
+      u[m] = yr * yr + yi * yi;
+    }
+  };
+
   // ---------------------------------------------------------------- pass A --
-  // first: U from x and the current W; else U = stored U * us (balance).
-  // Leaves the reduced Q_m (packed) in res[0, M^3) and the NLL in res[M^3],
-  // visible to warp 0 (the caller's serial section runs on thread 0).
+  // first: U from x and the current W; else U = stored U (times us[m] after
+  // the reduction).  Leaves Q_m packed in res[0, M^3), sum_t U r per channel
+  // in res[M^3 + m] and sum log2 sigma^2 in res[M^3 + M] (warp 0 visible).
   auto pass_a = [&](bool first, bool want_q, bool want_nll) {
-    constexpr int MSPLIT = S::MSPLIT, MG = S::MG, KA = S::KA;
+    constexpr int MSPLIT = S::MSPLIT, MG = S::MG, KQ = S::KQ, KA = S::KA;
     const int gs = nthreads / MSPLIT;
     const int g = tid / gs, lt = tid - g * gs;
     const int m0 = g * MG;
-    R q[MG * M * M];
+    R q[KQ];
 #pragma unroll
-    for (int k = 0; k < MG * M * M; ++k) q[k] = R(0);
-    double nll = 0.0;
+    for (int k = 0; k < KQ; ++k) q[k] = R(0);
+    R ur[MG], lg = R(0);
+#pragma unroll
+    for (int k = 0; k < MG; ++k) ur[k] = R(0);
     for (int t = lt; t < T; t += gs) {
-      C xv[M];
-#pragma unroll
-      for (int m = 0; m < M; ++m) xv[m] = xs[m * T + t];
+      R xv[XR];
+      ld_rec<XR>(xs + t * XR, xv);
       R h[NT];
-#pragma unroll
-      for (int k = 0; k < NT; ++k) h[k] = FFCA_NK(k) ? Hs[k * T + t] * hs[k] : R(0);
+      load_h(t, h);
       R P[M * M];
       if (want_q) {
 #pragma unroll
         for (int a = 0; a < M; ++a) {
-          P[a * M + a] = cabs2(xv[a]);
+          P[a * M + a] = xv[2 * a] * xv[2 * a] + xv[2 * a + 1] * xv[2 * a + 1];
 #pragma unroll
           for (int c = a + 1; c < M; ++c) {
-            const C z = cmulc(xv[c], xv[a]);  // x_a * conj(x_c)
-            P[a * M + c] = z.x;
-            P[c * M + a] = z.y;
+            // x_a conj(x_c)
+            P[a * M + c] = xv[2 * a] * xv[2 * c] + xv[2 * a + 1] * xv[2 * c + 1];
+            P[c * M + a] = xv[2 * a + 1] * xv[2 * c] - xv[2 * a] * xv[2 * c + 1];
           }
         }
       }
-      R nll_t = R(0);
+      R u[M];
+      if (want_nll) {
+        if (first) {
+          decorrelate(xv, u);
+        } else {
+          R w[WR];
+          ld_rec<WR>(wk + t * WR, w);
+#pragma unroll
+          for (int m = 0; m < M; ++m) u[m] = w[m];
+        }
+      }
 #pragma unroll
       for (int mi = 0; mi < MG; ++mi) {
         const int m = m0 + mi;
         R s2 = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) s2 += Lr[m + k * M] * h[k];
+          if (FFCA_NK(k)) s2 += Le[m + k * M] * h[k];
         const R r = rcp_fast(s2);
         if (want_nll) {
-          R u;
-          if (first) {
-            C y = mkc<R>(R(0), R(0));
+          R um = u[0];
 #pragma unroll
-            for (int c = 0; c < M; ++c) y = cadd(y, cmulc(Wr[c + m * M], xv[c]));
-            u = cabs2(y);
-          } else {
-            u = Us[m * T + t] * us[m];
-          }
-          nll_t += u * r + flog(s2);
+          for (int mm = 0; mm < M; ++mm)
+            if (mm == m) um = u[mm];
+          ur[mi] += um * r;
+          lg += flog2(s2);
         }
         if (want_q) {
 #pragma unroll
           for (int k = 0; k < M * M; ++k) q[mi * M * M + k] += r * P[k];
         }
       }
-      nll += double(nll_t);
     }
     if (want_q) {
 #pragma unroll
-      for (int k = 0; k < MG * M * M; ++k) {
+      for (int k = 0; k < KQ; ++k) {
         const R s = warp_sum(q[k]);
         if (lane == 0) red[warp * KA + k] = double(s);
       }
     }
-    {
-      const double s = warp_sum(nll);
-      if (lane == 0) red[warp * KA + KA - 1] = s;
+    if (want_nll) {
+#pragma unroll
+      for (int k = 0; k < MG; ++k) {
+        const R s = warp_sum(ur[k]);
+        if (lane == 0) red[warp * KA + KQ + k] = double(s);
+      }
+      const R s = warp_sum(lg);
+      if (lane == 0) red[warp * KA + KQ + MG] = double(s);
     }
     __syncthreads();
     if (warp == 0) {
       const int wpg = nwarps / MSPLIT;  // warps per channel group
-      const int nout = want_q ? M * M * M : 0;
-      for (int o = lane; o <= nout; o += 32) {
+      const int nq = want_q ? M * M * M : 0;
+      const int nout = nq + (want_nll ? M + 1 : 0);
+      for (int o = lane; o < nout; o += 32) {
         double s = 0.0;
-        if (o == nout) {
-          for (int w = 0; w < nwarps; ++w) s += red[w * KA + KA - 1];
-          res[M * M * M] = s;
-        } else {
+        if (o < nq) {
           const int m = o / (M * M), k = o - m * M * M;
           const int grp = m / MG, mi = m - grp * MG;
           for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + mi * M * M + k];
           res[o] = s;
+        } else if (o < nq + M) {
+          const int m = o - nq;
+          const int grp = m / MG, mi = m - grp * MG;
+          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + KQ + mi];
+          res[M * M * M + m] = s;
+        } else {
+          for (int w = 0; w < nwarps; ++w) s += red[w * KA + KQ + MG];
+          res[M * M * M + M] = s;
         }
       }
       __syncwarp();
     }
   };
 
+  // NLL of the current iterate from pass-A sums (thread 0).
+  auto nll_from_res = [&](double logdet) {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) s += us[m] * res[M * M * M + m];
+    return -double(T) * logdet + s + 0.69314718055994531 * res[M * M * M + M];
+  };
+
   // ------------------------------------------------- EM sweep n (0..N) --
-  // Finishes source n-1 (H row with the new L column) and accumulates the L
-  // reduction of source n (fastfca.cpp:85-97).
-  auto em_sweep = [&](int n, bool apply_hs) {
+  // n == 0: U = |W^H x|^2 (stored); n >= 1: finish source n-1 (H row from the
+  // stored Phi and the new L column); n < N: Phi of source n (stored) and its
+  // L reduction sum_t Phi / H_true (fastfca.cpp:85-97).
+  auto em_sweep = [&](int n) {
     R acc[M + 1];
 #pragma unroll
     for (int k = 0; k <= M; ++k) acc[k] = R(0);
     const int j = n - 1;
+    // Source n's effective loading and 1/hsc (H_true = H_stored * hsc).
     for (int t = tid; t < T; t += nthreads) {
       R h[NT];
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        if (FFCA_NK(k)) {
-          R v = Hs[k * T + t];
-          if (apply_hs) {
-            v *= hs[k];
-            Hs[k * T + t] = v;
-          }
-          h[k] = v;
-        } else {
-          h[k] = R(0);
-        }
-      }
-      R u[M];
+      load_h(t, h);
+      R w[WR];
       if (n == 0) {
-        C xv[M];
+        R xv[XR], u[M];
+        ld_rec<XR>(xs + t * XR, xv);
+        decorrelate(xv, u);
 #pragma unroll
-        for (int m = 0; m < M; ++m) xv[m] = xs[m * T + t];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          C y = mkc<R>(R(0), R(0));
-#pragma unroll
-          for (int c = 0; c < M; ++c) y = cadd(y, cmulc(Wr[c + m * M], xv[c]));
-          u[m] = cabs2(y);
-          Us[m * T + t] = u[m];
-        }
+        for (int m = 0; m < M; ++m) w[m] = u[m];
       } else {
-#pragma unroll
-        for (int m = 0; m < M; ++m) u[m] = Us[m * T + t];
+        ld_rec<WR>(wk + t * WR, w);
       }
       if (j >= 0) {
-        R hj = R(0);
+        R s = R(0);
 #pragma unroll
-        for (int k = 0; k < NT; ++k)
-          if (k == j) hj = h[k];
-        R hsum_m = R(0);
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          R lh = eps;
-#pragma unroll
-          for (int k = 0; k < NT; ++k)
-            if (FFCA_NK(k)) lh += ((k == j) ? Lold[m] : Lr[m + k * M]) * h[k];
-          const R lnhn = Lold[m] * hj;
-          const R gg = lnhn * rcp_fast(lh);
-          const R phi = gg * gg * u[m] + (R(1) - gg) * lnhn;
-          hsum_m += Linv[m] * phi;
-        }
-        R hn = hsum_m * R(1.0 / M);
-        hn = hn > tiny<R>() ? hn : tiny<R>();
+        for (int m = 0; m < M; ++m) s += Linv[m] * w[M + m];
+        R hn = s * R(1.0 / M);
+        hn = hn > tiny<R>() ? hn : tiny<R>();  // fastfca.cpp:96-97
 #pragma unroll
         for (int k = 0; k < NT; ++k)
           if (k == j) h[k] = hn;
-        Hs[j * T + t] = hn;
+        Hs[t * N + j] = hn;
         acc[M] += hn;
       }
       if (n < N) {
@@ -550,12 +669,14 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           R lh = eps;
 #pragma unroll
           for (int k = 0; k < NT; ++k)
-            if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
-          const R lnhn = Lr[m + n * M] * hn;
+            if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
+          const R lnhn = Le[m + n * M] * hn;
           const R gg = lnhn * rcp_fast(lh);
-          const R phi = gg * gg * u[m] + (R(1) - gg) * lnhn;
+          const R phi = gg * (gg * w[m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
+          w[M + m] = phi;
           acc[m] += phi * ihn;
         }
+        st_rec<WR>(wk + t * WR, w);
       }
     }
 #pragma unroll
@@ -569,7 +690,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
 
   // ------------------------------------------------------ MM sweeps --
   // L update: num/den reductions over t for sources [n0, n0+nc).
-  auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u, bool apply_hs) {
+  auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u) {
     constexpr int NCMAX = (16 / M) > 0 ? (16 / M) : 1;
     constexpr int K = 2 * M * NCMAX;
     R acc[K];
@@ -577,44 +698,26 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     for (int k = 0; k < K; ++k) acc[k] = R(0);
     for (int t = tid; t < T; t += nthreads) {
       R h[NT];
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        if (FFCA_NK(k)) {
-          R v = Hs[k * T + t];
-          if (apply_hs) {
-            v *= hs[k];
-            Hs[k * T + t] = v;
-          }
-          h[k] = v;
-        } else {
-          h[k] = R(0);
-        }
-      }
-      R u[M];
+      load_h(t, h);
+      R w[WR];
       if (compute_u) {
-        C xv[M];
+        R xv[XR], u[M];
+        ld_rec<XR>(xs + t * XR, xv);
+        decorrelate(xv, u);
 #pragma unroll
-        for (int m = 0; m < M; ++m) xv[m] = xs[m * T + t];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          C y = mkc<R>(R(0), R(0));
-#pragma unroll
-          for (int c = 0; c < M; ++c) y = cadd(y, cmulc(Wr[c + m * M], xv[c]));
-          u[m] = cabs2(y);
-          Us[m * T + t] = u[m];
-        }
+        for (int m = 0; m < M; ++m) w[m] = u[m], w[M + m] = R(0);
+        st_rec<WR>(wk + t * WR, w);
       } else {
-#pragma unroll
-        for (int m = 0; m < M; ++m) u[m] = Us[m * T + t];
+        ld_rec<WR>(wk + t * WR, w);
       }
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         R lh = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
+          if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
         const R il = rcp_fast(lh);
-        const R ul2 = u[m] * il * il;
+        const R ul2 = w[m] * il * il;
 #pragma unroll
         for (int c = 0; c < NCMAX; ++c) {
           if (c < ncnt) {
@@ -639,38 +742,29 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     gather(K, 2 * M * ncnt);
   };
 
-  auto mm_h_sweep = [&](bool compute_u, bool apply_hs) {
+  // H update with the new L (all sources from one lh, fastfca.cpp:111-116).
+  // Stores true H values; the caller resets hsc[] to 1.
+  auto mm_h_sweep = [&](bool compute_u) {
     R acc[NT];
 #pragma unroll
     for (int k = 0; k < NT; ++k) acc[k] = R(0);
     for (int t = tid; t < T; t += nthreads) {
       R h[NT];
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        if (FFCA_NK(k)) {
-          R v = Hs[k * T + t];
-          if (apply_hs) v *= hs[k];
-          h[k] = v;
-        } else {
-          h[k] = R(0);
-        }
-      }
+      load_h(t, h);
       R u[M];
       if (compute_u) {
-        C xv[M];
+        R xv[XR];
+        ld_rec<XR>(xs + t * XR, xv);
+        decorrelate(xv, u);
+        R w[WR];
 #pragma unroll
-        for (int m = 0; m < M; ++m) xv[m] = xs[m * T + t];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          C y = mkc<R>(R(0), R(0));
-#pragma unroll
-          for (int c = 0; c < M; ++c) y = cadd(y, cmulc(Wr[c + m * M], xv[c]));
-          u[m] = cabs2(y);
-          Us[m * T + t] = u[m];
-        }
+        for (int m = 0; m < M; ++m) w[m] = u[m], w[M + m] = R(0);
+        st_rec<WR>(wk + t * WR, w);
       } else {
+        R w[WR];
+        ld_rec<WR>(wk + t * WR, w);
 #pragma unroll
-        for (int m = 0; m < M; ++m) u[m] = Us[m * T + t];
+        for (int m = 0; m < M; ++m) u[m] = w[m];
       }
       R il[M], ul2[M];
 #pragma unroll
@@ -678,23 +772,25 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         R lh = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) lh += Lr[m + k * M] * h[k];
+          if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
         il[m] = rcp_fast(lh);
         ul2[m] = u[m] * il[m] * il[m];
       }
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         if (FFCA_NK(k)) {
+          // Le = L_new * hsc and H_true = H * hsc: the hsc factors cancel in
+          // the ratio, the product H_true * sqrt(num/den) keeps one.
           R num = R(0), den = R(0);
 #pragma unroll
           for (int m = 0; m < M; ++m) {
-            num += Lr[m + k * M] * ul2[m];
-            den += Lr[m + k * M] * il[m];
+            num += Le[m + k * M] * ul2[m];
+            den += Le[m + k * M] * il[m];
           }
           den = den > tiny<R>() ? den : tiny<R>();
-          R hv = h[k] * fsqrt(num / den);
+          R hv = h[k] * hscr[k] * fsqrt(num / den);
           hv = hv > tiny<R>() ? hv : tiny<R>();
-          Hs[k * T + t] = hv;
+          Hs[t * N + k] = hv;
           acc[k] += hv;
         }
       }
@@ -710,6 +806,13 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     gather(NT, N);
   };
 
+  // Le = L * hsc in the compute type (thread 0).
+  auto refresh_le = [&]() {
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int m = 0; m < M; ++m) Le[m + n * M] = narrow_pos<R>(Ld[m + n * M] * hsc[n]);
+  };
+
   // -------------------------------------------------------------- driver --
   const bool record = p.record != 0;
   const bool silent = !(power > 0.0);
@@ -721,7 +824,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         sc->status = kStatusSingularW;
         sc->stop = 1;
       }
-      sc->nll0 = -double(T) * ld + res[M * M * M];
+      sc->nll0 = nll_from_res(ld);
       p.nll[size_t(0) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
     if (silent && !sc->stop) {
@@ -749,22 +852,21 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       // ---- L/H updates (the IP sweep of this iteration already ran)
       if (p.flavor == 0) {
         for (int n = 0; n <= N; ++n) {
-          em_sweep(n, n == 0);
+          em_sweep(n);
           if (tid == 0) {
-            if (n == 0)
-              for (int k = 0; k < NT; ++k) hs[k] = R(1);
             if (n >= 1) hsumv[n - 1] = res[M];
             if (n < N) {
+              // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
+              // (fastfca.cpp:92-94).  Sweep n+1 stores the true H row n, so its
+              // scale resets to 1 and Le(:, n) becomes the new L column.
+              const double ih = 1.0 / hsc[n];
 #pragma unroll
               for (int m = 0; m < M; ++m) {
-                Lold[m] = Lr[m + n * M];
-                if (update_loading) {
-                  const double l = fmax(res[m] / double(T), 1e-300);  // :92-94
-                  Ld[m + n * M] = l;
-                  Lr[m + n * M] = narrow_pos<R>(l);
-                }
-                Linv[m] = rcp_fast(Lr[m + n * M]);
+                if (update_loading) Ld[m + n * M] = fmax(res[m] * ih / double(T), 1e-300);
+                Linv[m] = R(1.0 / Ld[m + n * M]);
+                Le[m + n * M] = narrow_pos<R>(Ld[m + n * M]);
               }
+              hsc[n] = 1.0;
             }
           }
           __syncthreads();
@@ -774,44 +876,50 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         if (update_loading) {
           for (int n0 = 0; n0 < N; n0 += p.nc) {
             const int cnt = min(p.nc, N - n0);
-            mm_l_sweep(n0, cnt, first, first);
+            mm_l_sweep(n0, cnt, first);
             if (tid == 0) {
-              if (first)
-                for (int k = 0; k < NT; ++k) hs[k] = R(1);
               for (int c = 0; c < cnt; ++c)
+#pragma unroll
                 for (int m = 0; m < M; ++m) {
                   numd[m + (n0 + c) * M] = res[(c * M + m) * 2 + 0];
                   dend[m + (n0 + c) * M] = res[(c * M + m) * 2 + 1];
                 }
               if (n0 + cnt >= N) {
+                // num, den were accumulated with H_stored; H_true = H * hsc scales
+                // both by hsc[n], which cancels in num/den.
                 for (int k = 0; k < M * N; ++k) {
                   const double den = fmax(dend[k], 1e-300);
-                  const double l = fmax(Ld[k] * sqrt(numd[k] / den), 1e-300);  // :107-109
-                  Ld[k] = l;
-                  Lr[k] = narrow_pos<R>(l);
+                  Ld[k] = fmax(Ld[k] * sqrt(numd[k] / den), 1e-300);  // :107-109
                 }
+                refresh_le();
+                for (int k = 0; k < N; ++k) hscr[k] = R(hsc[k]);
               }
             }
             __syncthreads();
             first = false;
           }
+        } else {
+          if (tid == 0) {
+            for (int k = 0; k < N; ++k) hscr[k] = R(hsc[k]);
+          }
+          __syncthreads();
         }
-        mm_h_sweep(first, first);
+        mm_h_sweep(first);
         if (tid == 0) {
-          if (first)
-            for (int k = 0; k < NT; ++k) hs[k] = R(1);
-          for (int k = 0; k < N; ++k) hsumv[k] = res[k];
+          for (int k = 0; k < N; ++k) hsumv[k] = res[k], hsc[k] = 1.0;
         }
         __syncthreads();
       }
       // ---- one serial section: balance_scales (fastfca.cpp:127-142),
-      //      log|det W|^2 for the trace, and the R copies of W and L.
+      //      log|det W|^2 for the trace, and the compute-type copies.
       if (tid == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) us[m] = 1.0;
         if (p.normalize && update_loading) {
           for (int n = 0; n < N; ++n) {
             const double mu = hsumv[n] / double(T);
             if (mu > 0.0 && isfinite(mu)) {
-              hs[n] = R(1.0 / mu);
+              hsc[n] = 1.0 / mu;
 #pragma unroll
               for (int m = 0; m < M; ++m) Ld[m + n * M] *= mu;
             }
@@ -829,7 +937,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
                 Wd[c + m * M].x *= r;
                 Wd[c + m * M].y *= r;
               }
-              us[m] = R(1.0 / s);
+              us[m] = 1.0 / s;
             }
           }
         }
@@ -841,7 +949,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           }
           sc->logdet = ld;
         }
-        for (int k = 0; k < M * N; ++k) Lr[k] = narrow_pos<R>(Ld[k]);
+        refresh_le();
 #pragma unroll
         for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
       }
@@ -852,12 +960,9 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         pass_a(false, more, record);
         if (tid == 0) {
           if (record)
-            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
-                -double(T) * sc->logdet + res[M * M * M];
+            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] = nll_from_res(sc->logdet);
           if (more) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
-#pragma unroll
-            for (int m = 0; m < M; ++m) us[m] = R(1);
             int bad = -1;
             if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)(it + 1), bin_index,
                               reinterpret_cast<Mt19937_64*>(red), bad)) {
@@ -878,14 +983,10 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   // ------------------------------------------------------------- epilogue --
   for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
   for (int k = tid; k < M * N; k += nthreads) p.L[size_t(b) * M * N + k] = Ld[k];
-  if (p.resident) {
-    for (int k = tid; k < N * T; k += nthreads) Hg[k] = Hs[k] * hs[k / T];
-  } else {
-    bool pending = false;
-    for (int k = 0; k < N; ++k) pending = pending || hs[k] != R(1);
-    if (pending)
-      for (int k = tid; k < N * T; k += nthreads) Hg[k] = Hg[k] * hs[k / T];
-  }
+  bool pending = false;
+  for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
+  if (p.resident || pending)
+    for (int k = tid; k < N * T; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
   if (tid == 0) p.status[b] = sc->status;
 }
 

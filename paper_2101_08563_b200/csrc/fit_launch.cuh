@@ -25,8 +25,8 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.T, nc, fp.resident != 0);
   cudaError_t err;
   if (!fp.resident) {
-    fp.U = ctx->get(kU, size_t(fp.nprob) * M * fp.T * sizeof(R), &err);
-    if (!fp.U)
+    fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
+    if (!fp.work)
       return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
   }
   auto kern = fit_kernel<M, NT, EXACT, R>;
