@@ -129,6 +129,11 @@ int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, in
 /* Number of kernels the last call on this context launched (bench evidence). */
 int ffca_last_launch_count(const ffca_ctx* ctx);
 
+/* Diagnostics: subsequent ffca_fit_device launches on this context record
+ * per-problem phase cycle counters into dev_counters ([P][16] uint64, device
+ * memory; NULL disables). */
+int ffca_debug_set_timing(ffca_ctx* ctx, unsigned long long* dev_counters);
+
 #ifdef __cplusplus
 }
 #endif

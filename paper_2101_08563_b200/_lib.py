@@ -24,7 +24,7 @@ EXPORTS = (
     "ffca_version", "ffca_last_error", "ffca_device_count", "ffca_ctx_create",
     "ffca_ctx_destroy", "ffca_fit", "ffca_separate", "ffca_nll_bins", "ffca_power_scale",
     "ffca_fit_device", "ffca_separate_device", "ffca_power_scale_device",
-    "ffca_last_launch_count",
+    "ffca_last_launch_count", "ffca_debug_set_timing",
 )
 
 
@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
                                            P, P, P, P, P, P]
         L.ffca_power_scale_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]
         L.ffca_last_launch_count.argtypes = [P]
+        L.ffca_debug_set_timing.argtypes = [P, P]
         _ = dp
         _lib = L
     return _lib

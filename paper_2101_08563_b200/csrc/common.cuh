@@ -161,3 +161,51 @@ namespace ffca {
 __device__ __forceinline__ float flog2(float a) { return __log2f(a); }
 __device__ __forceinline__ double flog2(double a) { return log2(a); }
 }  // namespace ffca
+
+namespace ffca {
+// log2 on the SFU with denormal flushing (fp32 path); libdevice log2 in fp64.
+__device__ __forceinline__ float flog2_ftz(float a) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ double flog2_ftz(double a) { return log2(a); }
+
+template <int K>
+struct Pow2Ceil {
+  static constexpr int value = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+};
+
+// Reduce K per-lane values over the warp and store the K totals to dst[0..K)
+// (as double).  Recursive halving: at each step the lanes split the remaining
+// values in two and exchange the half they give away, so the warp issues
+// Kp - 1 + (5 - log2 Kp) shuffles instead of 5K (Kp = K rounded up to a power
+// of two, <= 32).  The summation tree is fixed, so results are deterministic.
+template <int K, typename T>
+__device__ __forceinline__ void warp_reduce_store(const T (&in)[K], double* dst, int lane) {
+  static_assert(K <= 32, "warp_reduce_store: at most 32 values");
+  constexpr int KP = Pow2Ceil<K>::value;
+  T v[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) v[i] = i < K ? in[i] : T(0);
+  int idx = 0;
+  int o = 16;
+#pragma unroll
+  for (int c = KP; c > 1; c >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < c / 2; ++i) {
+      const T send = up ? v[i] : v[i + c / 2];
+      const T keep = up ? v[i + c / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    if (up) idx += c / 2;
+    o >>= 1;
+  }
+  T s = v[0];
+  for (int oo = o; oo > 0; oo >>= 1) s += __shfl_xor_sync(0xffffffffu, s, oo);
+  // Lanes whose low (plain-reduction) bits are zero hold distinct totals.
+  const int lowmask = o == 0 ? 0 : (o << 1) - 1;
+  if ((lane & lowmask) == 0 && idx < K) dst[idx] = double(s);
+}
+}  // namespace ffca

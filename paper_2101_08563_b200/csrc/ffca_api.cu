@@ -417,6 +417,7 @@ int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_
   fp.normalize = o->normalize_scales;
   fp.fix_loadings = o->fix_loadings;
   fp.seed = o->seed;
+  fp.timing = ctx->timing;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   return o->precision == FFCA_PREC_FP64 ? launch_fit<double>(ctx, dim, fp, st)
                                         : launch_fit<float>(ctx, dim, fp, st);
@@ -459,3 +460,9 @@ int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, in
 }
 
 }  // extern "C"
+
+extern "C" int ffca_debug_set_timing(ffca_ctx* ctx, unsigned long long* dev_counters) {
+  if (!ctx) return set_err(FFCA_INVALID_ARGUMENT, "ffca_debug_set_timing: null ctx");
+  ctx->timing = dev_counters;
+  return FFCA_OK;
+}

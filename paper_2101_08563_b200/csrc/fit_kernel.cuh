@@ -23,18 +23,19 @@
 //   EM       N+1 sweeps: sweep n stores U (n = 0), finishes source n-1's H row
 //            from the stored Phi and the freshly reduced L column, then forms
 //            Phi for source n and reduces its L column (em_update_lh,
-//            fastfca.cpp:80-99).
+//            fastfca.cpp:80-99).  Each sweep ends in ONE barrier: every thread
+//            then sums the per-warp partials itself and applies the identical
+//            L-column update (no serial section between sweeps).
 //   MM       two sweeps (mm_update_lh, fastfca.cpp:101-117).
 //   balance  one thread on the reduced row means (fastfca.cpp:127-142).  The H
 //            row scale 1/mu_n is kept as a per-source factor hsc[n] (H_true =
 //            H_stored * hsc) and folded into the effective loadings
 //            Le = L * hsc used by every product, so no sweep rescales H; the
-//            next H update stores true values and resets hsc[n] = 1.  The W
-//            column scale is folded the same way into the stored U (us[m]).
-// Every reduction is: warp shuffles -> per-warp partials in shared memory ->
-// barrier -> warp 0 sums the partials in a fixed order (fp64) -> lane 0 does
-// the serial update -> barrier.  The order is fixed for a launch shape, so
-// per-bin results do not depend on how bins are sharded over GPUs.
+//            next H update stores true values.  The W column scale is folded
+//            the same way into the stored U (us[m]).
+// Reductions: multi-value warp butterflies -> per-warp partials in shared
+// memory -> barrier -> fixed-order cross-warp sums.  The order is fixed for a
+// launch shape, so per-bin results do not depend on how bins are sharded.
 #pragma once
 
 #include "common.cuh"
@@ -57,6 +58,7 @@ struct FitParams {
   int* status;      // [nprob]: 0 ok, 1 silent band, 2 IP singular, 3 singular W
   int iters, flavor, record, normalize, fix_loadings, resident;
   int nc;           // MM: sources per L-reduction chunk
+  unsigned long long* timing;  // optional per-problem phase cycle counters [nprob][16]
   unsigned long long seed;
 };
 
@@ -82,12 +84,11 @@ struct Occ {
 template <int M, int NT, typename R>
 struct FitSmem {
   int off_wd, off_wr, off_ld, off_le, off_linv, off_hsc, off_hscr, off_us, off_hsum, off_num,
-      off_den, off_red, off_res, off_scal, off_big, kred, kres, total;
+      off_den, off_reda, off_redb, off_res, off_rng, off_scal, off_big, kred, kres, total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
     using S = Split<M>;
-    kred = S::KA;
-    if (M + 1 > kred) kred = M + 1;
+    kred = M + 1;
     if (2 * M * nc > kred) kred = 2 * M * nc;
     if (NT > kred) kred = NT;
     kres = M * M * M + M + 1;
@@ -104,12 +105,10 @@ struct FitSmem {
     off_hsum = o; o = al(o + NT * 8);
     off_num = o; o = al(o + M * NT * 8);
     off_den = o; o = al(o + M * NT * 8);
-    off_red = o;  // also the restart RNG state during the (serial) IP stage
-    {
-      const int need = nwarps * kred * 8;
-      o = al(o + (need > (int)sizeof(Mt19937_64) ? need : (int)sizeof(Mt19937_64)));
-    }
+    off_reda = o; o = al(o + nwarps * S::KA * 8);       // pass-A partials
+    off_redb = o; o = al(o + 2 * nwarps * kred * 8);    // sweep partials, double-buffered
     off_res = o; o = al(o + kres * 8);
+    off_rng = o; o = al(o + (int)sizeof(Mt19937_64));   // restart generator (cold)
     off_scal = o; o = al(o + 64);
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
@@ -166,6 +165,25 @@ __device__ __forceinline__ void st_rec(R* p, const R (&v)[K]) {
     for (int k = 0; k < K; ++k) p[k] = v[k];
   }
 }
+
+// Small uniform per-bin parameters: copied into registers at the top of a
+// pass when they fit (M*NT <= 32), else read from shared memory in the loop.
+template <int K, bool REG, typename R>
+struct Uniform {
+  R v[REG ? K : 1];
+  const R* s;
+  __device__ __forceinline__ void load(const R* src) {
+    s = src;
+    if constexpr (REG) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = src[k];
+    }
+  }
+  __device__ __forceinline__ R operator[](int k) const {
+    if constexpr (REG) return v[k];
+    else return s[k];
+  }
+};
 
 // ------------------------------------------------------------- fp64 algebra --
 // Everything below runs in one thread on register arrays (M is a compile-time
@@ -399,6 +417,8 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   using S = Split<M>;
   constexpr int XR = 2 * M;  // reals per x record
   constexpr int WR = 2 * M;  // reals per work record: U[M], Phi[M]
+  constexpr bool HOIST = (M * NT <= 32);
+  using WU = Uniform<2 * M * M, (2 * M * M <= 32), R>;  // W in the compute type
   extern __shared__ __align__(16) unsigned char smem[];
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
   const int lane = tid & 31, warp = tid >> 5;
@@ -417,9 +437,12 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   double* hsumv = reinterpret_cast<double*>(smem + lay.off_hsum);
   double* numd = reinterpret_cast<double*>(smem + lay.off_num);
   double* dend = reinterpret_cast<double*>(smem + lay.off_den);
-  double* red = reinterpret_cast<double*>(smem + lay.off_red);
+  double* reda = reinterpret_cast<double*>(smem + lay.off_reda);
+  double* redb = reinterpret_cast<double*>(smem + lay.off_redb);
   double* res = reinterpret_cast<double*>(smem + lay.off_res);
+  Mt19937_64* rng = reinterpret_cast<Mt19937_64*>(smem + lay.off_rng);
   Scalars* sc = reinterpret_cast<Scalars*>(smem + lay.off_scal);
+  const int kred = lay.kred;
 
   // Source-loop guard: folds away when N is the compile-time NT.
 #define FFCA_NK(k) (EXACT || (k) < N)
@@ -468,8 +491,20 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   }
   __syncthreads();
   const R eps = R(sc->eps);
+  const double invT = 1.0 / double(T);
   const bool update_loading = !p.fix_loadings;
   const int bin_index = (p.prob_offset + b) % p.F;
+  // Phase timing (diagnostics only; p.timing == nullptr in production).
+  unsigned long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tlast = clock64();
+#define FFCA_TIC(k)                              \
+  do {                                           \
+    if (p.timing && tid == 0) {                  \
+      const unsigned long long now_ = clock64(); \
+      tacc[k] += now_ - tlast;                   \
+      tlast = now_;                              \
+    }                                            \
+  } while (0)
 
   auto load_h = [&](int t, R (&h)[NT]) {
     if constexpr (EXACT) {
@@ -480,31 +515,29 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     }
   };
 
-  // Warp-0 fixed-order sum of per-warp partials red[w*K + o] -> res[o].
-  auto gather = [&](int K, int kact) {
-    if (warp == 0) {
-      for (int o = lane; o < kact; o += 32) {
-        double s = 0.0;
-        for (int w = 0; w < nwarps; ++w) s += red[w * K + o];
-        res[o] = s;
-      }
-      __syncwarp();
-    }
-  };
-
   // y = W^H x and U = |y|^2 of one frame.
-  auto decorrelate = [&](const R (&xv)[XR], R (&u)[M]) {
+  auto decorrelate = [&](const WU& w, const R (&xv)[XR], R (&u)[M]) {
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      R yr = R(0), yi = R(0);
+      R yr = w[2 * m * M] * xv[0] + w[2 * m * M + 1] * xv[1];
+      R yi = w[2 * m * M] * xv[1] - w[2 * m * M + 1] * xv[0];
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        const C w = Wr[c + m * M];
-        yr += w.x * xv[2 * c] + w.y * xv[2 * c + 1];
-        yi += w.x * xv[2 * c + 1] - w.y * xv[2 * c];
+      for (int c = 1; c < M; ++c) {
+        const R wx = w[2 * (c + m * M)], wy = w[2 * (c + m * M) + 1];
+        yr += wx * xv[2 * c] + wy * xv[2 * c + 1];
+        yi += wx * xv[2 * c + 1] - wy * xv[2 * c];
       }
       u[m] = yr * yr + yi * yi;
     }
+  };
+
+  // Every thread: totals[k] = sum over warps of red[w*K + k] (fixed order via
+  // a butterfly over the first nwarps lanes).
+  auto all_totals = [&](const double* red, int K, int k, double& out) {
+    double v = (lane < nwarps) ? red[lane * K + k] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    out = v;
   };
 
   // ---------------------------------------------------------------- pass A --
@@ -516,12 +549,13 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     const int gs = nthreads / MSPLIT;
     const int g = tid / gs, lt = tid - g * gs;
     const int m0 = g * MG;
-    R q[KQ];
+    Uniform<M * NT, HOIST, R> le;
+    le.load(Le);
+    WU wr;
+    wr.load(reinterpret_cast<const R*>(Wr));
+    R acc[KA];
 #pragma unroll
-    for (int k = 0; k < KQ; ++k) q[k] = R(0);
-    R ur[MG], lg = R(0);
-#pragma unroll
-    for (int k = 0; k < MG; ++k) ur[k] = R(0);
+    for (int k = 0; k < KA; ++k) acc[k] = R(0);
     for (int t = lt; t < T; t += gs) {
       R xv[XR];
       ld_rec<XR>(xs + t * XR, xv);
@@ -543,7 +577,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       R u[M];
       if (want_nll) {
         if (first) {
-          decorrelate(xv, u);
+          decorrelate(wr, xv, u);
         } else {
           R w[WR];
           ld_rec<WR>(wk + t * WR, w);
@@ -557,37 +591,31 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         R s2 = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) s2 += Le[m + k * M] * h[k];
+          if (FFCA_NK(k)) s2 += le[m + k * M] * h[k];
         const R r = rcp_fast(s2);
         if (want_nll) {
           R um = u[0];
 #pragma unroll
           for (int mm = 0; mm < M; ++mm)
             if (mm == m) um = u[mm];
-          ur[mi] += um * r;
-          lg += flog2(s2);
+          acc[KQ + mi] += um * r;
+          acc[KQ + MG] += flog2_ftz(s2);
         }
         if (want_q) {
 #pragma unroll
-          for (int k = 0; k < M * M; ++k) q[mi * M * M + k] += r * P[k];
+          for (int k = 0; k < M * M; ++k) acc[mi * M * M + k] += r * P[k];
         }
       }
     }
-    if (want_q) {
+    FFCA_TIC(0);
+    if constexpr (KA <= 32) {
+      warp_reduce_store<KA>(acc, reda + warp * KA, lane);
+    } else {
 #pragma unroll
-      for (int k = 0; k < KQ; ++k) {
-        const R s = warp_sum(q[k]);
-        if (lane == 0) red[warp * KA + k] = double(s);
+      for (int k = 0; k < KA; ++k) {
+        const R s = warp_sum(acc[k]);
+        if (lane == 0) reda[warp * KA + k] = double(s);
       }
-    }
-    if (want_nll) {
-#pragma unroll
-      for (int k = 0; k < MG; ++k) {
-        const R s = warp_sum(ur[k]);
-        if (lane == 0) red[warp * KA + KQ + k] = double(s);
-      }
-      const R s = warp_sum(lg);
-      if (lane == 0) red[warp * KA + KQ + MG] = double(s);
     }
     __syncthreads();
     if (warp == 0) {
@@ -599,15 +627,15 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         if (o < nq) {
           const int m = o / (M * M), k = o - m * M * M;
           const int grp = m / MG, mi = m - grp * MG;
-          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + mi * M * M + k];
+          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + mi * M * M + k];
           res[o] = s;
         } else if (o < nq + M) {
           const int m = o - nq;
           const int grp = m / MG, mi = m - grp * MG;
-          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += red[w * KA + KQ + mi];
+          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + KQ + mi];
           res[M * M * M + m] = s;
         } else {
-          for (int w = 0; w < nwarps; ++w) s += red[w * KA + KQ + MG];
+          for (int w = 0; w < nwarps; ++w) s += reda[w * KA + KQ + MG];
           res[M * M * M + M] = s;
         }
       }
@@ -626,13 +654,20 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   // ------------------------------------------------- EM sweep n (0..N) --
   // n == 0: U = |W^H x|^2 (stored); n >= 1: finish source n-1 (H row from the
   // stored Phi and the new L column); n < N: Phi of source n (stored) and its
-  // L reduction sum_t Phi / H_true (fastfca.cpp:85-97).
-  auto em_sweep = [&](int n) {
+  // L reduction sum_t Phi / H_true (fastfca.cpp:85-97).  Ends with the per-warp
+  // partials in red and one barrier.
+  auto em_sweep = [&](int n, double* red) {
+    Uniform<M * NT, HOIST, R> le;
+    le.load(Le);
+    WU wr;
+    if (n == 0) wr.load(reinterpret_cast<const R*>(Wr));
+    R linv[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) linv[m] = Linv[m];
     R acc[M + 1];
 #pragma unroll
     for (int k = 0; k <= M; ++k) acc[k] = R(0);
     const int j = n - 1;
-    // Source n's effective loading and 1/hsc (H_true = H_stored * hsc).
     for (int t = tid; t < T; t += nthreads) {
       R h[NT];
       load_h(t, h);
@@ -640,16 +675,16 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       if (n == 0) {
         R xv[XR], u[M];
         ld_rec<XR>(xs + t * XR, xv);
-        decorrelate(xv, u);
+        decorrelate(wr, xv, u);
 #pragma unroll
         for (int m = 0; m < M; ++m) w[m] = u[m];
       } else {
         ld_rec<WR>(wk + t * WR, w);
       }
       if (j >= 0) {
-        R s = R(0);
+        R s = linv[0] * w[M];
 #pragma unroll
-        for (int m = 0; m < M; ++m) s += Linv[m] * w[M + m];
+        for (int m = 1; m < M; ++m) s += linv[m] * w[M + m];
         R hn = s * R(1.0 / M);
         hn = hn > tiny<R>() ? hn : tiny<R>();  // fastfca.cpp:96-97
 #pragma unroll
@@ -669,8 +704,8 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           R lh = eps;
 #pragma unroll
           for (int k = 0; k < NT; ++k)
-            if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
-          const R lnhn = Le[m + n * M] * hn;
+            if (FFCA_NK(k)) lh += le[m + k * M] * h[k];
+          const R lnhn = le[m + n * M] * hn;
           const R gg = lnhn * rcp_fast(lh);
           const R phi = gg * (gg * w[m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
           w[M + m] = phi;
@@ -679,20 +714,20 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         st_rec<WR>(wk + t * WR, w);
       }
     }
-#pragma unroll
-    for (int k = 0; k <= M; ++k) {
-      const R s = warp_sum(acc[k]);
-      if (lane == 0) red[warp * (M + 1) + k] = double(s);
-    }
+    FFCA_TIC(4);
+    warp_reduce_store<M + 1>(acc, red + warp * (M + 1), lane);
     __syncthreads();
-    gather(M + 1, M + 1);
   };
 
   // ------------------------------------------------------ MM sweeps --
   // L update: num/den reductions over t for sources [n0, n0+nc).
-  auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u) {
+  auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u, double* red) {
     constexpr int NCMAX = (16 / M) > 0 ? (16 / M) : 1;
     constexpr int K = 2 * M * NCMAX;
+    Uniform<M * NT, HOIST, R> le;
+    le.load(Le);
+    WU wr;
+    if (compute_u) wr.load(reinterpret_cast<const R*>(Wr));
     R acc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = R(0);
@@ -703,7 +738,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       if (compute_u) {
         R xv[XR], u[M];
         ld_rec<XR>(xs + t * XR, xv);
-        decorrelate(xv, u);
+        decorrelate(wr, xv, u);
 #pragma unroll
         for (int m = 0; m < M; ++m) w[m] = u[m], w[M + m] = R(0);
         st_rec<WR>(wk + t * WR, w);
@@ -715,7 +750,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         R lh = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
+          if (FFCA_NK(k)) lh += le[m + k * M] * h[k];
         const R il = rcp_fast(lh);
         const R ul2 = w[m] * il * il;
 #pragma unroll
@@ -731,20 +766,25 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (k < 2 * M * ncnt) {
-        const R s = warp_sum(acc[k]);
-        if (lane == 0) red[warp * K + k] = double(s);
-      }
-    }
+    warp_reduce_store<K>(acc, red + warp * K, lane);
     __syncthreads();
-    gather(K, 2 * M * ncnt);
+    if (warp == 0) {
+      for (int o = lane; o < 2 * M * ncnt; o += 32) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w * K + o];
+        res[o] = s;
+      }
+      __syncwarp();
+    }
   };
 
   // H update with the new L (all sources from one lh, fastfca.cpp:111-116).
   // Stores true H values; the caller resets hsc[] to 1.
-  auto mm_h_sweep = [&](bool compute_u) {
+  auto mm_h_sweep = [&](bool compute_u, double* red) {
+    Uniform<M * NT, HOIST, R> le;
+    le.load(Le);
+    WU wr;
+    if (compute_u) wr.load(reinterpret_cast<const R*>(Wr));
     R acc[NT];
 #pragma unroll
     for (int k = 0; k < NT; ++k) acc[k] = R(0);
@@ -755,7 +795,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       if (compute_u) {
         R xv[XR];
         ld_rec<XR>(xs + t * XR, xv);
-        decorrelate(xv, u);
+        decorrelate(wr, xv, u);
         R w[WR];
 #pragma unroll
         for (int m = 0; m < M; ++m) w[m] = u[m], w[M + m] = R(0);
@@ -772,7 +812,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         R lh = eps;
 #pragma unroll
         for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) lh += Le[m + k * M] * h[k];
+          if (FFCA_NK(k)) lh += le[m + k * M] * h[k];
         il[m] = rcp_fast(lh);
         ul2[m] = u[m] * il[m] * il[m];
       }
@@ -784,8 +824,8 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           R num = R(0), den = R(0);
 #pragma unroll
           for (int m = 0; m < M; ++m) {
-            num += Le[m + k * M] * ul2[m];
-            den += Le[m + k * M] * il[m];
+            num += le[m + k * M] * ul2[m];
+            den += le[m + k * M] * il[m];
           }
           den = den > tiny<R>() ? den : tiny<R>();
           R hv = h[k] * hscr[k] * fsqrt(num / den);
@@ -795,15 +835,16 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      if (FFCA_NK(k)) {
-        const R s = warp_sum(acc[k]);
-        if (lane == 0) red[warp * NT + k] = double(s);
-      }
-    }
+    warp_reduce_store<NT>(acc, red + warp * NT, lane);
     __syncthreads();
-    gather(NT, N);
+    if (warp == 0) {
+      for (int o = lane; o < N; o += 32) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w * NT + o];
+        res[o] = s;
+      }
+      __syncwarp();
+    }
   };
 
   // Le = L * hsc in the compute type (thread 0).
@@ -816,7 +857,9 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   // -------------------------------------------------------------- driver --
   const bool record = p.record != 0;
   const bool silent = !(power > 0.0);
+  FFCA_TIC(9);
   pass_a(true, p.iters > 0 && !silent, record);
+  FFCA_TIC(1);
   if (tid == 0) {
     if (record) {
       double ld = 0.0;
@@ -838,7 +881,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     if (!sc->stop && p.iters > 0) {
       // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
       int bad = -1;
-      if (!ip_update<M>(Wd, res, T, p.seed, bin_index, reinterpret_cast<Mt19937_64*>(red), bad)) {
+      if (!ip_update<M>(Wd, res, T, p.seed, bin_index, rng, bad)) {
         sc->status = kStatusIpSingular | (bad << 8);
         sc->stop = 1;
       }
@@ -852,31 +895,45 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       // ---- L/H updates (the IP sweep of this iteration already ran)
       if (p.flavor == 0) {
         for (int n = 0; n <= N; ++n) {
-          em_sweep(n);
-          if (tid == 0) {
-            if (n >= 1) hsumv[n - 1] = res[M];
-            if (n < N) {
-              // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
-              // (fastfca.cpp:92-94).  Sweep n+1 stores the true H row n, so its
-              // scale resets to 1 and Le(:, n) becomes the new L column.
-              const double ih = 1.0 / hsc[n];
-#pragma unroll
-              for (int m = 0; m < M; ++m) {
-                if (update_loading) Ld[m + n * M] = fmax(res[m] * ih / double(T), 1e-300);
-                Linv[m] = R(1.0 / Ld[m + n * M]);
-                Le[m + n * M] = narrow_pos<R>(Ld[m + n * M]);
-              }
-              hsc[n] = 1.0;
-            }
+          double* red = redb + (n & 1) * nwarps * kred;
+          em_sweep(n, red);
+          FFCA_TIC(5);
+          // Every thread sums the partials and applies the identical update
+          // (each shared value below is written with the same bits by every
+          // thread and not read in its old state after the barrier).
+          if (n >= 1) {
+            double hs;
+            all_totals(red, M + 1, M, hs);
+            if (tid == 0) hsumv[n - 1] = hs;
           }
-          __syncthreads();
+          if (n < N) {
+            // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
+            // (fastfca.cpp:92-94).  Sweep n+1 stores the true H row n, so
+            // Le(:, n) becomes the new L column (no hsc).
+            const double ih = invT / hsc[n];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              double tot;
+              all_totals(red, M + 1, m, tot);
+              const double l = update_loading ? fmax(tot * ih, 1e-300) : Ld[m + n * M];
+              const R lr = narrow_pos<R>(l);
+              if (lane == 0) {
+                Ld[m + n * M] = l;
+                Le[m + n * M] = lr;
+                Linv[m] = rcp_fast(lr);
+              }
+            }
+            __syncwarp();
+          }
+          FFCA_TIC(6);
         }
       } else {
         bool first = true;
+        int pb = 0;
         if (update_loading) {
           for (int n0 = 0; n0 < N; n0 += p.nc) {
             const int cnt = min(p.nc, N - n0);
-            mm_l_sweep(n0, cnt, first);
+            mm_l_sweep(n0, cnt, first, redb + (pb++ & 1) * nwarps * kred);
             if (tid == 0) {
               for (int c = 0; c < cnt; ++c)
 #pragma unroll
@@ -904,20 +961,22 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           }
           __syncthreads();
         }
-        mm_h_sweep(first);
+        mm_h_sweep(first, redb + (pb & 1) * nwarps * kred);
         if (tid == 0) {
           for (int k = 0; k < N; ++k) hsumv[k] = res[k], hsc[k] = 1.0;
         }
-        __syncthreads();
       }
+      __syncthreads();
+      FFCA_TIC(5);
       // ---- one serial section: balance_scales (fastfca.cpp:127-142),
       //      log|det W|^2 for the trace, and the compute-type copies.
       if (tid == 0) {
 #pragma unroll
         for (int m = 0; m < M; ++m) us[m] = 1.0;
+        for (int n = 0; n < N; ++n) hsc[n] = 1.0;  // every H row is stored true now
         if (p.normalize && update_loading) {
           for (int n = 0; n < N; ++n) {
-            const double mu = hsumv[n] / double(T);
+            const double mu = hsumv[n] * invT;
             if (mu > 0.0 && isfinite(mu)) {
               hsc[n] = 1.0 / mu;
 #pragma unroll
@@ -930,14 +989,15 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
             for (int n = 0; n < N; ++n) s += Ld[m + n * M];
             s /= double(N);
             if (s > 0.0 && isfinite(s)) {
-              for (int n = 0; n < N; ++n) Ld[m + n * M] /= s;
-              const double r = 1.0 / sqrt(s);
+              const double is = 1.0 / s;
+              for (int n = 0; n < N; ++n) Ld[m + n * M] *= is;
+              const double r = rsqrt(s);
 #pragma unroll
               for (int c = 0; c < M; ++c) {
                 Wd[c + m * M].x *= r;
                 Wd[c + m * M].y *= r;
               }
-              us[m] = 1.0 / s;
+              us[m] = is;
             }
           }
         }
@@ -953,19 +1013,22 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
 #pragma unroll
         for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
       }
+      FFCA_TIC(7);
       __syncthreads();
+      FFCA_TIC(8);
       if (sc->stop) break;
       const bool more = it + 1 < p.iters;
       if (more || record) {
         pass_a(false, more, record);
+        FFCA_TIC(1);
         if (tid == 0) {
           if (record)
             p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] = nll_from_res(sc->logdet);
           if (more) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
             int bad = -1;
-            if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)(it + 1), bin_index,
-                              reinterpret_cast<Mt19937_64*>(red), bad)) {
+            if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)(it + 1), bin_index, rng,
+                              bad)) {
               sc->status = kStatusIpSingular | (bad << 8);
               sc->stop = 1;
             }
@@ -973,12 +1036,15 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
             for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
           }
         }
+          FFCA_TIC(2);
         __syncthreads();
+        FFCA_TIC(3);
         if (sc->stop) break;
       }
     }
   }
 #undef FFCA_NK
+#undef FFCA_TIC
   __syncthreads();
   // ------------------------------------------------------------- epilogue --
   for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
@@ -987,6 +1053,8 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
   if (p.resident || pending)
     for (int k = tid; k < N * T; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
+  if (p.timing && tid == 0)
+    for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];
   if (tid == 0) p.status[b] = sc->status;
 }
 

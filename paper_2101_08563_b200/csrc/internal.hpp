@@ -22,6 +22,7 @@ struct ffca_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int launches = 0;
+  unsigned long long* timing = nullptr;  // diagnostics: per-problem phase counters
   struct Buf {
     void* p = nullptr;
     size_t n = 0;
