@@ -12,7 +12,9 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libffca.so"
+# FFCA_LIB selects a diagnostics build (e.g. libffca_timing.so); default is
+# the production library.
+LIB_PATH = Path(os.environ.get("FFCA_LIB", Path(__file__).resolve().parent / "libffca.so"))
 
 OK, INVALID_ARGUMENT, NUMERICAL, CUDA_ERROR = 0, 1, 2, 3
 FLAVOR_EM, FLAVOR_MM = 0, 1

@@ -43,23 +43,34 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
 
 
-def build_lib(verbose: bool = False, jobs: int | None = None) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build_lib(verbose: bool = False, jobs: int | None = None, variant: str = "",
+              only: list[str] | None = None) -> Path:
+    """Build libffca.so; variant "timing" builds the phase-timing diagnostics
+    library libffca_timing.so (-DFFCA_PHASE_TIMING) in build_timing/.
+    `only` restricts the CUDA sources (diagnostics builds of one shape)."""
+    global LIB
+    lib = LIB if not variant else PKG / f"libffca_{variant}.so"
+    bdir = BUILD if not variant else ROOT / f"build_{variant}"
+    extra = [] if not variant else [f"-DFFCA_PHASE_{variant.upper()}"]
+    bdir.mkdir(exist_ok=True)
     deps = _headers()
     cu = sorted(CSRC.glob("*.cu"))
     cpp = sorted(CSRC.glob("*.cpp"))
     jobs_list = []
     objs = []
     for src in cu:
-        obj = BUILD / (src.stem + ".o")
+        obj = bdir / (src.stem + ".o")
+        if only and src.stem not in only and src.stem != "ffca_api":
+            continue
         objs.append(obj)
         if _stale(obj, src, deps):
-            jobs_list.append([NVCC, *ARCH, *NVFLAGS, "-c", str(src), "-o", str(obj)])
+            jobs_list.append([NVCC, *ARCH, *NVFLAGS, *extra, "-c", str(src), "-o", str(obj)])
     for src in cpp:
-        obj = BUILD / (src.stem + ".cpp.o")
+        obj = bdir / (src.stem + ".cpp.o")
         objs.append(obj)
         if _stale(obj, src, deps):
             jobs_list.append(["g++", *CXXFLAGS, "-c", str(src), "-o", str(obj)])
+    saved, LIB = LIB, lib
     if jobs_list:
         n = jobs or min(len(jobs_list), os.cpu_count() or 4)
         with cf.ThreadPoolExecutor(n) as ex:
@@ -67,9 +78,12 @@ def build_lib(verbose: bool = False, jobs: int | None = None) -> Path:
                 if verbose:
                     print("[build]", Path(cmd[-3]).name, file=sys.stderr)
                 fut.result()
-    if jobs_list or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"])
-    return LIB
+    try:
+        if jobs_list or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
+            _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"])
+        return LIB
+    finally:
+        LIB = saved
 
 
 def build_oracle() -> None:

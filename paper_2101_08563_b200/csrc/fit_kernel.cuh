@@ -23,7 +23,7 @@
 //   EM       N+1 sweeps: sweep n stores U (n = 0), finishes source n-1's H row
 //            from the stored Phi and the freshly reduced L column, then forms
 //            Phi for source n and reduces its L column (em_update_lh,
-//            fastfca.cpp:80-99).  Each sweep ends in ONE barrier: every thread
+//            fastfca.cpp:80-99).  Each sweep ends in ONE barrier: every warp
 //            then sums the per-warp partials itself and applies the identical
 //            L-column update (no serial section between sweeps).
 //   MM       two sweeps (mm_update_lh, fastfca.cpp:101-117).
@@ -74,17 +74,22 @@ struct Split {
   static constexpr int KA = KQ + MG + 1;         // + sum U r per channel + sum log2 s2
 };
 
-// Occupancy target: CTAs per SM the register budget must allow (256 threads).
+// Launch shape: threads per CTA (upper bound) and the CTAs per SM the
+// register budget must allow.  Small M: 192 threads x 4 CTAs (80 registers),
+// so the 513 bins of a 1024-point STFT fit on 148 SMs in one wave.
 template <int M>
-struct Occ {
-  static constexpr int value = (M <= 3) ? 4 : (M == 4 ? 2 : 1);
+struct Launch {
+  static constexpr int threads = (M <= 3) ? 192 : 256;
+  static constexpr int minb = (M <= 3) ? 4 : (M == 4 ? 2 : 1);
 };
+
+constexpr int kMaxWarps = 8;
 
 // Shared-memory carve-up, identical on host and device.
 template <int M, int NT, typename R>
 struct FitSmem {
-  int off_wd, off_wr, off_ld, off_le, off_linv, off_hsc, off_hscr, off_us, off_hsum, off_num,
-      off_den, off_reda, off_redb, off_res, off_rng, off_scal, off_big, kred, kres, total;
+  int off_wd, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr, off_us, off_hsum,
+      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_scal, off_big, kred, kres, total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
     using S = Split<M>;
@@ -100,6 +105,7 @@ struct FitSmem {
     off_le = o; o = al(o + M * NT * (int)sizeof(R));
     off_linv = o; o = al(o + M * (int)sizeof(R));
     off_hsc = o; o = al(o + NT * 8);
+    off_hinv = o; o = al(o + NT * 8);
     off_hscr = o; o = al(o + NT * (int)sizeof(R));
     off_us = o; o = al(o + M * 8);
     off_hsum = o; o = al(o + NT * 8);
@@ -167,7 +173,7 @@ __device__ __forceinline__ void st_rec(R* p, const R (&v)[K]) {
 }
 
 // Small uniform per-bin parameters: copied into registers at the top of a
-// pass when they fit (M*NT <= 32), else read from shared memory in the loop.
+// pass when they fit, else read from shared memory in the loop.
 template <int K, bool REG, typename R>
 struct Uniform {
   R v[REG ? K : 1];
@@ -186,6 +192,20 @@ struct Uniform {
 };
 
 // ------------------------------------------------------------- fp64 algebra --
+// 1/x to within an ulp without the division slow path: an SFU fp32 seed on
+// the mantissa refined by two fp64 Newton steps (zero/denormal/huge fall back
+// to the IEEE division).
+__device__ __forceinline__ double fast_rcp(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const int e = (hi >> 20) & 0x7ff;
+  if (e == 0 || e >= 2046) return 1.0 / x;
+  const double m = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, lo);  // |m| in [1, 2)
+  double r = double(rcp_fast(float(m)));
+  r = fma(r, fma(-m, r, 1.0), r);
+  r = fma(r, fma(-m, r, 1.0), r);
+  return r * __hiloint2double((2046 - e) << 20, 0);  // * 2^(1023 - e)
+}
+
 // Everything below runs in one thread on register arrays (M is a compile-time
 // constant, every loop unrolls).  Pivot order follows Eigen::PartialPivLU
 // (largest modulus; compared as squared modulus, the same order).
@@ -218,7 +238,7 @@ __device__ __forceinline__ void lu_factor(double2 (&a)[M * M], int (&perm)[M]) {
     }
     if (best != 0.0) {
       const double2 piv = a[k + k * M];
-      const double s = 1.0 / best;
+      const double s = fast_rcp(best);
       const double2 ipiv = make_double2(piv.x * s, -piv.y * s);  // 1 / piv
 #pragma unroll
       for (int r = k + 1; r < M; ++r) a[r + k * M] = cmul(a[r + k * M], ipiv);
@@ -243,7 +263,9 @@ __device__ __forceinline__ void lu_solve_unit(const double2 (&lu)[M * M], const 
     for (int r = k + 1; r < M; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
 #pragma unroll
   for (int k = M - 1; k >= 0; --k) {
-    y[k] = cdiv(y[k], lu[k + k * M]);
+    const double2 d = lu[k + k * M];
+    const double s = fast_rcp(cabs2(d));
+    y[k] = cmul(y[k], make_double2(d.x * s, -d.y * s));
 #pragma unroll
     for (int r = 0; r < k; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
   }
@@ -274,12 +296,16 @@ __device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
 #pragma unroll
     for (int k = 0; k < M * M; ++k) a[k] = w[k];
     lu_factor<M>(a, perm);
-    double acc = 0.0;
+    double prod = 1.0, acc = 0.0;
 #pragma unroll
     for (int k = 0; k < M; ++k) {
       const double v = cabs2(a[k + k * M]);
       if (!(v > 0.0) || !isfinite(v)) return false;
-      acc += log(v);
+      prod *= v;
+      if (k % 4 == 3 || k == M - 1) {  // batch the logs, keep the product in range
+        acc += log(prod);
+        prod = 1.0;
+      }
     }
     out = acc;  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
     return true;
@@ -311,12 +337,14 @@ static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64*
 // qraw[m*M*M + ...] holds sum_t x x^H / sigma2_m packed as: (a,a) real,
 // (a,b) a<b real part at a*M+b and imaginary part at b*M+a.
 template <int M>
-__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
+__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
                                           unsigned long long seed, int bin, Mt19937_64* rng,
                                           int& bad_col) {
   bool seeded = false;
   PolarNormal gauss{0.0, false};
-  const double invT = 1.0 / double(T);
+  double2 wr[M * M];
+#pragma unroll
+  for (int k = 0; k < M * M; ++k) wr[k] = w[k];
 #pragma unroll 1
   for (int col = 0; col < M; ++col) {
     double2 q[M * M];
@@ -332,27 +360,25 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
       }
     }
     for (int attempt = 0;; ++attempt) {
-      double2 wr[M * M];
-#pragma unroll
-      for (int k = 0; k < M * M; ++k) wr[k] = w[k];
       double2 a[M * M], wm[M];
       double anorm = 0.0;
 #pragma unroll
       for (int r = 0; r < M; ++r)
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-          double2 s = make_double2(0.0, 0.0);
+          double2 s = cmulc(wr[r * M], q[c * M]);
 #pragma unroll
-          for (int k = 0; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
+          for (int k = 1; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
           a[r + c * M] = s;  // (W^H Q)(r,c)
           anorm += cabs2(s);
         }
       if constexpr (M == 1) {
-        wm[0] = cdiv(make_double2(1.0, 0.0), a[0]);
+        const double s = fast_rcp(cabs2(a[0]));
+        wm[0] = make_double2(a[0].x * s, -a[0].y * s);
       } else if constexpr (M == 2) {
         // Closed-form inverse column; same solution as the pivoted LU.
         const double2 det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
-        const double s = 1.0 / cabs2(det);
+        const double s = fast_rcp(cabs2(det));
         const double2 idet = make_double2(det.x * s, -det.y * s);
         if (col == 0) {
           wm[0] = cmul(a[3], idet);
@@ -383,20 +409,25 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
         for (int c = 0; c < M; ++c) s = cadd(s, cmul(a[r + c * M], wm[c]));
         rn += cabs2(s);
       }
-      const double scale = sqrt(anorm * wn) + 1.0;
+      // Residual test ||a w - e|| <= 1e-8 (||a|| ||w|| + 1) (fastfca.cpp:55-56),
+      // squared; the scale is a tolerance, so an fp32 square root suffices.
+      const double scale = double(sqrtf(float(anorm * wn))) + 1.0;
       if (fin && rn <= 1e-16 * scale * scale) {
         double en = 0.0;
 #pragma unroll
         for (int r = 0; r < M; ++r) {
-          double2 qw = make_double2(0.0, 0.0);
+          double2 qw = cmul(q[r], wm[0]);
 #pragma unroll
-          for (int c = 0; c < M; ++c) qw = cadd(qw, cmul(q[r + c * M], wm[c]));
+          for (int c = 1; c < M; ++c) qw = cadd(qw, cmul(q[r + c * M], wm[c]));
           en += cmulc(wm[r], qw).x;
         }
         if (en > 0.0 && isfinite(en)) {
           const double s = rsqrt(en);
 #pragma unroll
-          for (int r = 0; r < M; ++r) w[r + col * M] = make_double2(wm[r].x * s, wm[r].y * s);
+          for (int r = 0; r < M; ++r) {
+            wr[r + col * M] = make_double2(wm[r].x * s, wm[r].y * s);
+            w[r + col * M] = wr[r + col * M];
+          }
           break;
         }
       }
@@ -405,6 +436,8 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
         return false;
       }
       ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
+#pragma unroll
+      for (int k = 0; k < M * M; ++k) wr[k] = w[k];
     }
   }
   return true;
@@ -412,7 +445,7 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, int T,
 
 // ------------------------------------------------------------------ kernel --
 template <int M, int NT, bool EXACT, typename R>
-__global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
+__global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
   constexpr int XR = 2 * M;  // reals per x record
@@ -432,6 +465,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   R* Le = reinterpret_cast<R*>(smem + lay.off_le);      // L * hsc, compute type
   R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);  // 1 / L(:, n) of the new column
   double* hsc = reinterpret_cast<double*>(smem + lay.off_hsc);
+  double* hinv = reinterpret_cast<double*>(smem + lay.off_hinv);  // 1 / hsc
   R* hscr = reinterpret_cast<R*>(smem + lay.off_hscr);  // hsc in the compute type (MM)
   double* us = reinterpret_cast<double*>(smem + lay.off_us);
   double* hsumv = reinterpret_cast<double*>(smem + lay.off_hsum);
@@ -481,7 +515,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     Ld[k] = l;
     Le[k] = R(l);
   }
-  for (int k = tid; k < NT; k += nthreads) hsc[k] = 1.0;
+  for (int k = tid; k < NT; k += nthreads) hsc[k] = 1.0, hinv[k] = 1.0;
   for (int k = tid; k < M; k += nthreads) us[k] = 1.0;
   const double power = p.power[b];
   if (tid == 0) {
@@ -494,7 +528,9 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   const double invT = 1.0 / double(T);
   const bool update_loading = !p.fix_loadings;
   const int bin_index = (p.prob_offset + b) % p.F;
-  // Phase timing (diagnostics only; p.timing == nullptr in production).
+  // Phase timing: diagnostics builds only (-DFFCA_PHASE_TIMING, see build.py);
+  // the counters would otherwise cost live registers across the whole kernel.
+#ifdef FFCA_PHASE_TIMING
   unsigned long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long tlast = clock64();
 #define FFCA_TIC(k)                              \
@@ -505,6 +541,11 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       tlast = now_;                              \
     }                                            \
   } while (0)
+#else
+#define FFCA_TIC(k) \
+  do {              \
+  } while (0)
+#endif
 
   auto load_h = [&](int t, R (&h)[NT]) {
     if constexpr (EXACT) {
@@ -531,13 +572,16 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     }
   };
 
-  // Every thread: totals[k] = sum over warps of red[w*K + k] (fixed order via
-  // a butterfly over the first nwarps lanes).
-  auto all_totals = [&](const double* red, int K, int k, double& out) {
-    double v = (lane < nwarps) ? red[lane * K + k] : 0.0;
+  // Fixed-order sum of the per-warp partials red[w*K + k] (issued as
+  // independent loads, then added in warp order).
+  auto sum_warps = [&](const double* red, int K, int k) {
+    double v[kMaxWarps];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    out = v;
+    for (int w = 0; w < kMaxWarps; ++w) v[w] = (w < nwarps) ? red[w * K + k] : 0.0;
+    double s = v[0];
+#pragma unroll
+    for (int w = 1; w < kMaxWarps; ++w) s += v[w];
+    return s;
   };
 
   // ---------------------------------------------------------------- pass A --
@@ -552,7 +596,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     Uniform<M * NT, HOIST, R> le;
     le.load(Le);
     WU wr;
-    wr.load(reinterpret_cast<const R*>(Wr));
+    if (first) wr.load(reinterpret_cast<const R*>(Wr));
     R acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) acc[k] = R(0);
@@ -623,20 +667,25 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       const int nq = want_q ? M * M * M : 0;
       const int nout = nq + (want_nll ? M + 1 : 0);
       for (int o = lane; o < nout; o += 32) {
-        double s = 0.0;
-        if (o < nq) {
-          const int m = o / (M * M), k = o - m * M * M;
-          const int grp = m / MG, mi = m - grp * MG;
-          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + mi * M * M + k];
-          res[o] = s;
-        } else if (o < nq + M) {
-          const int m = o - nq;
-          const int grp = m / MG, mi = m - grp * MG;
-          for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + KQ + mi];
-          res[M * M * M + m] = s;
+        if constexpr (MSPLIT == 1) {
+          const int k = o < nq ? o : (o < nq + M ? KQ + (o - nq) : KQ + MG);
+          res[o < nq ? o : M * M * M + (o - nq)] = sum_warps(reda, KA, k);
         } else {
-          for (int w = 0; w < nwarps; ++w) s += reda[w * KA + KQ + MG];
-          res[M * M * M + M] = s;
+          double s = 0.0;
+          if (o < nq) {
+            const int m = o / (M * M), k = o - m * M * M;
+            const int grp = m / MG, mi = m - grp * MG;
+            for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + mi * M * M + k];
+            res[o] = s;
+          } else if (o < nq + M) {
+            const int m = o - nq;
+            const int grp = m / MG, mi = m - grp * MG;
+            for (int w = grp * wpg; w < (grp + 1) * wpg; ++w) s += reda[w * KA + KQ + mi];
+            res[M * M * M + m] = s;
+          } else {
+            for (int w = 0; w < nwarps; ++w) s += reda[w * KA + KQ + MG];
+            res[M * M * M + M] = s;
+          }
         }
       }
       __syncwarp();
@@ -769,11 +818,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     warp_reduce_store<K>(acc, red + warp * K, lane);
     __syncthreads();
     if (warp == 0) {
-      for (int o = lane; o < 2 * M * ncnt; o += 32) {
-        double s = 0.0;
-        for (int w = 0; w < nwarps; ++w) s += red[w * K + o];
-        res[o] = s;
-      }
+      for (int o = lane; o < 2 * M * ncnt; o += 32) res[o] = sum_warps(red, K, o);
       __syncwarp();
     }
   };
@@ -838,11 +883,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     warp_reduce_store<NT>(acc, red + warp * NT, lane);
     __syncthreads();
     if (warp == 0) {
-      for (int o = lane; o < N; o += 32) {
-        double s = 0.0;
-        for (int w = 0; w < nwarps; ++w) s += red[w * NT + o];
-        res[o] = s;
-      }
+      for (int o = lane; o < N; o += 32) res[o] = sum_warps(red, NT, o);
       __syncwarp();
     }
   };
@@ -881,7 +922,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
     if (!sc->stop && p.iters > 0) {
       // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
       int bad = -1;
-      if (!ip_update<M>(Wd, res, T, p.seed, bin_index, rng, bad)) {
+      if (!ip_update<M>(Wd, res, invT, p.seed, bin_index, rng, bad)) {
         sc->status = kStatusIpSingular | (bad << 8);
         sc->stop = 1;
       }
@@ -898,33 +939,28 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           double* red = redb + (n & 1) * nwarps * kred;
           em_sweep(n, red);
           FFCA_TIC(5);
-          // Every thread sums the partials and applies the identical update
-          // (each shared value below is written with the same bits by every
-          // thread and not read in its old state after the barrier).
+          // Every warp sums the partials (lane k holds value k) and applies
+          // the identical update; each shared value below is written with the
+          // same bits by every warp and is not read in its old state after
+          // the barrier.
+          const double tot = (lane <= M) ? sum_warps(red, M + 1, lane) : 0.0;
           if (n >= 1) {
-            double hs;
-            all_totals(red, M + 1, M, hs);
+            const double hs = __shfl_sync(0xffffffffu, tot, M);
             if (tid == 0) hsumv[n - 1] = hs;
           }
-          if (n < N) {
+          if (n < N && lane < M) {
             // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
             // (fastfca.cpp:92-94).  Sweep n+1 stores the true H row n, so
             // Le(:, n) becomes the new L column (no hsc).
-            const double ih = invT / hsc[n];
-#pragma unroll
-            for (int m = 0; m < M; ++m) {
-              double tot;
-              all_totals(red, M + 1, m, tot);
-              const double l = update_loading ? fmax(tot * ih, 1e-300) : Ld[m + n * M];
-              const R lr = narrow_pos<R>(l);
-              if (lane == 0) {
-                Ld[m + n * M] = l;
-                Le[m + n * M] = lr;
-                Linv[m] = rcp_fast(lr);
-              }
-            }
-            __syncwarp();
+            const int m = lane;
+            const double l =
+                update_loading ? fmax(tot * invT * hinv[n], 1e-300) : Ld[m + n * M];
+            const R lr = narrow_pos<R>(l);
+            Ld[m + n * M] = l;
+            Le[m + n * M] = lr;
+            Linv[m] = rcp_fast(lr);
           }
+          __syncwarp();
           FFCA_TIC(6);
         }
       } else {
@@ -946,7 +982,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
                 // both by hsc[n], which cancels in num/den.
                 for (int k = 0; k < M * N; ++k) {
                   const double den = fmax(dend[k], 1e-300);
-                  Ld[k] = fmax(Ld[k] * sqrt(numd[k] / den), 1e-300);  // :107-109
+                  Ld[k] = fmax(Ld[k] * sqrt(numd[k] * fast_rcp(den)), 1e-300);  // :107-109
                 }
                 refresh_le();
                 for (int k = 0; k < N; ++k) hscr[k] = R(hsc[k]);
@@ -963,7 +999,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
         }
         mm_h_sweep(first, redb + (pb & 1) * nwarps * kred);
         if (tid == 0) {
-          for (int k = 0; k < N; ++k) hsumv[k] = res[k], hsc[k] = 1.0;
+          for (int k = 0; k < N; ++k) hsumv[k] = res[k];
         }
       }
       __syncthreads();
@@ -973,23 +1009,25 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
       if (tid == 0) {
 #pragma unroll
         for (int m = 0; m < M; ++m) us[m] = 1.0;
-        for (int n = 0; n < N; ++n) hsc[n] = 1.0;  // every H row is stored true now
+        for (int n = 0; n < N; ++n) hsc[n] = 1.0, hinv[n] = 1.0;  // every H row is stored true
         if (p.normalize && update_loading) {
           for (int n = 0; n < N; ++n) {
             const double mu = hsumv[n] * invT;
             if (mu > 0.0 && isfinite(mu)) {
-              hsc[n] = 1.0 / mu;
+              hsc[n] = fast_rcp(mu);
+              hinv[n] = mu;
 #pragma unroll
               for (int m = 0; m < M; ++m) Ld[m + n * M] *= mu;
             }
           }
+          const double invN = 1.0 / double(N);
 #pragma unroll
           for (int m = 0; m < M; ++m) {
             double s = 0.0;
             for (int n = 0; n < N; ++n) s += Ld[m + n * M];
-            s /= double(N);
+            s *= invN;
             if (s > 0.0 && isfinite(s)) {
-              const double is = 1.0 / s;
+              const double is = fast_rcp(s);
               for (int n = 0; n < N; ++n) Ld[m + n * M] *= is;
               const double r = rsqrt(s);
 #pragma unroll
@@ -1027,8 +1065,8 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
           if (more) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
             int bad = -1;
-            if (!ip_update<M>(Wd, res, T, p.seed + (unsigned long long)(it + 1), bin_index, rng,
-                              bad)) {
+            if (!ip_update<M>(Wd, res, invT, p.seed + (unsigned long long)(it + 1), bin_index,
+                              rng, bad)) {
               sc->status = kStatusIpSingular | (bad << 8);
               sc->stop = 1;
             }
@@ -1036,7 +1074,7 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
             for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
           }
         }
-          FFCA_TIC(2);
+        FFCA_TIC(2);
         __syncthreads();
         FFCA_TIC(3);
         if (sc->stop) break;
@@ -1053,8 +1091,10 @@ __global__ void __launch_bounds__(256, Occ<M>::value) fit_kernel(FitParams p) {
   for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
   if (p.resident || pending)
     for (int k = tid; k < N * T; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
+#ifdef FFCA_PHASE_TIMING
   if (p.timing && tid == 0)
     for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];
+#endif
   if (tid == 0) p.status[b] = sc->status;
 }
 

@@ -12,7 +12,7 @@ namespace ffca {
 
 template <int M, int NT, bool EXACT, typename R>
 int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
-  const int threads = fit_threads(M, fp.T);
+  const int threads = fit_threads(M, fp.T, Launch<M>::threads);
   const int nwarps = threads / 32;
   int nc = 16 / M;
   if (nc < 1) nc = 1;

@@ -47,13 +47,14 @@ namespace ffca {
 
 enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kNumSlots };
 
-// Threads per fit CTA: about 4 frames per thread, capped at 256; a multiple of
-// 32*M when the weighted-covariance pass is split by channel (M > 4).
-inline int fit_threads(int M, int T) {
+// Threads per fit CTA: about 4 frames per thread, capped at the kernel's
+// launch bound; a multiple of 32*M when the weighted-covariance pass is split
+// by channel (M > 4).
+inline int fit_threads(int M, int T, int maxt) {
   const int per = (M <= 4) ? 32 : 32 * M;
   const int want = (T + 3) / 4;
   int th = ((want + per - 1) / per) * per;
-  const int cap = (256 / per) * per;
+  const int cap = (maxt / per) * per;
   if (th > cap) th = cap;
   if (th < per) th = per;
   if (M <= 4 && th < 64) th = 64;
