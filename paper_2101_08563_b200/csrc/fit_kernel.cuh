@@ -85,10 +85,15 @@ struct Launch {
 
 constexpr int kMaxWarps = 8;
 
+#ifndef FFCA_FRAMES_IN_FLIGHT
+#define FFCA_FRAMES_IN_FLIGHT 1
+#endif
+
 // Shared-memory carve-up, identical on host and device.
 template <int M, int NT, typename R>
 struct FitSmem {
-  int off_wd, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr, off_us, off_hsum,
+  int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
+      off_us, off_hsum,
       off_num, off_den, off_reda, off_redb, off_res, off_rng, off_scal, off_big, kred, kres, total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
@@ -100,6 +105,8 @@ struct FitSmem {
     if (kres < kred) kres = kred;
     int o = 0;
     off_wd = o; o = al(o + M * M * 16);
+    off_wlg = o; o = al(o + M * M * 16);  // W after the IP sweep (log-det input)
+    off_wsc = o; o = al(o + M * 8);       // balance: W column scales
     off_wr = o; o = al(o + M * M * 2 * (int)sizeof(R));
     off_ld = o; o = al(o + M * NT * 8);
     off_le = o; o = al(o + M * NT * (int)sizeof(R));
@@ -126,8 +133,8 @@ struct FitSmem {
 };
 
 struct Scalars {
-  double eps, logdet, nll0;
-  int stop, status;
+  double eps, nll0, logdet0, logs;
+  int stop, status, ldok;
 };
 
 // --------------------------------------------------------- vector records --
@@ -451,6 +458,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   constexpr int XR = 2 * M;  // reals per x record
   constexpr int WR = 2 * M;  // reals per work record: U[M], Phi[M]
   constexpr bool HOIST = (M * NT <= 32);
+  constexpr int FU = FFCA_FRAMES_IN_FLIGHT;  // frames per loop trip (ILP vs registers)
   using WU = Uniform<2 * M * M, (2 * M * M <= 32), R>;  // W in the compute type
   extern __shared__ __align__(16) unsigned char smem[];
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
@@ -460,6 +468,8 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const int b = blockIdx.x;
   const FitSmem<M, NT, R> lay(nwarps, N, T, p.nc, p.resident != 0);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
+  double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
+  double* wsc = reinterpret_cast<double*>(smem + lay.off_wsc);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
   double* Ld = reinterpret_cast<double*>(smem + lay.off_ld);
   R* Le = reinterpret_cast<R*>(smem + lay.off_le);      // L * hsc, compute type
@@ -600,54 +610,61 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     R acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) acc[k] = R(0);
-    for (int t = lt; t < T; t += gs) {
-      R xv[XR];
-      ld_rec<XR>(xs + t * XR, xv);
-      R h[NT];
-      load_h(t, h);
-      R P[M * M];
-      if (want_q) {
+    // FU frames per trip: all loads first, then independent arithmetic chains.
+    for (int t0 = lt; t0 < T; t0 += FU * gs) {
+      R xv[FU][XR], h[FU][NT], u[FU][M];
+      bool ok[FU];
 #pragma unroll
-        for (int a = 0; a < M; ++a) {
-          P[a * M + a] = xv[2 * a] * xv[2 * a] + xv[2 * a + 1] * xv[2 * a + 1];
-#pragma unroll
-          for (int c = a + 1; c < M; ++c) {
-            // x_a conj(x_c)
-            P[a * M + c] = xv[2 * a] * xv[2 * c] + xv[2 * a + 1] * xv[2 * c + 1];
-            P[c * M + a] = xv[2 * a + 1] * xv[2 * c] - xv[2 * a] * xv[2 * c + 1];
-          }
-        }
-      }
-      R u[M];
-      if (want_nll) {
-        if (first) {
-          decorrelate(wr, xv, u);
-        } else {
+      for (int f = 0; f < FU; ++f) {
+        const int t = t0 + f * gs;
+        ok[f] = t < T;
+        const int tt = ok[f] ? t : t0;  // always a valid record
+        ld_rec<XR>(xs + tt * XR, xv[f]);
+        load_h(tt, h[f]);
+        if (want_nll && !first) {
           R w[WR];
-          ld_rec<WR>(wk + t * WR, w);
+          ld_rec<WR>(wk + tt * WR, w);
 #pragma unroll
-          for (int m = 0; m < M; ++m) u[m] = w[m];
+          for (int m = 0; m < M; ++m) u[f][m] = w[m];
         }
       }
 #pragma unroll
-      for (int mi = 0; mi < MG; ++mi) {
-        const int m = m0 + mi;
-        R s2 = eps;
-#pragma unroll
-        for (int k = 0; k < NT; ++k)
-          if (FFCA_NK(k)) s2 += le[m + k * M] * h[k];
-        const R r = rcp_fast(s2);
-        if (want_nll) {
-          R um = u[0];
-#pragma unroll
-          for (int mm = 0; mm < M; ++mm)
-            if (mm == m) um = u[mm];
-          acc[KQ + mi] += um * r;
-          acc[KQ + MG] += flog2_ftz(s2);
-        }
+      for (int f = 0; f < FU; ++f) {
+        if (!ok[f]) continue;
+        R P[M * M];
         if (want_q) {
 #pragma unroll
-          for (int k = 0; k < M * M; ++k) acc[mi * M * M + k] += r * P[k];
+          for (int a = 0; a < M; ++a) {
+            P[a * M + a] = xv[f][2 * a] * xv[f][2 * a] + xv[f][2 * a + 1] * xv[f][2 * a + 1];
+#pragma unroll
+            for (int c = a + 1; c < M; ++c) {
+              // x_a conj(x_c)
+              P[a * M + c] = xv[f][2 * a] * xv[f][2 * c] + xv[f][2 * a + 1] * xv[f][2 * c + 1];
+              P[c * M + a] = xv[f][2 * a + 1] * xv[f][2 * c] - xv[f][2 * a] * xv[f][2 * c + 1];
+            }
+          }
+        }
+        if (want_nll && first) decorrelate(wr, xv[f], u[f]);
+#pragma unroll
+        for (int mi = 0; mi < MG; ++mi) {
+          const int m = m0 + mi;
+          R s2 = eps;
+#pragma unroll
+          for (int k = 0; k < NT; ++k)
+            if (FFCA_NK(k)) s2 += le[m + k * M] * h[f][k];
+          const R r = rcp_fast(s2);
+          if (want_nll) {
+            R um = u[f][0];
+#pragma unroll
+            for (int mm = 0; mm < M; ++mm)
+              if (mm == m) um = u[f][mm];
+            acc[KQ + mi] += um * r;
+            acc[KQ + MG] += flog2_ftz(s2);
+          }
+          if (want_q) {
+#pragma unroll
+            for (int k = 0; k < M * M; ++k) acc[mi * M * M + k] += r * P[k];
+          }
         }
       }
     }
@@ -717,50 +734,72 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 #pragma unroll
     for (int k = 0; k <= M; ++k) acc[k] = R(0);
     const int j = n - 1;
-    for (int t = tid; t < T; t += nthreads) {
-      R h[NT];
-      load_h(t, h);
-      R w[WR];
-      if (n == 0) {
-        R xv[XR], u[M];
-        ld_rec<XR>(xs + t * XR, xv);
-        decorrelate(wr, xv, u);
+    // FU frames per trip: loads, independent arithmetic chains, then stores.
+    for (int t0 = tid; t0 < T; t0 += FU * nthreads) {
+      R h[FU][NT], w[FU][WR];
+      bool ok[FU];
 #pragma unroll
-        for (int m = 0; m < M; ++m) w[m] = u[m];
-      } else {
-        ld_rec<WR>(wk + t * WR, w);
+      for (int f = 0; f < FU; ++f) {
+        const int t = t0 + f * nthreads;
+        ok[f] = t < T;
+        const int tt = ok[f] ? t : t0;  // always a valid record
+        load_h(tt, h[f]);
+        if (n == 0) {
+          R xv[XR], u[M];
+          ld_rec<XR>(xs + tt * XR, xv);
+          decorrelate(wr, xv, u);
+#pragma unroll
+          for (int m = 0; m < M; ++m) w[f][m] = u[m];
+        } else {
+          ld_rec<WR>(wk + tt * WR, w[f]);
+        }
       }
-      if (j >= 0) {
-        R s = linv[0] * w[M];
 #pragma unroll
-        for (int m = 1; m < M; ++m) s += linv[m] * w[M + m];
-        R hn = s * R(1.0 / M);
-        hn = hn > tiny<R>() ? hn : tiny<R>();  // fastfca.cpp:96-97
+      for (int f = 0; f < FU; ++f) {
+        if (!ok[f]) continue;
+        if (j >= 0) {
+          R s = linv[0] * w[f][M];
 #pragma unroll
-        for (int k = 0; k < NT; ++k)
-          if (k == j) h[k] = hn;
-        Hs[t * N + j] = hn;
-        acc[M] += hn;
-      }
-      if (n < N) {
-        R hn = R(0);
-#pragma unroll
-        for (int k = 0; k < NT; ++k)
-          if (k == n) hn = h[k];
-        const R ihn = rcp_fast(hn);
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          R lh = eps;
+          for (int m = 1; m < M; ++m) s += linv[m] * w[f][M + m];
+          R hn = s * R(1.0 / M);
+          hn = hn > tiny<R>() ? hn : tiny<R>();  // fastfca.cpp:96-97
 #pragma unroll
           for (int k = 0; k < NT; ++k)
-            if (FFCA_NK(k)) lh += le[m + k * M] * h[k];
-          const R lnhn = le[m + n * M] * hn;
-          const R gg = lnhn * rcp_fast(lh);
-          const R phi = gg * (gg * w[m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
-          w[M + m] = phi;
-          acc[m] += phi * ihn;
+            if (k == j) h[f][k] = hn;
+          acc[M] += hn;
         }
-        st_rec<WR>(wk + t * WR, w);
+        if (n < N) {
+          R hn = R(0);
+#pragma unroll
+          for (int k = 0; k < NT; ++k)
+            if (k == n) hn = h[f][k];
+          const R ihn = rcp_fast(hn);
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            R lh = eps;
+#pragma unroll
+            for (int k = 0; k < NT; ++k)
+              if (FFCA_NK(k)) lh += le[m + k * M] * h[f][k];
+            const R lnhn = le[m + n * M] * hn;
+            const R gg = lnhn * rcp_fast(lh);
+            const R phi = gg * (gg * w[f][m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
+            w[f][M + m] = phi;
+            acc[m] += phi * ihn;
+          }
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < FU; ++f) {
+        if (!ok[f]) continue;
+        const int t = t0 + f * nthreads;
+        if (j >= 0) {
+          R hj = R(0);
+#pragma unroll
+          for (int k = 0; k < NT; ++k)
+            if (k == j) hj = h[f][k];
+          Hs[t * N + j] = hj;
+        }
+        if (n < N) st_rec<WR>(wk + t * WR, w[f]);
       }
     }
     FFCA_TIC(4);
@@ -927,7 +966,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         sc->stop = 1;
       }
 #pragma unroll
-      for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+      for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
     }
   }
   __syncthreads();
@@ -1004,52 +1043,50 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       }
       __syncthreads();
       FFCA_TIC(5);
-      // ---- one serial section: balance_scales (fastfca.cpp:127-142),
-      //      log|det W|^2 for the trace, and the compute-type copies.
-      if (tid == 0) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) us[m] = 1.0;
-        for (int n = 0; n < N; ++n) hsc[n] = 1.0, hinv[n] = 1.0;  // every H row is stored true
-        if (p.normalize && update_loading) {
-          for (int n = 0; n < N; ++n) {
-            const double mu = hsumv[n] * invT;
-            if (mu > 0.0 && isfinite(mu)) {
-              hsc[n] = fast_rcp(mu);
-              hinv[n] = mu;
-#pragma unroll
-              for (int m = 0; m < M; ++m) Ld[m + n * M] *= mu;
-            }
-          }
-          const double invN = 1.0 / double(N);
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            double s = 0.0;
-            for (int n = 0; n < N; ++n) s += Ld[m + n * M];
-            s *= invN;
-            if (s > 0.0 && isfinite(s)) {
-              const double is = fast_rcp(s);
-              for (int n = 0; n < N; ++n) Ld[m + n * M] *= is;
-              const double r = rsqrt(s);
-#pragma unroll
-              for (int c = 0; c < M; ++c) {
-                Wd[c + m * M].x *= r;
-                Wd[c + m * M].y *= r;
-              }
-              us[m] = is;
-            }
-          }
+      // ---- balance_scales (fastfca.cpp:127-142), lane-parallel in warp 0:
+      //      mu_n per source lane, s_m per channel lane, then the L and W
+      //      scalings.  Warp 1 meanwhile takes log|det W|^2 of the unscaled W
+      //      (copy Wlg); scaling column m by s_m^{-1/2} adds -log s_m.
+      const bool bal = p.normalize && update_loading;
+      if (warp == 0) {
+        for (int n = lane; n < N; n += 32) {  // every H row is stored true here
+          const double mu = hsumv[n] * invT;
+          const bool v = bal && mu > 0.0 && isfinite(mu);
+          hsc[n] = v ? fast_rcp(mu) : 1.0;
+          hinv[n] = v ? mu : 1.0;
         }
-        if (record) {
-          double ld = 0.0;
-          if (!log_abs_det2<M>(Wd, ld)) {
-            sc->status = kStatusSingularW;
-            sc->stop = 1;
-          }
-          sc->logdet = ld;
+        __syncwarp();
+        double lsum = 0.0;
+        for (int m = lane; m < M; m += 32) {
+          double s = 0.0;
+          for (int n = 0; n < N; ++n) s += Ld[m + n * M] * hinv[n];
+          s *= 1.0 / double(N);
+          const bool v = bal && s > 0.0 && isfinite(s);
+          us[m] = v ? fast_rcp(s) : 1.0;  // U and L-row scale 1/s
+          wsc[m] = v ? rsqrt(s) : 1.0;    // W column scale
+          if (v) lsum += log(s);
         }
-        refresh_le();
-#pragma unroll
-        for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+        __syncwarp();
+        for (int k = lane; k < M * N; k += 32) {
+          const int m = k % M, n = k / M;
+          const double l = Ld[k] * hinv[n] * us[m];  // L(m,n) mu_n / s_m
+          Ld[k] = l;
+          Le[k] = narrow_pos<R>(l * hsc[n]);
+        }
+        for (int k = lane; k < M * M; k += 32) {
+          double2 w = Wd[k];
+          const double c = wsc[k / M];
+          w.x *= c;
+          w.y *= c;
+          Wd[k] = w;
+          Wr[k] = mkc<R>(R(w.x), R(w.y));
+        }
+        lsum = warp_sum(lsum);
+        if (lane == 0) sc->logs = lsum;
+      } else if (warp == 1 && lane == 0 && record) {
+        double ld = 0.0;
+        sc->ldok = log_abs_det2<M>(Wlg, ld) ? 1 : 0;
+        sc->logdet0 = ld;
       }
       FFCA_TIC(7);
       __syncthreads();
@@ -1060,9 +1097,15 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         pass_a(false, more, record);
         FFCA_TIC(1);
         if (tid == 0) {
-          if (record)
-            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] = nll_from_res(sc->logdet);
-          if (more) {
+          if (record) {
+            if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
+              sc->status = kStatusSingularW;
+              sc->stop = 1;
+            }
+            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
+                nll_from_res(sc->logdet0 - sc->logs);
+          }
+          if (more && !sc->stop) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
             int bad = -1;
             if (!ip_update<M>(Wd, res, invT, p.seed + (unsigned long long)(it + 1), bin_index,
@@ -1071,7 +1114,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
               sc->stop = 1;
             }
 #pragma unroll
-            for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+            for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
           }
         }
         FFCA_TIC(2);
