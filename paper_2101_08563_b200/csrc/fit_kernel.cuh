@@ -39,6 +39,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "serial_math.cuh"
 
 namespace ffca {
 
@@ -197,258 +198,6 @@ struct Uniform {
     else return s[k];
   }
 };
-
-// ------------------------------------------------------------- fp64 algebra --
-// 1/x to within an ulp without the division slow path: an SFU fp32 seed on
-// the mantissa refined by two fp64 Newton steps (zero/denormal/huge fall back
-// to the IEEE division).
-__device__ __forceinline__ double fast_rcp(double x) {
-  const int hi = __double2hiint(x), lo = __double2loint(x);
-  const int e = (hi >> 20) & 0x7ff;
-  if (e == 0 || e >= 2046) return 1.0 / x;
-  const double m = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, lo);  // |m| in [1, 2)
-  double r = double(rcp_fast(float(m)));
-  r = fma(r, fma(-m, r, 1.0), r);
-  r = fma(r, fma(-m, r, 1.0), r);
-  return r * __hiloint2double((2046 - e) << 20, 0);  // * 2^(1023 - e)
-}
-
-// Everything below runs in one thread on register arrays (M is a compile-time
-// constant, every loop unrolls).  Pivot order follows Eigen::PartialPivLU
-// (largest modulus; compared as squared modulus, the same order).
-template <int M>
-__device__ __forceinline__ void lu_factor(double2 (&a)[M * M], int (&perm)[M]) {
-#pragma unroll
-  for (int k = 0; k < M; ++k) perm[k] = k;
-#pragma unroll
-  for (int k = 0; k < M; ++k) {
-    int p = k;
-    double best = cabs2(a[k + k * M]);
-#pragma unroll
-    for (int r = k + 1; r < M; ++r) {
-      const double v = cabs2(a[r + k * M]);
-      if (v > best) best = v, p = r;
-    }
-#pragma unroll
-    for (int r = k + 1; r < M; ++r) {
-      if (r == p) {
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          const double2 t = a[k + c * M];
-          a[k + c * M] = a[r + c * M];
-          a[r + c * M] = t;
-        }
-        const int t = perm[k];
-        perm[k] = perm[r];
-        perm[r] = t;
-      }
-    }
-    if (best != 0.0) {
-      const double2 piv = a[k + k * M];
-      const double s = fast_rcp(best);
-      const double2 ipiv = make_double2(piv.x * s, -piv.y * s);  // 1 / piv
-#pragma unroll
-      for (int r = k + 1; r < M; ++r) a[r + k * M] = cmul(a[r + k * M], ipiv);
-#pragma unroll
-      for (int c = k + 1; c < M; ++c)
-#pragma unroll
-        for (int r = k + 1; r < M; ++r)
-          a[r + c * M] = csub(a[r + c * M], cmul(a[r + k * M], a[k + c * M]));
-    }
-  }
-}
-
-// Solve (P^T L U) y = e_col.
-template <int M>
-__device__ __forceinline__ void lu_solve_unit(const double2 (&lu)[M * M], const int (&perm)[M],
-                                              int col, double2 (&y)[M]) {
-#pragma unroll
-  for (int k = 0; k < M; ++k) y[k] = make_double2(perm[k] == col ? 1.0 : 0.0, 0.0);
-#pragma unroll
-  for (int k = 0; k < M; ++k)
-#pragma unroll
-    for (int r = k + 1; r < M; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
-#pragma unroll
-  for (int k = M - 1; k >= 0; --k) {
-    const double2 d = lu[k + k * M];
-    const double s = fast_rcp(cabs2(d));
-    y[k] = cmul(y[k], make_double2(d.x * s, -d.y * s));
-#pragma unroll
-    for (int r = 0; r < k; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
-  }
-}
-
-// log|det W|^2 (sigmodel.cpp:118-129).  Returns false when W is numerically
-// singular (a zero or non-finite U diagonal).
-template <int M>
-__device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
-  if constexpr (M == 1) {
-    const double v = cabs2(w[0]);
-    if (!(v > 0.0) || !isfinite(v)) return false;
-    out = log(v);
-    return true;
-  } else if constexpr (M == 2) {
-    // |u00 u11|^2 of the pivoted LU equals |det W|^2; a vanishing pivot is
-    // the singular case the reference rejects.
-    const double2 w00 = w[0], w10 = w[1], w01 = w[2], w11 = w[3];
-    const double a0 = cabs2(w00), a1 = cabs2(w10);
-    const double2 det = csub(cmul(w00, w11), cmul(w01, w10));
-    const double d = cabs2(det);
-    if (!((a0 > 0.0 || a1 > 0.0) && d > 0.0) || !isfinite(d)) return false;
-    out = log(d);
-    return true;
-  } else {
-    double2 a[M * M];
-    int perm[M];
-#pragma unroll
-    for (int k = 0; k < M * M; ++k) a[k] = w[k];
-    lu_factor<M>(a, perm);
-    double prod = 1.0, acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < M; ++k) {
-      const double v = cabs2(a[k + k * M]);
-      if (!(v > 0.0) || !isfinite(v)) return false;
-      prod *= v;
-      if (k % 4 == 3 || k == M - 1) {  // batch the logs, keep the product in range
-        acc += log(prod);
-        prod = 1.0;
-      }
-    }
-    out = acc;  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
-    return true;
-  }
-}
-
-// Cold path of ip_update_w: one seeded perturbation of a column
-// (fastfca.cpp:66-69).  The generator is seeded lazily on the first restart
-// of the sweep and its state lives in shared scratch.
-static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng,
-                                               bool* seeded, PolarNormal* gauss,
-                                               unsigned long long seed, int bin) {
-  if (!*seeded) {
-    rng->seed(mix_seed(seed, bin));
-    *seeded = true;
-  }
-  double cn = 0.0;
-  for (int r = 0; r < m; ++r) cn += cabs2(wcol[r]);
-  const double mag = 1e-8 * (sqrt(cn) + 1.0);
-  for (int r = 0; r < m; ++r) {
-    const double im = (*gauss)(*rng);  // g++ evaluates Complex(g(), g()) right to left
-    const double re = (*gauss)(*rng);
-    wcol[r].x += mag * re;
-    wcol[r].y += mag * im;
-  }
-}
-
-// ip_update_w (fastfca.cpp:36-72) on the reduced weighted covariances.
-// qraw[m*M*M + ...] holds sum_t x x^H / sigma2_m packed as: (a,a) real,
-// (a,b) a<b real part at a*M+b and imaginary part at b*M+a.
-template <int M>
-__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
-                                          unsigned long long seed, int bin, Mt19937_64* rng,
-                                          int& bad_col) {
-  bool seeded = false;
-  PolarNormal gauss{0.0, false};
-  double2 wr[M * M];
-#pragma unroll
-  for (int k = 0; k < M * M; ++k) wr[k] = w[k];
-#pragma unroll 1
-  for (int col = 0; col < M; ++col) {
-    double2 q[M * M];
-    const double* p = qraw + col * M * M;
-#pragma unroll
-    for (int a = 0; a < M; ++a) {
-      q[a + a * M] = make_double2(p[a * M + a] * invT, 0.0);
-#pragma unroll
-      for (int b = a + 1; b < M; ++b) {
-        const double re = p[a * M + b] * invT, im = p[b * M + a] * invT;
-        q[a + b * M] = make_double2(re, im);   // Q(a,b) = sum x_a conj(x_b)
-        q[b + a * M] = make_double2(re, -im);  // Hermitian (symmetrize, hermitian.hpp:31-34)
-      }
-    }
-    for (int attempt = 0;; ++attempt) {
-      double2 a[M * M], wm[M];
-      double anorm = 0.0;
-#pragma unroll
-      for (int r = 0; r < M; ++r)
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double2 s = cmulc(wr[r * M], q[c * M]);
-#pragma unroll
-          for (int k = 1; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
-          a[r + c * M] = s;  // (W^H Q)(r,c)
-          anorm += cabs2(s);
-        }
-      if constexpr (M == 1) {
-        const double s = fast_rcp(cabs2(a[0]));
-        wm[0] = make_double2(a[0].x * s, -a[0].y * s);
-      } else if constexpr (M == 2) {
-        // Closed-form inverse column; same solution as the pivoted LU.
-        const double2 det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
-        const double s = fast_rcp(cabs2(det));
-        const double2 idet = make_double2(det.x * s, -det.y * s);
-        if (col == 0) {
-          wm[0] = cmul(a[3], idet);
-          wm[1] = cmul(make_double2(-a[1].x, -a[1].y), idet);
-        } else {
-          wm[0] = cmul(make_double2(-a[2].x, -a[2].y), idet);
-          wm[1] = cmul(a[0], idet);
-        }
-      } else {
-        double2 lu[M * M];
-        int perm[M];
-#pragma unroll
-        for (int k = 0; k < M * M; ++k) lu[k] = a[k];
-        lu_factor<M>(lu, perm);
-        lu_solve_unit<M>(lu, perm, col, wm);
-      }
-      double wn = 0.0, rn = 0.0;
-      bool fin = true;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        wn += cabs2(wm[k]);
-        fin = fin && isfinite(wm[k].x) && isfinite(wm[k].y);
-      }
-#pragma unroll
-      for (int r = 0; r < M; ++r) {
-        double2 s = make_double2(r == col ? -1.0 : 0.0, 0.0);
-#pragma unroll
-        for (int c = 0; c < M; ++c) s = cadd(s, cmul(a[r + c * M], wm[c]));
-        rn += cabs2(s);
-      }
-      // Residual test ||a w - e|| <= 1e-8 (||a|| ||w|| + 1) (fastfca.cpp:55-56),
-      // squared; the scale is a tolerance, so an fp32 square root suffices.
-      const double scale = double(sqrtf(float(anorm * wn))) + 1.0;
-      if (fin && rn <= 1e-16 * scale * scale) {
-        double en = 0.0;
-#pragma unroll
-        for (int r = 0; r < M; ++r) {
-          double2 qw = cmul(q[r], wm[0]);
-#pragma unroll
-          for (int c = 1; c < M; ++c) qw = cadd(qw, cmul(q[r + c * M], wm[c]));
-          en += cmulc(wm[r], qw).x;
-        }
-        if (en > 0.0 && isfinite(en)) {
-          const double s = rsqrt(en);
-#pragma unroll
-          for (int r = 0; r < M; ++r) {
-            wr[r + col * M] = make_double2(wm[r].x * s, wm[r].y * s);
-            w[r + col * M] = wr[r + col * M];
-          }
-          break;
-        }
-      }
-      if (attempt >= 1) {
-        bad_col = col;
-        return false;
-      }
-      ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
-#pragma unroll
-      for (int k = 0; k < M * M; ++k) wr[k] = w[k];
-    }
-  }
-  return true;
-}
 
 // ------------------------------------------------------------------ kernel --
 template <int M, int NT, bool EXACT, typename R>
@@ -943,7 +692,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   if (tid == 0) {
     if (record) {
       double ld = 0.0;
-      if (!log_abs_det2<M>(Wd, ld)) {
+      if (!log_abs_det2<M, R>(Wd, ld)) {
         sc->status = kStatusSingularW;
         sc->stop = 1;
       }
@@ -961,7 +710,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     if (!sc->stop && p.iters > 0) {
       // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
       int bad = -1;
-      if (!ip_update<M>(Wd, res, invT, p.seed, bin_index, rng, bad)) {
+      if (!ip_update<M, R>(Wd, res, invT, p.seed, bin_index, rng, bad)) {
         sc->status = kStatusIpSingular | (bad << 8);
         sc->stop = 1;
       }
@@ -1085,7 +834,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         if (lane == 0) sc->logs = lsum;
       } else if (warp == 1 && lane == 0 && record) {
         double ld = 0.0;
-        sc->ldok = log_abs_det2<M>(Wlg, ld) ? 1 : 0;
+        sc->ldok = log_abs_det2<M, R>(Wlg, ld) ? 1 : 0;
         sc->logdet0 = ld;
       }
       FFCA_TIC(7);
@@ -1108,7 +857,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
           if (more && !sc->stop) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
             int bad = -1;
-            if (!ip_update<M>(Wd, res, invT, p.seed + (unsigned long long)(it + 1), bin_index,
+            if (!ip_update<M, R>(Wd, res, invT, p.seed + (unsigned long long)(it + 1), bin_index,
                               rng, bad)) {
               sc->status = kStatusIpSingular | (bad << 8);
               sc->stop = 1;

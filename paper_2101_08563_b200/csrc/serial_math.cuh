@@ -1,0 +1,293 @@
+// serial_math.cuh -- the per-bin serial algebra of the fit (one thread, M x M
+// complex, registers only), templated on its arithmetic type SR.
+//
+// SR = double in the fp64 check mode: faithful to the reference's fp64
+// Eigen::PartialPivLU arithmetic up to rounding.  SR = float in the fp32
+// path: the weighted covariances it consumes are fp32-accurate sums anyway,
+// and fp32 SFU reciprocals / square roots shorten the dependent chain that
+// every thread of the CTA waits on, by ~4x versus fp64 division.  The only
+// semantic knob is the IP residual test of fastfca.cpp:55-56: the reference's
+// 1e-8 relative threshold is below fp32 rounding of a backward-stable 2x2 /
+// LU solve (~1e-7 ||a|| ||w||), so the fp32 path tests at 64 * FLT_EPSILON
+// (7.6e-6) -- still a singularity guard, restarts stay the rare event the
+// reference intends.
+#pragma once
+
+#include "common.cuh"
+
+namespace ffca {
+
+template <typename SR>
+struct SMath;
+
+template <>
+struct SMath<float> {
+  static constexpr float kResidTol2 = 7.62939453125e-06f * 7.62939453125e-06f;  // (64 eps)^2
+  __device__ static __forceinline__ float rcp(float x) { return rcp_fast(x); }
+  __device__ static __forceinline__ float rsq(float x) { return rsqrtf(x); }
+  __device__ static __forceinline__ float sq(float x) { return sqrtf(x); }
+  __device__ static __forceinline__ double log_d(float x) {
+    return double(flog2_ftz(x)) * 0.69314718055994531;
+  }
+};
+
+template <>
+struct SMath<double> {
+  static constexpr double kResidTol2 = 1e-16;  // (1e-8)^2, fastfca.cpp:56
+  // 1/x to within an ulp without the division slow path: an SFU fp32 seed on
+  // the mantissa refined by two fp64 Newton steps (zero/denormal/huge fall
+  // back to the IEEE division).
+  __device__ static __forceinline__ double rcp(double x) {
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) & 0x7ff;
+    if (e == 0 || e >= 2046) return 1.0 / x;
+    const double m = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, lo);  // |m| in [1, 2)
+    double r = double(rcp_fast(float(m)));
+    r = fma(r, fma(-m, r, 1.0), r);
+    r = fma(r, fma(-m, r, 1.0), r);
+    return r * __hiloint2double((2046 - e) << 20, 0);  // * 2^(1023 - e)
+  }
+  __device__ static __forceinline__ double rsq(double x) { return rsqrt(x); }
+  __device__ static __forceinline__ double sq(double x) { return sqrt(x); }
+  __device__ static __forceinline__ double log_d(double x) { return log(x); }
+};
+
+__device__ __forceinline__ double fast_rcp(double x) { return SMath<double>::rcp(x); }
+
+// In-place LU with partial pivoting.  Pivot order follows Eigen::PartialPivLU
+// (largest modulus; compared as squared modulus, the same order).
+template <int M, typename SR>
+__device__ __forceinline__ void lu_factor(cplx_t<SR> (&a)[M * M], int (&perm)[M]) {
+  using SC = cplx_t<SR>;
+#pragma unroll
+  for (int k = 0; k < M; ++k) perm[k] = k;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    int p = k;
+    SR best = cabs2(a[k + k * M]);
+#pragma unroll
+    for (int r = k + 1; r < M; ++r) {
+      const SR v = cabs2(a[r + k * M]);
+      if (v > best) best = v, p = r;
+    }
+#pragma unroll
+    for (int r = k + 1; r < M; ++r) {
+      if (r == p) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const SC t = a[k + c * M];
+          a[k + c * M] = a[r + c * M];
+          a[r + c * M] = t;
+        }
+        const int t = perm[k];
+        perm[k] = perm[r];
+        perm[r] = t;
+      }
+    }
+    if (best != SR(0)) {
+      const SC piv = a[k + k * M];
+      const SR s = SMath<SR>::rcp(best);
+      const SC ipiv = mkc<SR>(piv.x * s, -piv.y * s);  // 1 / piv
+#pragma unroll
+      for (int r = k + 1; r < M; ++r) a[r + k * M] = cmul(a[r + k * M], ipiv);
+#pragma unroll
+      for (int c = k + 1; c < M; ++c)
+#pragma unroll
+        for (int r = k + 1; r < M; ++r)
+          a[r + c * M] = csub(a[r + c * M], cmul(a[r + k * M], a[k + c * M]));
+    }
+  }
+}
+
+// Solve (P^T L U) y = e_col.
+template <int M, typename SR>
+__device__ __forceinline__ void lu_solve_unit(const cplx_t<SR> (&lu)[M * M], const int (&perm)[M],
+                                              int col, cplx_t<SR> (&y)[M]) {
+#pragma unroll
+  for (int k = 0; k < M; ++k) y[k] = mkc<SR>(perm[k] == col ? SR(1) : SR(0), SR(0));
+#pragma unroll
+  for (int k = 0; k < M; ++k)
+#pragma unroll
+    for (int r = k + 1; r < M; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
+#pragma unroll
+  for (int k = M - 1; k >= 0; --k) {
+    const cplx_t<SR> d = lu[k + k * M];
+    const SR s = SMath<SR>::rcp(cabs2(d));
+    y[k] = cmul(y[k], mkc<SR>(d.x * s, -d.y * s));
+#pragma unroll
+    for (int r = 0; r < k; ++r) y[r] = csub(y[r], cmul(lu[r + k * M], y[k]));
+  }
+}
+
+// log|det W|^2 (sigmodel.cpp:118-129) of the fp64 master W, computed in SR.
+// Returns false when W is numerically singular (a zero or non-finite pivot).
+template <int M, typename SR>
+__device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
+  using SC = cplx_t<SR>;
+  if constexpr (M == 1) {
+    const SR v = SR(w[0].x) * SR(w[0].x) + SR(w[0].y) * SR(w[0].y);
+    if (!(v > SR(0)) || !isfinite(v)) return false;
+    out = SMath<SR>::log_d(v);
+    return true;
+  } else if constexpr (M == 2) {
+    // |u00 u11|^2 of the pivoted LU equals |det W|^2; a vanishing pivot is
+    // the singular case the reference rejects.
+    const SC w00 = mkc<SR>(SR(w[0].x), SR(w[0].y)), w10 = mkc<SR>(SR(w[1].x), SR(w[1].y));
+    const SC w01 = mkc<SR>(SR(w[2].x), SR(w[2].y)), w11 = mkc<SR>(SR(w[3].x), SR(w[3].y));
+    const SR a0 = cabs2(w00), a1 = cabs2(w10);
+    const SR d = cabs2(csub(cmul(w00, w11), cmul(w01, w10)));
+    if (!((a0 > SR(0) || a1 > SR(0)) && d > SR(0)) || !isfinite(d)) return false;
+    out = SMath<SR>::log_d(d);
+    return true;
+  } else {
+    SC a[M * M];
+    int perm[M];
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) a[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+    lu_factor<M, SR>(a, perm);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const SR v = cabs2(a[k + k * M]);
+      if (!(v > SR(0)) || !isfinite(v)) return false;
+      acc += SMath<SR>::log_d(v);  // sum of log|u_kk|^2 = 2 * sum log|u_kk|
+    }
+    out = acc;
+    return true;
+  }
+}
+
+// Cold path of ip_update_w: one seeded perturbation of a column
+// (fastfca.cpp:66-69).  The generator is seeded lazily on the first restart
+// of the sweep and its state lives in shared scratch.
+static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng,
+                                               bool* seeded, PolarNormal* gauss,
+                                               unsigned long long seed, int bin) {
+  if (!*seeded) {
+    rng->seed(mix_seed(seed, bin));
+    *seeded = true;
+  }
+  double cn = 0.0;
+  for (int r = 0; r < m; ++r) cn += cabs2(wcol[r]);
+  const double mag = 1e-8 * (sqrt(cn) + 1.0);
+  for (int r = 0; r < m; ++r) {
+    const double im = (*gauss)(*rng);  // g++ evaluates Complex(g(), g()) right to left
+    const double re = (*gauss)(*rng);
+    wcol[r].x += mag * re;
+    wcol[r].y += mag * im;
+  }
+}
+
+// ip_update_w (fastfca.cpp:36-72) on the reduced weighted covariances.
+// qraw[m*M*M + ...] holds sum_t x x^H / sigma2_m packed as: (a,a) real,
+// (a,b) a<b real part at a*M+b and imaginary part at b*M+a.  w is the fp64
+// master W (updated in place).
+template <int M, typename SR>
+__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
+                                          unsigned long long seed, int bin, Mt19937_64* rng,
+                                          int& bad_col) {
+  using SC = cplx_t<SR>;
+  bool seeded = false;
+  PolarNormal gauss{0.0, false};
+  SC wr[M * M];
+#pragma unroll
+  for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+#pragma unroll 1
+  for (int col = 0; col < M; ++col) {
+    SC q[M * M];
+    const double* p = qraw + col * M * M;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      q[a + a * M] = mkc<SR>(SR(p[a * M + a] * invT), SR(0));
+#pragma unroll
+      for (int b = a + 1; b < M; ++b) {
+        const SR re = SR(p[a * M + b] * invT), im = SR(p[b * M + a] * invT);
+        q[a + b * M] = mkc<SR>(re, im);   // Q(a,b) = sum x_a conj(x_b)
+        q[b + a * M] = mkc<SR>(re, -im);  // Hermitian (symmetrize, hermitian.hpp:31-34)
+      }
+    }
+    for (int attempt = 0;; ++attempt) {
+      SC a[M * M], wm[M];
+      SR anorm = SR(0);
+#pragma unroll
+      for (int r = 0; r < M; ++r)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          SC s = cmulc(wr[r * M], q[c * M]);
+#pragma unroll
+          for (int k = 1; k < M; ++k) s = cadd(s, cmulc(wr[k + r * M], q[k + c * M]));
+          a[r + c * M] = s;  // (W^H Q)(r,c)
+          anorm += cabs2(s);
+        }
+      if constexpr (M == 1) {
+        const SR s = SMath<SR>::rcp(cabs2(a[0]));
+        wm[0] = mkc<SR>(a[0].x * s, -a[0].y * s);
+      } else if constexpr (M == 2) {
+        // Closed-form inverse column; the same solution as the pivoted LU.
+        const SC det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
+        const SR s = SMath<SR>::rcp(cabs2(det));
+        const SC idet = mkc<SR>(det.x * s, -det.y * s);
+        if (col == 0) {
+          wm[0] = cmul(a[3], idet);
+          wm[1] = cmul(mkc<SR>(-a[1].x, -a[1].y), idet);
+        } else {
+          wm[0] = cmul(mkc<SR>(-a[2].x, -a[2].y), idet);
+          wm[1] = cmul(a[0], idet);
+        }
+      } else {
+        SC lu[M * M];
+        int perm[M];
+#pragma unroll
+        for (int k = 0; k < M * M; ++k) lu[k] = a[k];
+        lu_factor<M, SR>(lu, perm);
+        lu_solve_unit<M, SR>(lu, perm, col, wm);
+      }
+      SR wn = SR(0), rn = SR(0);
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        wn += cabs2(wm[k]);
+        fin = fin && isfinite(wm[k].x) && isfinite(wm[k].y);
+      }
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        SC s = mkc<SR>(r == col ? SR(-1) : SR(0), SR(0));
+#pragma unroll
+        for (int c = 0; c < M; ++c) s = cadd(s, cmul(a[r + c * M], wm[c]));
+        rn += cabs2(s);
+      }
+      // Residual test ||a w - e|| <= tol (||a|| ||w|| + 1) (fastfca.cpp:55-56),
+      // squared; the scale is a tolerance, so an fp32 square root suffices.
+      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
+      if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale) {
+        SR en = SR(0);
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+          SC qw = cmul(q[r], wm[0]);
+#pragma unroll
+          for (int c = 1; c < M; ++c) qw = cadd(qw, cmul(q[r + c * M], wm[c]));
+          en += cmulc(wm[r], qw).x;
+        }
+        if (en > SR(0) && isfinite(en)) {
+          const SR s = SMath<SR>::rsq(en);
+#pragma unroll
+          for (int r = 0; r < M; ++r) {
+            wr[r + col * M] = mkc<SR>(wm[r].x * s, wm[r].y * s);
+            w[r + col * M] = make_double2(double(wr[r + col * M].x), double(wr[r + col * M].y));
+          }
+          break;
+        }
+      }
+      if (attempt >= 1) {
+        bad_col = col;
+        return false;
+      }
+      ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
+#pragma unroll
+      for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+    }
+  }
+  return true;
+}
+
+}  // namespace ffca
