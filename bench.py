@@ -4,23 +4,30 @@
                     [--impl ours|reference] [--no-cpu-baseline]
 
 A step is one full fastfca_fit (all `iters` IP+EM iterations) over the
-config's synthetic mixture(s) -- SURVEY §8(d): the work unit is one TF-bin EM
-update, throughput = B*F*T*iters / t.  Under torchrun (N > 1) the flattened
-(mixture, bin) problems are split into contiguous balanced ranges, one per
-rank (frequency sharding: no exchange during the fit); the per-bin NLL slots
-are all-gathered over NCCL after the timed region to assemble the trace.
+workload's synthetic mixtures -- SURVEY §8(d): the work unit is one TF-bin EM
+update, throughput = B*F*T*iters / t.
+
+Workload: BASELINE.json configs[1] ("c1": M=2, N=2, F=513, T=1250, 100 EM
+iterations), one mixture per GPU.  Under torchrun (N > 1) the N mixtures'
+flattened (mixture, bin) problems are split into contiguous balanced ranges,
+one per rank (frequency sharding: no exchange during the fit), so per-GPU
+work is fixed as N grows (scaling "weak"); the per-bin NLL slots are
+all-gathered over NCCL after the timed region to assemble each mixture's
+trace in bin order.  Other configs (--config c0|c2|c3|c4) are parity cases;
+c4 (256 mixtures) shards its fixed batch over the ranks (scaling "strong").
 
 value : device-resident inputs (x, H, W, L already in HBM), one fit kernel per
         step timed with CUDA events on the launching stream, L2 flushed
         between steps (a 256 MiB write), max over ranks.
 e2e   : the reference-facing C-ABI call ffca_fit with pinned HOST buffers in
         the reference's Eigen layout (complex<double> x, double W/L/H): H2D,
-        boundary pack, fit, unpack, D2H -- host clock around the synchronous
-        call, max over ranks.
+        boundary conversion, fit, unpack, D2H -- host clock around the
+        synchronous call, max over ranks.
 """
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -47,11 +54,14 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def shard(P: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous balanced range of the flattened problem index p = b*F + f."""
-    base, rem = divmod(P, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
+from paper_2101_08563_b200.shard import bin_order_trace, gather_slots, shard  # noqa: E402
+
+
+def workload(cfg, world: int):
+    """The benchmarked batch: one mixture per rank for single-mixture configs."""
+    if cfg.batch == 1 and world > 1:
+        return dataclasses.replace(cfg, batch=world), "weak"
+    return cfg, ("weak" if cfg.batch == 1 else "strong")
 
 
 class ClockSampler:
@@ -67,17 +77,20 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _sample(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                  f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=5).stdout.strip()
+            if out:
+                self.samples.append([s.strip() for s in out.split(",")])
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+            self._sample()
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -116,53 +129,48 @@ def build_inputs(cfg, lo: int, hi: int):
     return (np.concatenate(xs), np.concatenate(Ws), np.concatenate(Ls), np.concatenate(Hs))
 
 
-def cpu_baseline(cfg, args) -> dict:
-    """The oracle (fp64 restatement of the reference, all host threads) on a
-    bounded sample of the same workload: the first S bins of mixture 0, all
-    frames and iterations."""
+def oracle_sample(cfg, args):
+    """The bounded CPU sample: the first S bins of mixture 0, all frames and
+    iterations (S = 2 x host threads unless --cpu-bins)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # test infrastructure: the CPU baseline leg only
+    from paper_2101_08563_b200 import synth
     cores = oracle.default_workers()
     S = min(cfg.F, max(1, args.cpu_bins or 2 * cores))
-    from paper_2101_08563_b200 import synth
     x = synth.mixture(cfg, 0)[:S].astype(np.complex128)
     W, L, H = synth.init_params(cfg, 0)
-    _, _, _, _, _, secs = oracle.fit(x, W[:S], L[:S], H[:S], cfg.iters, record_trace=True,
-                                     workers=cores)
-    units = S * cfg.T * cfg.iters
-    return {"value": units / secs, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, "
-                      f"{cfg.iters} iters, fastfca_fit only ({secs:.2f} s)"}
+    sample = (f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, {cfg.iters} "
+              f"iters, fastfca_fit only, fp64 oracle port of the reference (the reference "
+              f"itself needs Eigen3, absent)")
+    return oracle, cores, S, (x, W[:S], L[:S], H[:S]), sample
+
+
+def cpu_baseline(cfg, args) -> dict:
+    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args)
+    _, _, _, _, _, secs = oracle.fit(x, W, L, H, cfg.iters, record_trace=True, workers=cores)
+    return {"value": S * cfg.T * cfg.iters / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": sample + f" ({secs:.2f} s)"}
 
 
 def run_reference(cfg, args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle  # the reference's CPU path (oracle port; reference unbuildable here)
-    from paper_2101_08563_b200 import synth
-    cores = oracle.default_workers()
-    S = min(cfg.F, max(1, args.cpu_bins or 2 * cores))
-    x = synth.mixture(cfg, 0)[:S].astype(np.complex128)
-    W, L, H = synth.init_params(cfg, 0)
+    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args)
     times = []
     for i in range(args.warmup + args.steps):
-        _, _, _, _, _, secs = oracle.fit(x, W[:S], L[:S], H[:S], cfg.iters, record_trace=True,
-                                         workers=cores)
+        _, _, _, _, _, secs = oracle.fit(x, W, L, H, cfg.iters, record_trace=True, workers=cores)
         if i >= args.warmup:
             times.append(secs)
-    units = S * cfg.T * cfg.iters
     tot = sum(times)
-    v = units * len(times) / tot
-    sample = (f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, {cfg.iters} "
-              f"iters per step (oracle port of the reference; the reference needs Eigen3, absent)")
+    v = S * cfg.T * cfg.iters * len(times) / tot
+    wl, scaling = workload(cfg, world)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config shapes)",
         "config": {"workload": cfg.name, "M": cfg.M, "N": cfg.N, "F": cfg.F, "T": cfg.T,
-                   "iters": cfg.iters, "batch": cfg.batch, "sample_bins": S},
+                   "iters": cfg.iters, "batch": wl.batch, "sample_bins": S},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -172,7 +180,7 @@ def run_reference(cfg, args, rank: int, world: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c1"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -184,13 +192,13 @@ def main() -> None:
     args.warmup = max(args.warmup, 3)
 
     from paper_2101_08563_b200 import synth
-    cfg = synth.CONFIGS[args.config]
+    cfg0 = synth.CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        run_reference(cfg, args, rank, world)
+        run_reference(cfg0, args, rank, world)
         return
 
     import torch
@@ -201,6 +209,7 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2101_08563_b200 import _lib
 
+    cfg, scaling = workload(cfg0, world)
     P = cfg.batch * cfg.F
     lo, hi = shard(P, world, rank)
     Pl = hi - lo
@@ -222,7 +231,7 @@ def main() -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ctx = _lib.Context(local)
     L_ = _lib.lib()
-    # A dedicated stream: every copy, flush, event and fit kernel is ordered on it
+    # A dedicated stream: every copy, flush, event and kernel is ordered on it
     # (the library launches on the stream it is given).
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -273,21 +282,33 @@ def main() -> None:
     # Trace assembly: all-gather the per-bin slots (NCCL), bin-order sums.
     st = status.cpu().numpy()
     bad = int((st >= 2).sum())
+    all_slots = gather_slots(slots, P, world, rank, dist)
     if dist:
-        sizes = [shard(P, world, r)[1] - shard(P, world, r)[0] for r in range(world)]
-        mx = max(sizes)
-        pad = torch.zeros((iters + 1, mx), dtype=torch.float64, device=dev)
-        pad[:, :Pl] = slots
-        gath = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(gath, pad)
-        all_slots = torch.cat([g[:, :n] for g, n in zip(gath, sizes)], dim=1).cpu().numpy()
         badt = torch.tensor([bad], device=dev)
         dist.all_reduce(badt)
         bad = int(badt.item())
-    else:
-        all_slots = slots.cpu().numpy()
-    trace = all_slots.reshape(iters + 1, cfg.batch, cfg.F).sum(axis=2)  # [iters+1, batch]
+    trace = bin_order_trace(all_slots, cfg.batch, cfg.F)  # [iters+1, batch]
     monotone = bool((trace[1:] <= trace[:-1] + 1e-5 * np.abs(trace[:-1])).all())
+
+    # Separation (fastfca_separate) of the fitted parameters, device path.
+    img = torch.empty((N, Pl, T, M), dtype=cdt, device=dev)
+    sep_ms = []
+    for i in range(3 + 5):
+        flush.fill_(i & 0xff)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(L_.ffca_separate_device(ctx.handle, Pl, M, N, T, prec, _lib.ptr(x_d),
+                                           _lib.ptr(W_d), _lib.ptr(L_d), _lib.ptr(H_d),
+                                           _lib.ptr(img), sp))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            sep_ms.append(e0.elapsed_time(e1))
+    sep_s = statistics.median(sep_ms) / 1e3
+    esz = 16 if fp64 else 8
+    sep_bytes = Pl * T * (esz * M + (esz // 2) * N + esz * N * M)
+    separate = {"ms": sep_s * 1e3, "bytes": int(sep_bytes), "GB_per_s": sep_bytes / sep_s / 1e9,
+                "bytes_per_frame": "x read + H read + N images written"}
 
     # e2e through the reference-facing C-ABI with pinned host buffers.
     e2e = None
@@ -300,7 +321,6 @@ def main() -> None:
         Wpin, Lpin = Wr.clone().pin_memory(), Lr.clone().pin_memory()
         nll_h = torch.zeros(iters + 1, dtype=torch.float64).pin_memory()
         d = _lib.Dims(1, Pl, M, N, T)
-        eopts = _lib.FitOpts(_lib.FLAVOR_EM, iters, 1, 0, 1, 0, prec)
         ectx = _lib.Context(local)
         times = []
         for i in range(args.warmup + args.steps):
@@ -308,7 +328,7 @@ def main() -> None:
             flush.fill_(i & 0xff)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            _lib.check(L_.ffca_fit(ectx.handle, d, eopts, _lib.ptr(xr), None, _lib.ptr(Wpin),
+            _lib.check(L_.ffca_fit(ectx.handle, d, opts, _lib.ptr(xr), None, _lib.ptr(Wpin),
                                    _lib.ptr(Lpin), _lib.ptr(Hr), _lib.ptr(nll_h), None, None))
             t1 = time.perf_counter()
             if i >= args.warmup:
@@ -322,42 +342,46 @@ def main() -> None:
         d2h = Hr.numel() * 8 + Wpin.numel() * 16 + Lpin.numel() * 8 + nll_h.numel() * 8
         e2e = {"value": P * T * iters * len(times) / et, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "ms_per_step": 1e3 * et / len(times)}
+               "ms_per_step": 1e3 * et / len(times), "launches_per_step": ectx.launches(),
+               "timing": "host clock around the synchronous C-ABI call, max over ranks"}
 
     if rank == 0:
         pk = peaks()
         b_alg = 8 * M + 8 * N  # bytes per TF-bin-iteration
         kern_s = (tot_ms / 1e3) / args.steps
-        achieved = (Pl * world) * T * iters * b_alg / kern_s / 1e9  # GB/s (whole job / world)
-        per_gpu = achieved / world
+        achieved = Pl * T * iters * b_alg / kern_s / 1e9  # per GPU (rank 0's shard)
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
-            traffic = json.loads(tp.read_text()).get(cfg.name)
+            tj = json.loads(tp.read_text()).get(cfg0.name)
+            if tj and world == 1:
+                traffic = tj
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg, args)
+            cpu = cpu_baseline(cfg0, args)
         clocks = clk.summary()
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if cfg.batch == 1 else "weak",
+            "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if not fp64 else "f64",
             "data": "synthetic (seeded, BASELINE.json config shapes; paper data unavailable)",
-            "config": {"workload": cfg.name, "M": M, "N": N, "F": cfg.F, "T": T,
+            "config": {"workload": cfg0.name, "M": M, "N": N, "F": cfg.F, "T": T,
                        "iters": iters, "batch": cfg.batch, "flavor": "em",
                        "record_trace": True, "parallelism": f"freq-shard x{world}",
                        "l2": "flushed between steps (256 MiB write)"},
-            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": per_gpu / pk["hbm_gbs"], "traffic": traffic,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "peak_source": pk["source"],
                          "algorithmic_bytes_per_unit": b_alg,
-                         "note": "algorithmic bytes (8M+8N per TF-bin-iteration) / kernel time;"
-                                 " x and H stay in shared memory across iterations, so DRAM"
-                                 " traffic is far below the algorithmic bytes"},
+                         "note": "algorithmic bytes (8M+8N per TF-bin-iteration, SURVEY 8(d)) x"
+                                 " units per launch / kernel time; x and H stay in shared memory"
+                                 " for the whole fit, so DRAM traffic (traffic) is far below the"
+                                 " algorithmic bytes"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "separate": separate,
             "clocks": clocks,
             "trace": {"nll_first": float(trace[0].sum()), "nll_last": float(trace[-1].sum()),
                       "monotone": monotone, "failed_bins": bad},
