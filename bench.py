@@ -129,16 +129,25 @@ def build_inputs(cfg, lo: int, hi: int):
     return (np.concatenate(xs), np.concatenate(Ws), np.concatenate(Ls), np.concatenate(Hs))
 
 
-def oracle_sample(cfg, args):
+def oracle_sample(cfg, args, budget_s: float = 10.0):
     """The bounded CPU sample: the first S bins of mixture 0, all frames and
-    iterations (S = 2 x host threads unless --cpu-bins)."""
+    iterations.  S = all F bins when that fits ~budget_s of fastfca_fit on all
+    host threads (calibrated on one bin), else the largest S that does."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # test infrastructure: the CPU baseline leg only
     from paper_2101_08563_b200 import synth
     cores = oracle.default_workers()
-    S = min(cfg.F, max(1, args.cpu_bins or 2 * cores))
-    x = synth.mixture(cfg, 0)[:S].astype(np.complex128)
+    xall = synth.mixture(cfg, 0)
     W, L, H = synth.init_params(cfg, 0)
+    if args.cpu_bins:
+        S = min(cfg.F, args.cpu_bins)
+    else:
+        cal_it = min(cfg.iters, 3)
+        x1 = xall[:1].astype(np.complex128)
+        _, _, _, _, _, s1 = oracle.fit(x1, W[:1], L[:1], H[:1], cal_it, workers=1)
+        per_bin = max(s1, 1e-6) * cfg.iters / cal_it
+        S = int(min(cfg.F, max(cores, budget_s * cores / per_bin)))
+    x = xall[:S].astype(np.complex128)
     sample = (f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, {cfg.iters} "
               f"iters, fastfca_fit only, fp64 oracle port of the reference (the reference "
               f"itself needs Eigen3, absent)")
@@ -155,7 +164,10 @@ def cpu_baseline(cfg, args) -> dict:
 def run_reference(cfg, args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args)
+    # Each step is a bounded sample sized so the whole --steps/--warmup run
+    # stays within about two minutes.
+    budget = min(10.0, 120.0 / (args.steps + args.warmup))
+    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args, budget_s=budget)
     times = []
     for i in range(args.warmup + args.steps):
         _, _, _, _, _, secs = oracle.fit(x, W, L, H, cfg.iters, record_trace=True, workers=cores)
@@ -180,7 +192,7 @@ def run_reference(cfg, args, rank: int, world: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c1"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
