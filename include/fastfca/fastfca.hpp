@@ -1,0 +1,60 @@
+// fastfca.hpp -- the FastFCA fit / separate entry points, B200 backend
+// (drop-in for reference proj/include/fastfca/fastfca.hpp:16-66).
+//
+// Same names, argument order, defaults and error behaviour as the reference:
+// std::invalid_argument on shape mismatch, NumericalError on a singular IP
+// system after its restart or a singular W, `init` copied, `iters == 0` and
+// silent bands return the init bit-exactly, record_trace == false returns an
+// empty trace.  Every call runs the sm_100a kernels of libffca.so (no CPU
+// fallback).  The appended GpuOptions overloads select devices (frequency
+// sharding over several GPUs, one host thread per device) and the arithmetic
+// (fp32 data path, or the fp64 check mode).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "fastfca/sigmodel.hpp"
+
+namespace fastfca {
+
+enum class LhFlavor { em, mm };  // fastfca.hpp:16
+
+struct FastFcaOptions {  // fastfca.hpp:18-21
+  bool fix_loadings = false;
+  bool normalize_scales = true;
+};
+
+struct FastFcaFitResult {  // fastfca.hpp:23-26
+  FastFcaParams params;
+  std::vector<double> nll;  // nll[0] at init, then one entry per iteration
+};
+
+enum class Precision { fp32, fp64 };
+
+struct GpuOptions {
+  std::vector<int> devices = {0};  // bins are split into contiguous ranges, one per device
+  Precision precision = Precision::fp32;
+};
+
+FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
+                             int iters, const FitOptions& fit = {},
+                             const FastFcaOptions& opts = {});
+FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
+                             int iters, const FitOptions& fit, const FastFcaOptions& opts,
+                             const GpuOptions& gpu);
+
+// A batch of independent mixtures in one launch; equal to a loop of fastfca_fit.
+std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>& covs,
+                                                const std::vector<FastFcaParams>& init,
+                                                LhFlavor flavor, int iters,
+                                                const FitOptions& fit = {},
+                                                const FastFcaOptions& opts = {},
+                                                const GpuOptions& gpu = {});
+
+// Decomposed multichannel Wiener filter (fastfca.cpp:205-223).
+std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params);
+std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params,
+                                          const GpuOptions& gpu);
+
+}  // namespace fastfca

@@ -1,0 +1,60 @@
+// sigmodel.hpp -- observation statistics and parameter containers of the
+// FastFCA C++ API (reference proj/include/fastfca/sigmodel.hpp:19-111), for
+// the block_size == 1 snapshot path the GPU fit runs.
+//
+// Deviation: sample_covs does not materialise the per-(i, j) rank-one
+// matrices `mats` (F*T M x M heap matrices, ~17 GB at BASELINE config 3); the
+// reference's hot path never reads them when snapshots exist
+// (fastfca.cpp:25-28, sigmodel.cpp:95-96).  `mats` stays in the struct, empty.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "fastfca/stft.hpp"
+#include "fastfca/types.hpp"
+
+namespace fastfca {
+
+constexpr double kPowerFloorRel = 1e-12;  // sigmodel.hpp:19
+constexpr double kVarEpsRel = 1e-8;       // sigmodel.hpp:26
+
+inline double var_eps(double data_power) {  // sigmodel.hpp:29-31
+  return std::max(kVarEpsRel * data_power, 1e-300);
+}
+
+struct FitOptions {  // sigmodel.hpp:34-38
+  int workers = 1;             // host threads (layout conversion); devices: GpuOptions
+  bool record_trace = true;    // benchmark runs disable this
+  std::uint64_t seed = 0;      // recovery restarts only
+};
+
+struct SampleCovSet {  // sigmodel.hpp:48-56 (block_size == 1)
+  int dim = 0, bins = 0, blocks = 0, frames = 0, block_size = 1;
+  std::vector<std::vector<CMat>> mats;  // not materialised (see header note)
+  std::vector<CMat> snapshots;          // [i], dim x frames
+  RVec power_scale;                     // [i], mean per-channel data power
+  bool has_snapshots() const { return !snapshots.empty(); }
+  double power(int i) const { return power_scale(i); }
+};
+
+// Snapshots + power_scale (sigmodel.cpp:17-48); the power reduction runs on
+// the GPU.  block_size != 1 throws std::invalid_argument (block-stationary
+// statistics are outside the GPU path).
+SampleCovSet sample_covs(const Spectrogram& spec, int block_size = 1);
+
+struct FastFcaParams {  // sigmodel.hpp:72-78
+  int dim = 0, bins = 0, frames = 0, sources = 0;
+  std::vector<CMat> decorr;
+  std::vector<RMat> loading;
+  std::vector<RMat> act;
+};
+
+// Negative log-likelihood (sigmodel.cpp:155-162, 215-222) evaluated on the GPU
+// in fp64 (check-mode kernels); per-bin values are summed in bin order.
+double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& params);
+double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RMat& loading,
+                        const RMat& act);
+
+}  // namespace fastfca

@@ -3,7 +3,7 @@
  * Drop-in boundary for the reference's fit / separate entry points
  * (reference proj/include/fastfca/fastfca.hpp:55-66, sigmodel.hpp:58,104).
  * The reference is a C++ library with no FFI of its own; these entry points
- * are what its C++ API (re-exposed in include/fastfca/*.hpp, implemented in
+ * are what its C++ API (re-exposed in include/fastfca/, implemented in
  * paper_2101_08563_b200/csrc/shim.cpp on top of this ABI) and any ctypes /
  * cgo / JNI binding call.  Plain pointers and sizes only.
  *
@@ -55,6 +55,12 @@ typedef struct {
   int dim;     /* M, 1..8 */
   int sources; /* N, 1..16 */
   int frames;  /* T */
+  /* Restart-seed numbering (fastfca.cpp:40 seeds bin i with mix_seed(seed+t, i)):
+   * when the call covers bins [first_bin, first_bin + bins) of a mixture with
+   * mixture_bins bins (frequency sharding), pass them so restarts draw the
+   * reference's streams.  0 / 0 for a whole mixture. */
+  int first_bin;
+  int mixture_bins;
 } ffca_dims;
 
 typedef struct {

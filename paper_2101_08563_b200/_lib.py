@@ -48,7 +48,8 @@ class CudaError(FfcaError):
 
 class Dims(C.Structure):
     _fields_ = [("batch", C.c_int), ("bins", C.c_int), ("dim", C.c_int),
-                ("sources", C.c_int), ("frames", C.c_int)]
+                ("sources", C.c_int), ("frames", C.c_int), ("first_bin", C.c_int),
+                ("mixture_bins", C.c_int)]
 
 
 class FitOpts(C.Structure):

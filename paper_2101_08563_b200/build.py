@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-I", str(ROOT / "include"),
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-class-memaccess", "-I", str(ROOT / "include"),
             "-I", "/usr/local/cuda/include"]
 
 

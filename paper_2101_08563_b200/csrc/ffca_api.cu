@@ -168,7 +168,11 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   fp.nprob = P;
   fp.N = N;
   fp.T = T;
-  fp.F = d->bins;
+  // Restart seeds use the bin's index within its full mixture
+  // (fastfca.cpp:40): a sub-range of a mixture passes its first bin and the
+  // mixture's bin count.
+  fp.F = d->mixture_bins > 0 ? d->mixture_bins : d->bins;
+  fp.seed_bin0 = d->first_bin;
   fp.prob_offset = 0;
   fp.x = xs;
   fp.H = hs;
@@ -403,6 +407,7 @@ int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_
   fp.T = frames;
   fp.F = bins_per_mixture;
   fp.prob_offset = prob_offset;
+  fp.seed_bin0 = prob_offset % bins_per_mixture;
   fp.x = x_dev;
   fp.H = H_dev;
   fp.W = reinterpret_cast<double2*>(W);

@@ -46,8 +46,9 @@ namespace ffca {
 struct FitParams {
   int nprob;        // problems in this launch (= gridDim.x)
   int N, T;         // sources, frames
-  int F;            // bins per mixture (restart seed index i = global % F)
-  int prob_offset;  // global problem index of blockIdx.x == 0
+  int F;            // bins per mixture (restart seed index i = (seed_bin0 + b) % F)
+  int prob_offset;  // global problem index of blockIdx.x == 0 (NLL slot column)
+  int seed_bin0;    // bin index of blockIdx.x == 0 within its mixture's numbering
   const void* x;    // R2 [nprob][T][M]
   void* H;          // R  [nprob][T][N]   in/out
   void* work;       // R  [nprob][T][2M]  scratch (streaming mode only)
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const R eps = R(sc->eps);
   const double invT = 1.0 / double(T);
   const bool update_loading = !p.fix_loadings;
-  const int bin_index = (p.prob_offset + b) % p.F;
+  const int bin_index = (p.seed_bin0 + b) % p.F;  // mix_seed index (fastfca.cpp:40)
   // Phase timing: diagnostics builds only (-DFFCA_PHASE_TIMING, see build.py);
   // the counters would otherwise cost live registers across the whole kernel.
 #ifdef FFCA_PHASE_TIMING

@@ -1,0 +1,329 @@
+// shim.cpp -- the reference's C++ API (include/fastfca/*.hpp) on top of the
+// C ABI (include/ffca.h).  Host work only: validation with the reference's
+// exceptions, gathering the per-bin containers into the contiguous buffers
+// the ABI takes, and one host thread per device for frequency sharding.
+// All arithmetic runs in libffca.so's sm_100a kernels.
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "fastfca/fastfca.hpp"
+#include "ffca.h"
+
+namespace fastfca {
+
+namespace {
+
+void raise(int rc) {
+  if (rc == FFCA_OK) return;
+  const std::string msg = ffca_last_error();
+  if (rc == FFCA_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == FFCA_NUMERICAL) throw NumericalError(msg);
+  throw std::runtime_error("ffca: " + msg);
+}
+
+// One context per (host thread, device): contexts are not thread-safe.
+ffca_ctx* context(int device) {
+  struct Holder {
+    std::unordered_map<int, ffca_ctx*> m;
+    ~Holder() {
+      for (auto& kv : m) ffca_ctx_destroy(kv.second);
+    }
+  };
+  thread_local Holder h;
+  auto it = h.m.find(device);
+  if (it != h.m.end()) return it->second;
+  ffca_ctx* c = nullptr;
+  raise(ffca_ctx_create(device, &c));
+  h.m[device] = c;
+  return c;
+}
+
+int prec(const GpuOptions& g) {
+  return g.precision == Precision::fp64 ? FFCA_PREC_FP64 : FFCA_PREC_FP32;
+}
+
+// Contiguous host copies of bins [lo, hi) in the ABI's (reference) layout.
+struct Packed {
+  std::vector<double> x, power, W, L, H;
+};
+
+void pack_bins(const SampleCovSet& covs, const FastFcaParams& p, int lo, int hi, Packed& out) {
+  const int M = covs.dim, N = p.sources, T = covs.blocks, n = hi - lo;
+  out.x.resize(size_t(n) * T * M * 2);
+  out.power.resize(n);
+  out.W.resize(size_t(n) * M * M * 2);
+  out.L.resize(size_t(n) * M * N);
+  out.H.resize(size_t(n) * N * T);
+  for (int i = lo; i < hi; ++i) {
+    const size_t k = size_t(i - lo);
+    std::memcpy(out.x.data() + k * T * M * 2, covs.snapshots[i].data(), sizeof(double) * T * M * 2);
+    out.power[k] = covs.power(i);
+    std::memcpy(out.W.data() + k * M * M * 2, p.decorr[i].data(), sizeof(double) * M * M * 2);
+    std::memcpy(out.L.data() + k * M * N, p.loading[i].data(), sizeof(double) * M * N);
+    std::memcpy(out.H.data() + k * N * T, p.act[i].data(), sizeof(double) * N * T);
+  }
+}
+
+void unpack_bins(const Packed& in, int lo, int hi, FastFcaParams& p) {
+  const int M = p.dim, N = p.sources, T = p.frames;
+  for (int i = lo; i < hi; ++i) {
+    const size_t k = size_t(i - lo);
+    std::memcpy(p.decorr[i].data(), in.W.data() + k * M * M * 2, sizeof(double) * M * M * 2);
+    std::memcpy(p.loading[i].data(), in.L.data() + k * M * N, sizeof(double) * M * N);
+    std::memcpy(p.act[i].data(), in.H.data() + k * N * T, sizeof(double) * N * T);
+  }
+}
+
+void check_fit_shapes(const SampleCovSet& covs, const FastFcaParams& init) {
+  // fastfca.cpp:150-152
+  if (init.dim != covs.dim || init.bins != covs.bins || init.frames != covs.blocks)
+    throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
+  if (!covs.has_snapshots() || int(covs.snapshots.size()) != covs.bins ||
+      covs.power_scale.size() != covs.bins)
+    throw std::invalid_argument("fastfca_fit: covariance set has no snapshots (block_size > 1)");
+  if (int(init.decorr.size()) != init.bins || int(init.loading.size()) != init.bins ||
+      int(init.act.size()) != init.bins)
+    throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
+  for (int i = 0; i < init.bins; ++i)
+    if (init.decorr[i].rows() != init.dim || init.decorr[i].cols() != init.dim ||
+        init.loading[i].rows() != init.dim || init.loading[i].cols() != init.sources ||
+        init.act[i].rows() != init.sources || init.act[i].cols() != init.frames ||
+        covs.snapshots[i].rows() != covs.dim || covs.snapshots[i].cols() != covs.blocks)
+      throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
+}
+
+ffca_fit_opts fit_opts(LhFlavor flavor, int iters, const FitOptions& fit,
+                       const FastFcaOptions& opts, const GpuOptions& gpu) {
+  ffca_fit_opts o{};
+  o.flavor = flavor == LhFlavor::em ? FFCA_FLAVOR_EM : FFCA_FLAVOR_MM;
+  o.iters = iters;
+  o.record_trace = fit.record_trace ? 1 : 0;
+  o.seed = fit.seed;
+  o.normalize_scales = opts.normalize_scales ? 1 : 0;
+  o.fix_loadings = opts.fix_loadings ? 1 : 0;
+  o.precision = prec(gpu);
+  return o;
+}
+
+// Run fn(d, lo, hi) for contiguous balanced ranges of `count`, one host
+// thread per device; rethrow the first error on the caller (parallel.cpp:30-44).
+template <typename Fn>
+void over_devices(const std::vector<int>& devs, int count, Fn fn) {
+  const int G = std::max(1, std::min<int>(int(devs.size()), count));
+  if (G == 1) {
+    fn(devs.empty() ? 0 : devs[0], 0, count);
+    return;
+  }
+  std::vector<std::exception_ptr> errs(G);
+  std::vector<std::thread> th;
+  const int base = count / G, rem = count % G;
+  int lo = 0;
+  for (int g = 0; g < G; ++g) {
+    const int hi = lo + base + (g < rem ? 1 : 0);
+    th.emplace_back([&, g, lo, hi] {
+      try {
+        fn(devs[g], lo, hi);
+      } catch (...) {
+        errs[g] = std::current_exception();
+      }
+    });
+    lo = hi;
+  }
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- sigmodel --
+
+SampleCovSet sample_covs(const Spectrogram& spec, int block_size) {
+  if (spec.bins == 0 || spec.frames == 0 || spec.channels == 0)
+    throw std::invalid_argument("sample_covs: empty spectrogram");
+  if (block_size < 1) throw std::invalid_argument("sample_covs: block size must be >= 1");
+  if (block_size != 1)
+    throw std::invalid_argument(
+        "sample_covs: block-stationary statistics (block_size > 1) are outside the GPU path");
+  SampleCovSet covs;
+  covs.dim = spec.channels;
+  covs.bins = spec.bins;
+  covs.frames = spec.frames;
+  covs.blocks = spec.frames;
+  covs.block_size = 1;
+  covs.snapshots = spec.f;
+  std::vector<double> x(size_t(spec.bins) * spec.frames * spec.channels * 2);
+  for (int i = 0; i < spec.bins; ++i)
+    std::memcpy(x.data() + size_t(i) * spec.frames * spec.channels * 2, spec.f[i].data(),
+                sizeof(double) * spec.frames * spec.channels * 2);
+  std::vector<double> pw(spec.bins);
+  ffca_dims d{1, spec.bins, spec.channels, 1, spec.frames, 0, 0};
+  raise(ffca_power_scale(context(0), &d, x.data(), pw.data()));
+  covs.power_scale = RVec::Zero(spec.bins);
+  for (int i = 0; i < spec.bins; ++i) covs.power_scale(i) = pw[i];
+  return covs;
+}
+
+double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& p) {
+  if (covs.dim != p.dim || covs.bins != p.bins || covs.blocks != p.frames)
+    throw std::invalid_argument("nll: covariance/parameter shape mismatch");  // sigmodel.cpp:226-229
+  Packed pk;
+  pack_bins(covs, p, 0, covs.bins, pk);
+  std::vector<double> out(covs.bins);
+  ffca_dims d{1, covs.bins, covs.dim, p.sources, covs.blocks, 0, 0};
+  raise(ffca_nll_bins(context(0), &d, FFCA_PREC_FP64, pk.x.data(), pk.W.data(), pk.L.data(),
+                      pk.H.data(), out.data()));
+  double acc = 0.0;
+  for (double v : out) acc += v;  // bin order
+  return acc;
+}
+
+double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RMat& loading,
+                        const RMat& act) {
+  FastFcaParams one;
+  one.dim = covs.dim, one.bins = 1, one.frames = covs.blocks, one.sources = int(loading.cols());
+  one.decorr = {w};
+  one.loading = {loading};
+  one.act = {act};
+  SampleCovSet c1;
+  c1.dim = covs.dim, c1.bins = 1, c1.frames = covs.frames, c1.blocks = covs.blocks;
+  c1.snapshots = {covs.snapshots.at(i)};
+  c1.power_scale = RVec::Zero(1);
+  c1.power_scale(0) = covs.power(i);
+  return fastfca_nll(c1, one);
+}
+
+// ---------------------------------------------------------------- fastfca --
+
+FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
+                             int iters, const FitOptions& fit, const FastFcaOptions& opts) {
+  return fastfca_fit(covs, init, flavor, iters, fit, opts, GpuOptions{});
+}
+
+FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
+                             int iters, const FitOptions& fit, const FastFcaOptions& opts,
+                             const GpuOptions& gpu) {
+  check_fit_shapes(covs, init);
+  if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
+  FastFcaFitResult result;
+  result.params = init;  // fastfca.cpp:153-154
+  const int F = covs.bins;
+  const ffca_fit_opts o = fit_opts(flavor, iters, fit, opts, gpu);
+  std::vector<double> slots(fit.record_trace ? size_t(iters + 1) * F : 0);
+  over_devices(gpu.devices, F, [&](int dev, int lo, int hi) {
+    Packed pk;
+    pack_bins(covs, init, lo, hi, pk);
+    const int n = hi - lo;
+    std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
+    ffca_dims d{1, n, covs.dim, init.sources, covs.blocks, lo, F};
+    raise(ffca_fit(context(dev), &d, &o, pk.x.data(), pk.power.data(), pk.W.data(), pk.L.data(),
+                   pk.H.data(), nullptr, fit.record_trace ? sl.data() : nullptr, nullptr));
+    if (iters > 0) unpack_bins(pk, lo, hi, result.params);
+    for (int t = 0; fit.record_trace && t <= iters; ++t)
+      for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
+  });
+  if (fit.record_trace) {  // fastfca.cpp:186-189, bin order
+    result.nll.assign(iters + 1, 0.0);
+    for (int t = 0; t <= iters; ++t) {
+      double s = 0.0;
+      for (int i = 0; i < F; ++i) s += slots[size_t(t) * F + i];
+      result.nll[t] = s;
+    }
+  }
+  return result;
+}
+
+std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>& covs,
+                                                const std::vector<FastFcaParams>& init,
+                                                LhFlavor flavor, int iters,
+                                                const FitOptions& fit,
+                                                const FastFcaOptions& opts,
+                                                const GpuOptions& gpu) {
+  if (covs.size() != init.size())
+    throw std::invalid_argument("fastfca_fit_batch: covariance/init count mismatch");
+  const int B = int(covs.size());
+  std::vector<FastFcaFitResult> out(B);
+  if (B == 0) return out;
+  for (int b = 0; b < B; ++b) {
+    check_fit_shapes(covs[b], init[b]);
+    if (covs[b].dim != covs[0].dim || covs[b].bins != covs[0].bins ||
+        covs[b].blocks != covs[0].blocks || init[b].sources != init[0].sources)
+      throw std::invalid_argument("fastfca_fit_batch: mixtures must share one shape");
+  }
+  if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
+  const ffca_fit_opts o = fit_opts(flavor, iters, fit, opts, gpu);
+  const int F = covs[0].bins;
+  for (int b = 0; b < B; ++b) out[b].params = init[b];
+  over_devices(gpu.devices, B, [&](int dev, int lo, int hi) {  // whole mixtures per device
+    const int nb = hi - lo;
+    std::vector<Packed> pk(nb);
+    Packed all;
+    for (int b = lo; b < hi; ++b) {
+      pack_bins(covs[b], init[b], 0, F, pk[b - lo]);
+      using Field = std::vector<double> Packed::*;
+      for (Field v : {&Packed::x, &Packed::power, &Packed::W, &Packed::L, &Packed::H})
+        (all.*v).insert((all.*v).end(), (pk[b - lo].*v).begin(), (pk[b - lo].*v).end());
+    }
+    std::vector<double> nll(fit.record_trace ? size_t(nb) * (iters + 1) : 0);
+    ffca_dims d{nb, F, covs[0].dim, init[0].sources, covs[0].blocks, 0, 0};
+    raise(ffca_fit(context(dev), &d, &o, all.x.data(), all.power.data(), all.W.data(),
+                   all.L.data(), all.H.data(), fit.record_trace ? nll.data() : nullptr, nullptr,
+                   nullptr));
+    if (iters > 0) {
+      const int M = covs[0].dim, N = init[0].sources, T = covs[0].blocks;
+      for (int b = lo; b < hi; ++b) {
+        Packed one;
+        const size_t k = size_t(b - lo);
+        one.W.assign(all.W.begin() + k * F * M * M * 2, all.W.begin() + (k + 1) * F * M * M * 2);
+        one.L.assign(all.L.begin() + k * F * M * N, all.L.begin() + (k + 1) * F * M * N);
+        one.H.assign(all.H.begin() + k * F * N * T, all.H.begin() + (k + 1) * F * N * T);
+        unpack_bins(one, 0, F, out[b].params);
+      }
+    }
+    if (fit.record_trace)
+      for (int b = lo; b < hi; ++b)
+        out[b].nll.assign(nll.begin() + size_t(b - lo) * (iters + 1),
+                          nll.begin() + size_t(b - lo + 1) * (iters + 1));
+  });
+  return out;
+}
+
+std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params) {
+  return fastfca_separate(spec, params, GpuOptions{});
+}
+
+std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params,
+                                          const GpuOptions& gpu) {
+  if (spec.channels != params.dim || spec.bins != params.bins || spec.frames != params.frames)
+    throw std::invalid_argument("fastfca_separate: shape mismatch");  // fastfca.cpp:207-209
+  const int M = spec.channels, F = spec.bins, T = spec.frames, N = params.sources;
+  std::vector<Spectrogram> images(N, Spectrogram::zero(M, F, T));
+  over_devices(gpu.devices, F, [&](int dev, int lo, int hi) {
+    const int n = hi - lo;
+    std::vector<double> x(size_t(n) * T * M * 2), W(size_t(n) * M * M * 2), L(size_t(n) * M * N),
+        H(size_t(n) * N * T), img(size_t(N) * n * T * M * 2);
+    for (int i = lo; i < hi; ++i) {
+      const size_t k = size_t(i - lo);
+      std::memcpy(x.data() + k * T * M * 2, spec.f[i].data(), sizeof(double) * T * M * 2);
+      std::memcpy(W.data() + k * M * M * 2, params.decorr[i].data(), sizeof(double) * M * M * 2);
+      std::memcpy(L.data() + k * M * N, params.loading[i].data(), sizeof(double) * M * N);
+      std::memcpy(H.data() + k * N * T, params.act[i].data(), sizeof(double) * N * T);
+    }
+    ffca_dims d{1, n, M, N, T, lo, F};
+    raise(ffca_separate(context(dev), &d, prec(gpu), x.data(), W.data(), L.data(), H.data(),
+                        img.data()));
+    for (int s = 0; s < N; ++s)
+      for (int i = lo; i < hi; ++i)
+        std::memcpy(images[s].f[i].data(), img.data() + (size_t(s) * n + (i - lo)) * T * M * 2,
+                    sizeof(double) * T * M * 2);
+  });
+  return images;
+}
+
+}  // namespace fastfca

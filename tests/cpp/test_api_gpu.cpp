@@ -1,0 +1,234 @@
+// test_api_gpu.cpp -- the reference's C++ API (include/fastfca/*.hpp) on the
+// B200 backend, checked against the fp64 oracle with the reference tests'
+// own generators (tests/testutil.hpp, tests/test_fastfca.cpp:16-46).
+// Built and run by tests/test_cpp_api.py (gpu-marked).  Exit code 0 = pass.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "fastfca/fastfca.hpp"
+#include "oracle.hpp"
+
+namespace {
+
+int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                         \
+  do {                                                                      \
+    ++g_checks;                                                             \
+    if (!(cond)) {                                                          \
+      ++g_fail;                                                             \
+      std::printf("  FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);         \
+    }                                                                       \
+  } while (0)
+
+using fastfca::CMat;
+using fastfca::Complex;
+using fastfca::RMat;
+
+Complex crandn(std::mt19937& rng) {
+  std::normal_distribution<double> d(0.0, 1.0);
+  return Complex(d(rng), d(rng)) / std::sqrt(2.0);
+}
+double log_uniform(std::mt19937& rng, double lo, double hi) {
+  std::uniform_real_distribution<double> d(std::log(lo), std::log(hi));
+  return std::exp(d(rng));
+}
+
+// test_fastfca.cpp:16-30 (W = I + 0.5 CN, L and H log-uniform on [0.3, 3]).
+fastfca::FastFcaParams random_params(int dim, int bins, int frames, int sources,
+                                     std::mt19937& rng) {
+  fastfca::FastFcaParams p;
+  p.dim = dim, p.bins = bins, p.frames = frames, p.sources = sources;
+  for (int i = 0; i < bins; ++i) {
+    CMat w = CMat::Identity(dim, dim);
+    for (int c = 0; c < dim; ++c)
+      for (int r = 0; r < dim; ++r) w(r, c) += 0.5 * crandn(rng);
+    RMat l(dim, sources), h(sources, frames);
+    for (int c = 0; c < sources; ++c)
+      for (int r = 0; r < dim; ++r) l(r, c) = log_uniform(rng, 0.3, 3.0);
+    for (int c = 0; c < frames; ++c)
+      for (int r = 0; r < sources; ++r) h(r, c) = log_uniform(rng, 0.3, 3.0);
+    p.decorr.push_back(w);
+    p.loading.push_back(l);
+    p.act.push_back(h);
+  }
+  return p;
+}
+
+// test_fastfca.cpp:33-46: y ~ CN(0, diag(LH)), x = W^-H y (solved with the
+// oracle's pivoted LU), rounded to complex64 so both paths see identical data.
+fastfca::Spectrogram sample_jd_model(const fastfca::FastFcaParams& t, std::mt19937& rng) {
+  fastfca::Spectrogram s = fastfca::Spectrogram::zero(t.dim, t.bins, t.frames);
+  for (int i = 0; i < t.bins; ++i) {
+    oracle::CMat wh(t.dim, t.dim);
+    for (int c = 0; c < t.dim; ++c)
+      for (int r = 0; r < t.dim; ++r) wh(r, c) = std::conj(t.decorr[i](c, r));
+    oracle::PartialPivLU lu(wh);
+    for (int j = 0; j < t.frames; ++j) {
+      std::vector<Complex> y(t.dim);
+      for (int k = 0; k < t.dim; ++k) {
+        double s2 = 0.0;
+        for (int n = 0; n < t.sources; ++n) s2 += t.loading[i](k, n) * t.act[i](n, j);
+        y[k] = std::sqrt(s2) * crandn(rng);
+      }
+      const auto x = lu.solve(y);
+      for (int k = 0; k < t.dim; ++k)
+        s.f[i](k, j) = Complex(float(x[k].real()), float(x[k].imag()));
+    }
+  }
+  return s;
+}
+
+oracle::SampleCovSet oracle_covs(const fastfca::Spectrogram& s) {
+  std::vector<Complex> x(size_t(s.bins) * s.frames * s.channels);
+  for (int i = 0; i < s.bins; ++i)
+    for (int j = 0; j < s.frames; ++j)
+      for (int k = 0; k < s.channels; ++k) x[(size_t(i) * s.frames + j) * s.channels + k] = s.f[i](k, j);
+  return oracle::sample_covs(s.channels, s.bins, s.frames, x.data());
+}
+
+oracle::FastFcaParams oracle_params(const fastfca::FastFcaParams& p) {
+  oracle::FastFcaParams o;
+  o.dim = p.dim, o.bins = p.bins, o.frames = p.frames, o.sources = p.sources;
+  for (int i = 0; i < p.bins; ++i) {
+    oracle::CMat w(p.dim, p.dim);
+    for (int c = 0; c < p.dim; ++c)
+      for (int r = 0; r < p.dim; ++r) w(r, c) = p.decorr[i](r, c);
+    oracle::RMat l(p.dim, p.sources), h(p.sources, p.frames);
+    for (int c = 0; c < p.sources; ++c)
+      for (int r = 0; r < p.dim; ++r) l(r, c) = p.loading[i](r, c);
+    for (int c = 0; c < p.frames; ++c)
+      for (int r = 0; r < p.sources; ++r) h(r, c) = p.act[i](r, c);
+    o.decorr.push_back(w), o.loading.push_back(l), o.act.push_back(h);
+  }
+  return o;
+}
+
+double max_rel(const std::vector<double>& a, const std::vector<double>& b) {
+  double m = 0.0;
+  for (size_t k = 0; k < a.size(); ++k) m = std::max(m, std::abs(a[k] - b[k]) / std::abs(b[k]));
+  return a.size() == b.size() ? m : 1e300;
+}
+
+}  // namespace
+
+int main() {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);
+  // ---- fit: both flavors, both precisions, against the oracle trace
+  // (test_fastfca.cpp:230-259 shapes: M=3, F=4, T=120, N=3, 50 iterations).
+  std::mt19937 rng(69);
+  const auto truth = random_params(3, 4, 120, 3, rng);
+  const auto spec = sample_jd_model(truth, rng);
+  const auto covs = fastfca::sample_covs(spec, 1);
+  const auto ocovs = oracle_covs(spec);
+  for (int i = 0; i < covs.bins; ++i)
+    CHECK(std::abs(covs.power(i) - ocovs.power(i)) <= 1e-13 * ocovs.power(i));
+  for (auto flavor : {fastfca::LhFlavor::em, fastfca::LhFlavor::mm}) {
+    const auto init = random_params(3, 4, 120, 3, rng);
+    const auto ref = oracle::fastfca_fit(
+        ocovs, oracle_params(init),
+        flavor == fastfca::LhFlavor::em ? oracle::LhFlavor::em : oracle::LhFlavor::mm, 50);
+    for (auto pr : {fastfca::Precision::fp64, fastfca::Precision::fp32}) {
+      fastfca::GpuOptions g;
+      g.precision = pr;
+      const auto fit = fastfca::fastfca_fit(covs, init, flavor, 50, {}, {}, g);
+      const double tol = pr == fastfca::Precision::fp64 ? 1e-10 : 1e-5;
+      const double err = max_rel(fit.nll, ref.nll);
+      std::printf("fit flavor=%d prec=%d max rel NLL err %.3e\n", int(flavor), int(pr), err);
+      CHECK(err <= tol);
+      // fastfca_nll(returned params) == nll.back() (test_fastfca.cpp:245-246)
+      if (pr == fastfca::Precision::fp64) {
+        const double back = fastfca::fastfca_nll(covs, fit.params);
+        CHECK(std::abs(back - fit.nll.back()) <= 1e-10 * std::abs(fit.nll.back()));
+      }
+    }
+  }
+  // ---- frequency sharding over two device contexts (threads) == one device,
+  // bit for bit (per-bin slots are summed in bin order).
+  {
+    const auto init = random_params(3, 4, 120, 3, rng);
+    fastfca::GpuOptions one, two;
+    two.devices = {0, 0};
+    const auto a = fastfca::fastfca_fit(covs, init, fastfca::LhFlavor::em, 20, {}, {}, one);
+    const auto b = fastfca::fastfca_fit(covs, init, fastfca::LhFlavor::em, 20, {}, {}, two);
+    CHECK(a.nll == b.nll);
+    for (int i = 0; i < covs.bins; ++i)
+      for (long k = 0; k < a.params.act[i].size(); ++k)
+        CHECK(a.params.act[i](k) == b.params.act[i](k));
+    // batch == loop of fastfca_fit
+    const auto batch = fastfca::fastfca_fit_batch({covs, covs}, {init, init},
+                                                  fastfca::LhFlavor::em, 20);
+    CHECK(batch.size() == 2 && batch[0].nll == a.nll && batch[1].nll == a.nll);
+  }
+  // ---- iters == 0 returns the init bit-exactly (test_fastfca.cpp:273-284)
+  {
+    const auto p = random_params(2, 2, 10, 2, rng);
+    const auto s = sample_jd_model(p, rng);
+    const auto fit = fastfca::fastfca_fit(fastfca::sample_covs(s), p, fastfca::LhFlavor::mm, 0);
+    CHECK(fit.nll.size() == 1);
+    for (int i = 0; i < 2; ++i)
+      for (long k = 0; k < p.act[i].size(); ++k) CHECK(fit.params.act[i](k) == p.act[i](k));
+  }
+  // ---- separation partitions the mixture (test_fastfca.cpp:342-359) and
+  // matches the oracle
+  {
+    const auto p = random_params(3, 3, 12, 4, rng);
+    const auto s = sample_jd_model(p, rng);
+    fastfca::GpuOptions g;
+    g.precision = fastfca::Precision::fp64;
+    const auto img = fastfca::fastfca_separate(s, p, g);
+    const auto ref = oracle::fastfca_separate(oracle_covs(s), oracle_params(p));
+    CHECK(img.size() == 4);
+    double num = 0.0, den = 0.0, part = 0.0, xn = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 12; ++j)
+        for (int k = 0; k < 3; ++k) {
+          Complex tot = 0.0;
+          for (int n = 0; n < 4; ++n) {
+            num += std::norm(img[n].f[i](k, j) - ref[n][i](k, j));
+            den += std::norm(ref[n][i](k, j));
+            tot += img[n].f[i](k, j);
+          }
+          part += std::norm(tot - s.f[i](k, j));
+          xn += std::norm(s.f[i](k, j));
+        }
+    std::printf("separate rel L2 %.3e partition %.3e\n", std::sqrt(num / den), std::sqrt(part / xn));
+    CHECK(std::sqrt(num / den) <= 1e-10);
+    CHECK(std::sqrt(part / xn) <= 1e-9);
+  }
+  // ---- errors: shape mismatch -> std::invalid_argument; singular W ->
+  // NumericalError (fastfca.cpp:150-152, sigmodel.cpp:124-125)
+  {
+    auto p = random_params(2, 3, 20, 2, rng);
+    const auto s = sample_jd_model(p, rng);
+    const auto c = fastfca::sample_covs(s);
+    bool threw = false;
+    try {
+      auto bad = p;
+      bad.frames = 19;
+      fastfca::fastfca_fit(c, bad, fastfca::LhFlavor::em, 2);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      p.decorr[1] = CMat::Zero(2, 2);
+      fastfca::fastfca_fit(c, p, fastfca::LhFlavor::em, 2);
+    } catch (const fastfca::NumericalError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      fastfca::sample_covs(fastfca::Spectrogram{}, 1);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
