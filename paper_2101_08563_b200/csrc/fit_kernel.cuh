@@ -38,6 +38,8 @@
 // launch shape, so per-bin results do not depend on how bins are sharded.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "serial_math.cuh"
 
@@ -60,6 +62,7 @@ struct FitParams {
   int* status;      // [nprob]: 0 ok, 1 silent band, 2 IP singular, 3 singular W
   int iters, flavor, record, normalize, fix_loadings, resident;
   int nc;           // MM: sources per L-reduction chunk
+  int tloc;         // frames held per CTA (= T, or ceil(T/C) for a C-CTA cluster)
   unsigned long long* timing;  // optional per-problem phase cycle counters [nprob][16]
   unsigned long long seed;
 };
@@ -96,7 +99,8 @@ template <int M, int NT, typename R>
 struct FitSmem {
   int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
       off_us, off_hsum,
-      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_scal, off_big, kred, kres, total;
+      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_scal, off_big, kred, kres,
+      total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
     using S = Split<M>;
@@ -124,6 +128,7 @@ struct FitSmem {
     off_redb = o; o = al(o + 2 * nwarps * kred * 8);    // sweep partials, double-buffered
     off_res = o; o = al(o + kres * 8);
     off_rng = o; o = al(o + (int)sizeof(Mt19937_64));   // restart generator (cold)
+    off_cx = o; o = al(o + 2 * kres * 8);               // cluster exchange, double-buffered
     off_scal = o; o = al(o + 64);
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
@@ -201,7 +206,10 @@ struct Uniform {
 };
 
 // ------------------------------------------------------------------ kernel --
-template <int M, int NT, bool EXACT, typename R>
+// CL: the bin's frames are split over a thread-block cluster (one CTA per
+// frame range, cluster rank order); reductions add a DSMEM exchange and every
+// CTA repeats the (identical) serial algebra, so no broadcast is needed.
+template <int M, int NT, bool EXACT, typename R, bool CL>
 __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
@@ -214,9 +222,19 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
   const int lane = tid & 31, warp = tid >> 5;
   const int N = EXACT ? NT : p.N;
-  const int T = p.T;
-  const int b = blockIdx.x;
-  const FitSmem<M, NT, R> lay(nwarps, N, T, p.nc, p.resident != 0);
+  const int T = p.T;  // the bin's frame count (all global formulas use T)
+  int crank = 0, csize = 1;
+  if constexpr (CL) {
+    namespace cg = cooperative_groups;
+    const cg::cluster_group cl = cg::this_cluster();
+    crank = int(cl.block_rank());
+    csize = int(cl.num_blocks());
+  }
+  const int b = CL ? blockIdx.x / csize : blockIdx.x;
+  const int t0g = int((long long)T * crank / csize);  // this CTA's frames [t0g, t0g + Tl)
+  const int Tl = int((long long)T * (crank + 1) / csize) - t0g;
+  const bool lead = crank == 0;  // writes the per-bin outputs
+  const FitSmem<M, NT, R> lay(nwarps, N, p.tloc, p.nc, p.resident != 0);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
   double* wsc = reinterpret_cast<double*>(smem + lay.off_wsc);
@@ -236,34 +254,57 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   double* res = reinterpret_cast<double*>(smem + lay.off_res);
   Mt19937_64* rng = reinterpret_cast<Mt19937_64*>(smem + lay.off_rng);
   Scalars* sc = reinterpret_cast<Scalars*>(smem + lay.off_scal);
-  const int kred = lay.kred;
+  double* cx = reinterpret_cast<double*>(smem + lay.off_cx);
+  const int kred = lay.kred, kres = lay.kres;
+  int cxbuf = 0;
+  // Cluster sum of v[0..K) (per-CTA totals in this CTA's shared memory):
+  // publish, cluster barrier, add every rank's copy in rank order.  Called by
+  // all threads; `who` selects the threads that need the result in out[].
+  auto cluster_sum = [&](const double* v, int K, double* out, bool who) {
+    if constexpr (CL) {
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      double* slot = cx + cxbuf * kres;
+      if (warp == 0)  // v was produced by warp 0
+        for (int k = lane; k < K; k += 32) slot[k] = v[k];
+      cl.sync();
+      if (who)
+        for (int k = lane; k < K; k += 32) {
+          double s = 0.0;
+          for (int r = 0; r < csize; ++r) s += cl.map_shared_rank(slot, r)[k];
+          out[k] = s;
+        }
+      cxbuf ^= 1;
+      __syncwarp();
+    }
+  };
 
   // Source-loop guard: folds away when N is the compile-time NT.
 #define FFCA_NK(k) (EXACT || (k) < N)
 
-  const R* xg = reinterpret_cast<const R*>(p.x) + size_t(b) * XR * T;
-  R* Hg = reinterpret_cast<R*>(p.H) + size_t(b) * N * T;
+  const R* xg = reinterpret_cast<const R*>(p.x) + (size_t(b) * T + t0g) * XR;
+  R* Hg = reinterpret_cast<R*>(p.H) + (size_t(b) * T + t0g) * N;
   const R* xs;
   R* Hs;
   R* wk;
   if (p.resident) {
     const int ox = lay.off_big;
-    const int oh = FitSmem<M, NT, R>::al(ox + T * XR * (int)sizeof(R));
-    const int ow = FitSmem<M, NT, R>::al(oh + T * N * (int)sizeof(R));
+    const int oh = FitSmem<M, NT, R>::al(ox + p.tloc * XR * (int)sizeof(R));
+    const int ow = FitSmem<M, NT, R>::al(oh + p.tloc * N * (int)sizeof(R));
     R* xsm = reinterpret_cast<R*>(smem + ox);
     Hs = reinterpret_cast<R*>(smem + oh);
     wk = reinterpret_cast<R*>(smem + ow);
     {
       const C* src = reinterpret_cast<const C*>(xg);
       C* dst = reinterpret_cast<C*>(xsm);
-      for (int k = tid; k < M * T; k += nthreads) dst[k] = src[k];
+      for (int k = tid; k < M * Tl; k += nthreads) dst[k] = src[k];
     }
-    for (int k = tid; k < N * T; k += nthreads) Hs[k] = Hg[k];
+    for (int k = tid; k < N * Tl; k += nthreads) Hs[k] = Hg[k];
     xs = xsm;
   } else {
     xs = xg;
     Hs = Hg;
-    wk = reinterpret_cast<R*>(p.work) + size_t(b) * WR * T;
+    wk = reinterpret_cast<R*>(p.work) + (size_t(b) * T + t0g) * WR;
   }
   for (int k = tid; k < M * M; k += nthreads) {
     const double2 w = p.W[size_t(b) * M * M + k];
@@ -361,14 +402,14 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 #pragma unroll
     for (int k = 0; k < KA; ++k) acc[k] = R(0);
     // FU frames per trip: all loads first, then independent arithmetic chains.
-    for (int t0 = lt; t0 < T; t0 += FU * gs) {
+    for (int tb = lt; tb < Tl; tb += FU * gs) {
       R xv[FU][XR], h[FU][NT], u[FU][M];
       bool ok[FU];
 #pragma unroll
       for (int f = 0; f < FU; ++f) {
-        const int t = t0 + f * gs;
-        ok[f] = t < T;
-        const int tt = ok[f] ? t : t0;  // always a valid record
+        const int t = tb + f * gs;
+        ok[f] = t < Tl;
+        const int tt = ok[f] ? t : tb;  // always a valid record
         ld_rec<XR>(xs + tt * XR, xv[f]);
         load_h(tt, h[f]);
         if (want_nll && !first) {
@@ -457,6 +498,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       }
       __syncwarp();
     }
+    cluster_sum(res, M * M * M + M + 1, res, warp == 0);
   };
 
   // NLL of the current iterate from pass-A sums (thread 0).
@@ -485,14 +527,14 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     for (int k = 0; k <= M; ++k) acc[k] = R(0);
     const int j = n - 1;
     // FU frames per trip: loads, independent arithmetic chains, then stores.
-    for (int t0 = tid; t0 < T; t0 += FU * nthreads) {
+    for (int tb = tid; tb < Tl; tb += FU * nthreads) {
       R h[FU][NT], w[FU][WR];
       bool ok[FU];
 #pragma unroll
       for (int f = 0; f < FU; ++f) {
-        const int t = t0 + f * nthreads;
-        ok[f] = t < T;
-        const int tt = ok[f] ? t : t0;  // always a valid record
+        const int t = tb + f * nthreads;
+        ok[f] = t < Tl;
+        const int tt = ok[f] ? t : tb;  // always a valid record
         load_h(tt, h[f]);
         if (n == 0) {
           R xv[XR], u[M];
@@ -541,7 +583,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 #pragma unroll
       for (int f = 0; f < FU; ++f) {
         if (!ok[f]) continue;
-        const int t = t0 + f * nthreads;
+        const int t = tb + f * nthreads;
         if (j >= 0) {
           R hj = R(0);
 #pragma unroll
@@ -569,7 +611,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     R acc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = R(0);
-    for (int t = tid; t < T; t += nthreads) {
+    for (int t = tid; t < Tl; t += nthreads) {
       R h[NT];
       load_h(t, h);
       R w[WR];
@@ -610,6 +652,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       for (int o = lane; o < 2 * M * ncnt; o += 32) res[o] = sum_warps(red, K, o);
       __syncwarp();
     }
+    cluster_sum(res, 2 * M * ncnt, res, warp == 0);
   };
 
   // H update with the new L (all sources from one lh, fastfca.cpp:111-116).
@@ -622,7 +665,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     R acc[NT];
 #pragma unroll
     for (int k = 0; k < NT; ++k) acc[k] = R(0);
-    for (int t = tid; t < T; t += nthreads) {
+    for (int t = tid; t < Tl; t += nthreads) {
       R h[NT];
       load_h(t, h);
       R u[M];
@@ -675,6 +718,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       for (int o = lane; o < N; o += 32) res[o] = sum_warps(red, NT, o);
       __syncwarp();
     }
+    cluster_sum(res, N, res, warp == 0);
   };
 
   // Le = L * hsc in the compute type (thread 0).
@@ -698,13 +742,13 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         sc->stop = 1;
       }
       sc->nll0 = nll_from_res(ld);
-      p.nll[size_t(0) * p.nll_stride + p.prob_offset + b] = sc->nll0;
+      if (lead) p.nll[size_t(0) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
     if (silent && !sc->stop) {
       // Entirely silent band: parameters stay at the init (fastfca.cpp:165-170).
       sc->status = kStatusSilent;
       sc->stop = 1;
-      if (record)
+      if (record && lead)
         for (int t = 0; t < p.iters; ++t)
           p.nll[size_t(t + 1) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
@@ -732,7 +776,15 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
           // the identical update; each shared value below is written with the
           // same bits by every warp and is not read in its old state after
           // the barrier.
-          const double tot = (lane <= M) ? sum_warps(red, M + 1, lane) : 0.0;
+          double tot = (lane <= M) ? sum_warps(red, M + 1, lane) : 0.0;
+          if constexpr (CL) {
+            // CTA totals -> cluster totals (rank order); every warp reads them.
+            if (warp == 0 && lane <= M) res[lane] = tot;
+            __syncwarp();
+            cluster_sum(res, M + 1, res, true);
+            tot = (lane <= M) ? res[lane] : 0.0;
+            __syncwarp();
+          }
           if (n >= 1) {
             const double hs = __shfl_sync(0xffffffffu, tot, M);
             if (tid == 0) hsumv[n - 1] = hs;
@@ -852,8 +904,9 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
               sc->status = kStatusSingularW;
               sc->stop = 1;
             }
-            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
-                nll_from_res(sc->logdet0 - sc->logs);
+            if (lead)
+              p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
+                  nll_from_res(sc->logdet0 - sc->logs);
           }
           if (more && !sc->stop) {
             // Next iteration's IP sweep, fused into the pass-A serial section.
@@ -878,17 +931,19 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 #undef FFCA_TIC
   __syncthreads();
   // ------------------------------------------------------------- epilogue --
-  for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
-  for (int k = tid; k < M * N; k += nthreads) p.L[size_t(b) * M * N + k] = Ld[k];
+  if (lead) {
+    for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
+    for (int k = tid; k < M * N; k += nthreads) p.L[size_t(b) * M * N + k] = Ld[k];
+  }
   bool pending = false;
   for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
   if (p.resident || pending)
-    for (int k = tid; k < N * T; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
+    for (int k = tid; k < N * Tl; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
 #ifdef FFCA_PHASE_TIMING
   if (p.timing && tid == 0)
     for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];
 #endif
-  if (tid == 0) p.status[b] = sc->status;
+  if (tid == 0 && lead) p.status[b] = sc->status;
 }
 
 }  // namespace ffca

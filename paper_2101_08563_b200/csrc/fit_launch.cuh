@@ -4,50 +4,113 @@
 // fp32 variants for M <= 4 are specialized on the source count N in
 // {2,3,4,6,12} (no source-loop guards); every other shape uses NT in {4,8,16}
 // with runtime guards.  The fp64 check mode uses NT in {4,16}.
+//
+// Placement: a bin whose records (16M + 4N bytes per frame) fit one CTA's
+// shared memory runs on one CTA; otherwise its frames are split over a
+// thread-block cluster of C = 2..16 CTAs (guarded variants, DSMEM
+// reductions); beyond 16 CTAs the bin streams from global memory.
 #pragma once
 
 #include "internal.hpp"
 
 namespace ffca {
 
-template <int M, int NT, bool EXACT, typename R>
-int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
-  const int threads = fit_threads(M, fp.T, Launch<M>::threads);
+template <int M, int NT, bool EXACT, typename R, bool CL>
+int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev_max) {
+  const int threads = fit_threads(M, fp.tloc, Launch<M>::threads);
   const int nwarps = threads / 32;
-  int nc = 16 / M;
-  if (nc < 1) nc = 1;
-  fp.nc = nc;
-  int dev_max = 0;
-  cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  const FitSmem<M, NT, R> res_lay(nwarps, fp.N, fp.T, nc, true);
-  const int budget = dev_max > 0 ? dev_max - 2048 : 200 * 1024;
-  fp.resident = (res_lay.total <= budget) ? 1 : 0;
-  const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.T, nc, fp.resident != 0);
-  cudaError_t err;
-  if (!fp.resident) {
-    fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
-    if (!fp.work)
-      return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
-  }
-  auto kern = fit_kernel<M, NT, EXACT, R>;
+  const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.tloc, fp.nc, fp.resident != 0);
+  if (lay.total > dev_max)
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca: fit kernel shared memory exceeds the device limit");
+  auto kern = fit_kernel<M, NT, EXACT, R, CL>;
   FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
-  kern<<<fp.nprob, threads, lay.total, st>>>(fp);
+  if constexpr (CL) {
+    if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(fp.nprob) * unsigned(C));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = lay.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FFCA_CUDA(cudaLaunchKernelEx(&cfg, kern, fp));
+  } else {
+    kern<<<fp.nprob, threads, lay.total, st>>>(fp);
+  }
   ctx->launches++;
   FFCA_CUDA(cudaGetLastError());
   return FFCA_OK;
 }
 
+// Cluster size for a bin: the smallest C in {1, 2, 4, 8, 16} whose per-CTA
+// frame range fits the shared-memory budget; 0 when even 16 does not.
+template <int M, int NT, typename R>
+int pick_cluster(const FitParams& fp, int budget) {
+  for (int C = 1; C <= 16; C *= 2) {
+    const int tloc = (fp.T + C - 1) / C;
+    const int nwarps = fit_threads(M, tloc, Launch<M>::threads) / 32;
+    if (FitSmem<M, NT, R>(nwarps, fp.N, tloc, fp.nc, true).total <= budget) return C;
+  }
+  return 0;
+}
+
+template <int M, int NT, bool EXACT, typename R>
+int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
+  int nc = 16 / M;
+  if (nc < 1) nc = 1;
+  fp.nc = nc;
+  int dev_max = 0;
+  cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (dev_max <= 0) dev_max = 227 * 1024;
+  const int budget = dev_max - 2048;
+  const int C = pick_cluster<M, NT, R>(fp, budget);
+  cudaError_t err;
+  if (C == 1) {
+    fp.resident = 1;
+    fp.tloc = fp.T;
+    return launch_fit_cfg<M, NT, EXACT, R, false>(ctx, fp, st, 1, dev_max);
+  }
+  if (C > 1) {
+    if constexpr (!EXACT) {
+      fp.resident = 1;
+      fp.tloc = (fp.T + C - 1) / C;
+      return launch_fit_cfg<M, NT, EXACT, R, true>(ctx, fp, st, C, dev_max);
+    }
+  }
+  // Streaming: the bin's records stay in global memory (L2/HBM).
+  fp.resident = 0;
+  fp.tloc = fp.T;
+  fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
+  if (!fp.work)
+    return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
+  return launch_fit_cfg<M, NT, EXACT, R, false>(ctx, fp, st, 1, dev_max);
+}
+
+// Large bins go to the guarded (cluster-capable) variants.
+template <int M, typename R>
+bool needs_cluster(const FitParams& fp) {
+  int dev_max = 227 * 1024;
+  return pick_cluster<M, 16, R>(fp, dev_max - 2048) != 1;
+}
+
 template <int M>
 int launch_fit_f32(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   if constexpr (M <= 4) {
-    // Exact source-count specializations for the common shapes.
-    switch (fp.N) {
-      case 2: return launch_fit_t<M, 2, true, float>(ctx, fp, st);
-      case 3: return launch_fit_t<M, 3, true, float>(ctx, fp, st);
-      case 4: return launch_fit_t<M, 4, true, float>(ctx, fp, st);
-      case 6: return launch_fit_t<M, 6, true, float>(ctx, fp, st);
-      case 12: return launch_fit_t<M, 12, true, float>(ctx, fp, st);
-      default: break;
+    if (!needs_cluster<M, float>(fp)) {
+      // Exact source-count specializations for the common shapes.
+      switch (fp.N) {
+        case 2: return launch_fit_t<M, 2, true, float>(ctx, fp, st);
+        case 3: return launch_fit_t<M, 3, true, float>(ctx, fp, st);
+        case 4: return launch_fit_t<M, 4, true, float>(ctx, fp, st);
+        case 6: return launch_fit_t<M, 6, true, float>(ctx, fp, st);
+        case 12: return launch_fit_t<M, 12, true, float>(ctx, fp, st);
+        default: break;
+      }
     }
   }
   if (fp.N <= 4) return launch_fit_t<M, 4, false, float>(ctx, fp, st);

@@ -193,3 +193,19 @@ def test_singular_init_raises_numerical_error(gpu):
     W[1] = 0.0  # log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
     with pytest.raises(NumericalError):
         gpu_fit(x, W, L, H, 3, "fp32")
+
+
+# Bins too large for one CTA's shared memory: frames split over a thread-block
+# cluster (DSMEM reductions); config 3's M, N, T.
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("M,N,T,iters", [(8, 12, 8000, 3), (2, 3, 14000, 5), (4, 6, 6000, 4)])
+def test_cluster_split_bins_match_oracle(gpu, precision, M, N, T, iters):
+    x, W, L, H = make_case(M, N, 2, T, seed=17)
+    r = gpu_fit(x, W, L, H, iters, precision)
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, iters)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision], rel.max()
+    img_g = api.fastfca_separate(api.Spectrogram(x), r.params, precision=precision)
+    img_o = oracle.separate(x, Wo, Lo, Ho)
+    for n in range(N):
+        assert rel_l2(img_g[n].f, img_o[n]) <= SEP_TOL[precision]
