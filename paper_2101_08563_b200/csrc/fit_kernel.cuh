@@ -99,7 +99,8 @@ template <int M, int NT, typename R>
 struct FitSmem {
   int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
       off_us, off_hsum,
-      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_scal, off_big, kred, kres,
+      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_wsm, off_scal, off_big,
+      kred, kres,
       total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
@@ -129,6 +130,8 @@ struct FitSmem {
     off_res = o; o = al(o + kres * 8);
     off_rng = o; o = al(o + (int)sizeof(Mt19937_64));   // restart generator (cold)
     off_cx = o; o = al(o + 2 * kres * 8);               // cluster exchange, double-buffered
+    off_wsm = o;  // warp-cooperative algebra scratch (M > 4): warp 0 then warp 1
+    o = al(o + (M > 4 ? (4 * M * M + M + M * (M + 1)) * 2 * (int)sizeof(R) : 0));
     off_scal = o; o = al(o + 64);
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
@@ -728,23 +731,60 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       for (int m = 0; m < M; ++m) Le[m + n * M] = narrow_pos<R>(Ld[m + n * M] * hsc[n]);
   };
 
+  // Serial algebra entry points, called by a whole warp: M <= 4 runs on lane 0
+  // in registers; M > 4 uses the warp-cooperative versions on shared scratch.
+  C* wsm0 = reinterpret_cast<C*>(smem + lay.off_wsm);  // warp 0 (IP, first log-det)
+  C* wsm1 = wsm0 + 4 * M * M + M;                       // warp 1 (balance log-det)
+  auto logdet_warp = [&](const double2* w, C* scratch, double& ld) -> bool {
+    if constexpr (M > 4) {
+      return warp_log_abs_det2<M, R>(w, scratch, lane, ld);
+    } else {
+      bool ok = true;
+      if (lane == 0) ok = log_abs_det2<M, R>(w, ld);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      ld = __shfl_sync(0xffffffffu, ld, 0);
+      return ok;
+    }
+  };
+  auto logdet_w0 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm0, ld); };
+  auto logdet_w1 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm1, ld); };
+  auto run_ip = [&](unsigned long long seed) {
+    int bad = -1;
+    bool ok = true;
+    if constexpr (M > 4) {
+      ok = ip_update_warp<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
+    } else {
+      if (lane == 0) ok = ip_update<M, R>(Wd, res, invT, seed, bin_index, rng, bad);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+    }
+    if (lane == 0 && !ok) {
+      sc->status = kStatusIpSingular | (bad << 8);
+      sc->stop = 1;
+    }
+    __syncwarp();
+    for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
+  };
+
   // -------------------------------------------------------------- driver --
   const bool record = p.record != 0;
   const bool silent = !(power > 0.0);
   FFCA_TIC(9);
   pass_a(true, p.iters > 0 && !silent, record);
   FFCA_TIC(1);
-  if (tid == 0) {
+  if (warp == 0) {
     if (record) {
       double ld = 0.0;
-      if (!log_abs_det2<M, R>(Wd, ld)) {
-        sc->status = kStatusSingularW;
-        sc->stop = 1;
+      const bool ok = logdet_w0(Wd, ld);
+      if (lane == 0) {
+        if (!ok) {
+          sc->status = kStatusSingularW;
+          sc->stop = 1;
+        }
+        sc->nll0 = nll_from_res(ld);
+        if (lead) p.nll[size_t(0) * p.nll_stride + p.prob_offset + b] = sc->nll0;
       }
-      sc->nll0 = nll_from_res(ld);
-      if (lead) p.nll[size_t(0) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
-    if (silent && !sc->stop) {
+    if (lane == 0 && silent && !sc->stop) {
       // Entirely silent band: parameters stay at the init (fastfca.cpp:165-170).
       sc->status = kStatusSilent;
       sc->stop = 1;
@@ -752,16 +792,9 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         for (int t = 0; t < p.iters; ++t)
           p.nll[size_t(t + 1) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
-    if (!sc->stop && p.iters > 0) {
-      // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
-      int bad = -1;
-      if (!ip_update<M, R>(Wd, res, invT, p.seed, bin_index, rng, bad)) {
-        sc->status = kStatusIpSingular | (bad << 8);
-        sc->stop = 1;
-      }
-#pragma unroll
-      for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
-    }
+    __syncwarp();
+    // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
+    if (!sc->stop && p.iters > 0) run_ip(p.seed);
   }
   __syncthreads();
   if (!sc->stop) {
@@ -885,10 +918,13 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
         lsum = warp_sum(lsum);
         if (lane == 0) sc->logs = lsum;
-      } else if (warp == 1 && lane == 0 && record) {
+      } else if (warp == 1 && record) {
         double ld = 0.0;
-        sc->ldok = log_abs_det2<M, R>(Wlg, ld) ? 1 : 0;
-        sc->logdet0 = ld;
+        const bool ok = logdet_w1(Wlg, ld);
+        if (lane == 0) {
+          sc->ldok = ok ? 1 : 0;
+          sc->logdet0 = ld;
+        }
       }
       FFCA_TIC(7);
       __syncthreads();
@@ -898,8 +934,8 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       if (more || record) {
         pass_a(false, more, record);
         FFCA_TIC(1);
-        if (tid == 0) {
-          if (record) {
+        if (warp == 0) {
+          if (lane == 0 && record) {
             if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
               sc->status = kStatusSingularW;
               sc->stop = 1;
@@ -908,17 +944,9 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
               p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
                   nll_from_res(sc->logdet0 - sc->logs);
           }
-          if (more && !sc->stop) {
-            // Next iteration's IP sweep, fused into the pass-A serial section.
-            int bad = -1;
-            if (!ip_update<M, R>(Wd, res, invT, p.seed + (unsigned long long)(it + 1), bin_index,
-                              rng, bad)) {
-              sc->status = kStatusIpSingular | (bad << 8);
-              sc->stop = 1;
-            }
-#pragma unroll
-            for (int k = 0; k < M * M; ++k) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
-          }
+          __syncwarp();
+          // Next iteration's IP sweep, fused into the pass-A serial section.
+          if (more && !sc->stop) run_ip(p.seed + (unsigned long long)(it + 1));
         }
         FFCA_TIC(2);
         __syncthreads();

@@ -290,4 +290,159 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
   return true;
 }
 
+// ------------------------------------------------ warp-cooperative (M > 4) --
+// For M > 4 the single-thread register algebra above spills and serialises
+// ~M^3 complex operations; one warp shares the work instead: matrices live in
+// shared scratch, lanes own matrix entries, Gauss-Jordan elimination with the
+// same partial pivoting (largest modulus, lowest row on ties) replaces the
+// LU + substitution, and reductions are warp shuffles.
+
+// Warp argmax of v over lanes [k, M) (ties -> lowest lane); result broadcast.
+template <typename SR>
+__device__ __forceinline__ int warp_pivot(SR v, int k, int M, int lane) {
+  SR best = (lane >= k && lane < M) ? v : SR(-1);
+  int idx = lane;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const SR ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) best = ob, idx = oi;
+  }
+  return idx;
+}
+
+template <typename SR>
+__device__ __forceinline__ SR warp_allsum(SR v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// In-place Gauss-Jordan on the augmented M x (M+1) matrix A (column-major,
+// column M is the right-hand side).  Returns false on a zero pivot; the
+// pivots' log|.|^2 sum (log-det of the original matrix) goes to *logdet2.
+template <int M, typename SR>
+__device__ bool warp_gauss_jordan(cplx_t<SR>* A, int lane, double* logdet2) {
+  using SC = cplx_t<SR>;
+  constexpr int MA = M + 1;
+  double ld = 0.0;
+  bool ok = true;
+  for (int k = 0; k < M; ++k) {
+    const SR v = lane < M ? cabs2(A[lane + k * M]) : SR(-1);
+    const int p = warp_pivot(v, k, M, lane);
+    if (p != k)
+      for (int c = lane; c < MA; c += 32) {
+        const SC t = A[k + c * M];
+        A[k + c * M] = A[p + c * M];
+        A[p + c * M] = t;
+      }
+    __syncwarp();
+    const SC piv = A[k + k * M];
+    const SR pm = cabs2(piv);
+    if (!(pm > SR(0)) || !isfinite(pm)) ok = false;
+    ld += SMath<SR>::log_d(pm);
+    const SR s = SMath<SR>::rcp(pm);
+    const SC ipiv = mkc<SR>(piv.x * s, -piv.y * s);
+    // Scale the pivot row by 1/A(k,k) (columns > k); column k keeps the
+    // elimination factors A(r,k) of the other rows.
+    for (int c = k + 1 + lane; c < MA; c += 32) A[k + c * M] = cmul(A[k + c * M], ipiv);
+    __syncwarp();
+    // Eliminate column k from every other row: A(r,c) -= A(r,k) A(k,c)/A(k,k), c > k.
+    for (int e = lane; e < M * (MA - k - 1); e += 32) {
+      const int r = e % M, c = k + 1 + e / M;
+      if (r != k) A[r + c * M] = csub(A[r + c * M], cmul(A[r + k * M], A[k + c * M]));
+    }
+    __syncwarp();
+  }
+  *logdet2 = ld;
+  return ok;
+}
+
+template <int M, typename SR>
+__device__ bool warp_log_abs_det2(const double2* w, cplx_t<SR>* scratch, int lane, double& out) {
+  for (int e = lane; e < M * (M + 1); e += 32)
+    scratch[e] = e < M * M ? mkc<SR>(SR(w[e].x), SR(w[e].y)) : mkc<SR>(SR(0), SR(0));
+  __syncwarp();
+  double ld = 0.0;
+  const bool ok = warp_gauss_jordan<M, SR>(scratch, lane, &ld);
+  out = ld;
+  return ok;
+}
+
+// ip_update_w (fastfca.cpp:36-72) by one warp.  scratch: 3*M*M + 2*M complex.
+template <int M, typename SR>
+__device__ bool ip_update_warp(double2* w, const double* qraw, double invT,
+                               unsigned long long seed, int bin, Mt19937_64* rng,
+                               cplx_t<SR>* scratch, int lane, int& bad_col) {
+  using SC = cplx_t<SR>;
+  SC* Q = scratch;              // M x M
+  SC* A = Q + M * M;            // M x (M+1) augmented, eliminated in place
+  SC* A0 = A + M * (M + 1);     // M x M, W^H Q kept for the residual
+  SC* Wc = A0 + M * M;          // M x M compute-type copy of W
+  bool seeded = false;
+  PolarNormal gauss{0.0, false};
+  for (int e = lane; e < M * M; e += 32) Wc[e] = mkc<SR>(SR(w[e].x), SR(w[e].y));
+  for (int col = 0; col < M; ++col) {
+    const double* p = qraw + col * M * M;
+    for (int e = lane; e < M * M; e += 32) {
+      const int a = e % M, b = e / M;
+      if (a == b) Q[e] = mkc<SR>(SR(p[a * M + a] * invT), SR(0));
+      else if (a < b) Q[e] = mkc<SR>(SR(p[a * M + b] * invT), SR(p[b * M + a] * invT));
+      else Q[e] = mkc<SR>(SR(p[b * M + a] * invT), SR(-p[a * M + b] * invT));
+    }
+    __syncwarp();
+    for (int attempt = 0;; ++attempt) {
+      SR an = SR(0);
+      for (int e = lane; e < M * M; e += 32) {
+        const int r = e % M, c = e / M;
+        SC s = cmulc(Wc[r * M], Q[c * M]);
+        for (int k = 1; k < M; ++k) s = cadd(s, cmulc(Wc[k + r * M], Q[k + c * M]));
+        A[e] = s;  // (W^H Q)(r,c), column-major like the augmented matrix
+        A0[e] = s;
+        an += cabs2(s);
+      }
+      if (lane < M) A[lane + M * M] = mkc<SR>(lane == col ? SR(1) : SR(0), SR(0));
+      const SR anorm = warp_allsum(an);
+      __syncwarp();
+      double ldummy;
+      warp_gauss_jordan<M, SR>(A, lane, &ldummy);
+      // w = the eliminated right-hand side (lane r holds w_r).
+      const SC wmr = lane < M ? A[lane + M * M] : mkc<SR>(SR(0), SR(0));
+      const bool fin = __all_sync(0xffffffffu, isfinite(wmr.x) && isfinite(wmr.y));
+      const SR wn = warp_allsum(cabs2(wmr));
+      SC rr = mkc<SR>(lane == col ? SR(-1) : SR(0), SR(0));
+      SC qw = mkc<SR>(SR(0), SR(0));
+      for (int c = 0; c < M; ++c) {
+        const SC wc = mkc<SR>(__shfl_sync(0xffffffffu, wmr.x, c), __shfl_sync(0xffffffffu, wmr.y, c));
+        if (lane < M) {
+          rr = cadd(rr, cmul(A0[lane + c * M], wc));
+          qw = cadd(qw, cmul(Q[lane + c * M], wc));
+        }
+      }
+      const SR rn = warp_allsum(lane < M ? cabs2(rr) : SR(0));
+      const SR en = warp_allsum(lane < M ? cmulc(wmr, qw).x : SR(0));
+      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
+      if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en)) {
+        const SR s = SMath<SR>::rsq(en);
+        if (lane < M) {
+          const SC nw = mkc<SR>(wmr.x * s, wmr.y * s);
+          Wc[lane + col * M] = nw;
+          w[lane + col * M] = make_double2(double(nw.x), double(nw.y));
+        }
+        __syncwarp();
+        break;
+      }
+      if (attempt >= 1) {
+        bad_col = col;
+        return false;
+      }
+      if (lane == 0) ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
+      __syncwarp();
+      for (int e = lane; e < M * M; e += 32) Wc[e] = mkc<SR>(SR(w[e].x), SR(w[e].y));
+      __syncwarp();
+    }
+  }
+  return true;
+}
+
 }  // namespace ffca
