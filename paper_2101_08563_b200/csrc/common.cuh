@@ -126,6 +126,14 @@ struct PolarNormal {
   }
 };
 
+// Restart state of one IP sweep, kept in shared scratch so the hot path of
+// the column solves holds no address-taken locals (those live in local
+// memory and cost a round trip per call).
+struct RestartRng {
+  Mt19937_64 mt;
+  PolarNormal gauss;
+};
+
 // fastfca.cpp:13-18
 __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, int i) {
   uint64_t z = seed + 0x9e3779b97f4a7c15ULL * uint64_t(int64_t(i) + 1);

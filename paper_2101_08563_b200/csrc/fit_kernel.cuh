@@ -94,6 +94,13 @@ constexpr int kMaxWarps = 8;
 #define FFCA_FRAMES_IN_FLIGHT 1
 #endif
 
+// MM: sources per L-reduction chunk (2 M values each, <= 32 per warp pass).
+template <int M, int NT>
+struct MmChunk {
+  static constexpr int nc0 = (16 / M) > 0 ? (16 / M) : 1;
+  static constexpr int value = nc0 < NT ? nc0 : NT;
+};
+
 // Shared-memory carve-up, identical on host and device.
 template <int M, int NT, typename R>
 struct FitSmem {
@@ -105,8 +112,8 @@ struct FitSmem {
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
     using S = Split<M>;
-    kred = M + 1;
-    if (2 * M * nc > kred) kred = 2 * M * nc;
+    kred = 2 * M + 1;  // EM sweep partials (+ Phi sums in the last sweep)
+    if (2 * M * MmChunk<M, NT>::value > kred) kred = 2 * M * MmChunk<M, NT>::value;
     if (NT > kred) kred = NT;
     kres = M * M * M + M + 1;
     if (kres < kred) kres = kred;
@@ -115,20 +122,34 @@ struct FitSmem {
     off_wlg = o; o = al(o + M * M * 16);  // W after the IP sweep (log-det input)
     off_wsc = o; o = al(o + M * 8);       // balance: W column scales
     off_wr = o; o = al(o + M * M * 2 * (int)sizeof(R));
-    off_ld = o; o = al(o + M * NT * 8);
+    off_ld = o; o = al(o + 2 * M * NT * 8);  // parity double-buffered (balance)
     off_le = o; o = al(o + M * NT * (int)sizeof(R));
     off_linv = o; o = al(o + M * (int)sizeof(R));
-    off_hsc = o; o = al(o + NT * 8);
-    off_hinv = o; o = al(o + NT * 8);
+    off_hsc = o; o = al(o + 2 * NT * 8);
+    off_hinv = o; o = al(o + 2 * NT * 8);
     off_hscr = o; o = al(o + NT * (int)sizeof(R));
     off_us = o; o = al(o + M * 8);
     off_hsum = o; o = al(o + NT * 8);
     off_num = o; o = al(o + M * NT * 8);
     off_den = o; o = al(o + M * NT * 8);
     off_reda = o; o = al(o + nwarps * S::KA * 8);       // pass-A partials
-    off_redb = o; o = al(o + 2 * nwarps * kred * 8);    // sweep partials, double-buffered
+    // Sweep partials, double-buffered.  The IP restart generator (cold, live
+    // only inside one IP sweep, when no sweep partials are pending) shares
+    // the region; the phase-timing diagnostics keep their counters there, so
+    // that build gives the generator its own space.
+    off_redb = o;
+    {
+      int rb = 2 * nwarps * kred * 8;
+#ifndef FFCA_PHASE_TIMING
+      if (rb < (int)sizeof(RestartRng)) rb = (int)sizeof(RestartRng);
+      off_rng = o;
+#endif
+      o = al(o + rb);
+    }
+#ifdef FFCA_PHASE_TIMING
+    off_rng = o; o = al(o + (int)sizeof(RestartRng));
+#endif
     off_res = o; o = al(o + kres * 8);
-    off_rng = o; o = al(o + (int)sizeof(Mt19937_64));   // restart generator (cold)
     off_cx = o; o = al(o + 2 * kres * 8);               // cluster exchange, double-buffered
     off_wsm = o;  // warp-cooperative algebra scratch (M > 4): warp 0 then warp 1
     o = al(o + (M > 4 ? (4 * M * M + M + M * (M + 1)) * 2 * (int)sizeof(R) : 0));
@@ -212,7 +233,10 @@ struct Uniform {
 // CL: the bin's frames are split over a thread-block cluster (one CTA per
 // frame range, cluster rank order); reductions add a DSMEM exchange and every
 // CTA repeats the (identical) serial algebra, so no broadcast is needed.
-template <int M, int NT, bool EXACT, typename R, bool CL>
+// RES: the bin's records live in shared memory (compile-time, so the record
+// accesses are LDS/STS rather than generic loads); !RES streams them from
+// global memory (bins beyond a 16-CTA cluster).
+template <int M, int NT, bool EXACT, typename R, bool CL, bool RES>
 __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
@@ -237,25 +261,33 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const int t0g = int((long long)T * crank / csize);  // this CTA's frames [t0g, t0g + Tl)
   const int Tl = int((long long)T * (crank + 1) / csize) - t0g;
   const bool lead = crank == 0;  // writes the per-bin outputs
-  const FitSmem<M, NT, R> lay(nwarps, N, p.tloc, p.nc, p.resident != 0);
+  const FitSmem<M, NT, R> lay(nwarps, N, p.tloc, p.nc, RES);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
   double* wsc = reinterpret_cast<double*>(smem + lay.off_wsc);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
-  double* Ld = reinterpret_cast<double*>(smem + lay.off_ld);
+  // Ld, hsc and hinv are double-buffered by iteration parity: every warp
+  // computes the balance itself and writes the other buffer, so no warp can
+  // overwrite a value another warp still reads (see balance_all below).
+  double* const Ld0 = reinterpret_cast<double*>(smem + lay.off_ld);
+  double* const hsc0 = reinterpret_cast<double*>(smem + lay.off_hsc);
+  double* const hinv0 = reinterpret_cast<double*>(smem + lay.off_hinv);
+  double* Ld = Ld0;      // current L (fp64 master)
+  double* hsc = hsc0;    // current lazy H row scales
+  double* hinv = hinv0;  // 1 / hsc
+  int par = 0;
   R* Le = reinterpret_cast<R*>(smem + lay.off_le);      // L * hsc, compute type
   R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);  // 1 / L(:, n) of the new column
-  double* hsc = reinterpret_cast<double*>(smem + lay.off_hsc);
-  double* hinv = reinterpret_cast<double*>(smem + lay.off_hinv);  // 1 / hsc
   R* hscr = reinterpret_cast<R*>(smem + lay.off_hscr);  // hsc in the compute type (MM)
   double* us = reinterpret_cast<double*>(smem + lay.off_us);
   double* hsumv = reinterpret_cast<double*>(smem + lay.off_hsum);
   double* numd = reinterpret_cast<double*>(smem + lay.off_num);
+  double* psum = numd;  // EM: sum_t Phi(m) of the last sweep (numd is MM-only)
   double* dend = reinterpret_cast<double*>(smem + lay.off_den);
   double* reda = reinterpret_cast<double*>(smem + lay.off_reda);
   double* redb = reinterpret_cast<double*>(smem + lay.off_redb);
   double* res = reinterpret_cast<double*>(smem + lay.off_res);
-  Mt19937_64* rng = reinterpret_cast<Mt19937_64*>(smem + lay.off_rng);
+  RestartRng* rng = reinterpret_cast<RestartRng*>(smem + lay.off_rng);
   Scalars* sc = reinterpret_cast<Scalars*>(smem + lay.off_scal);
   double* cx = reinterpret_cast<double*>(smem + lay.off_cx);
   const int kred = lay.kred, kres = lay.kres;
@@ -290,7 +322,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const R* xs;
   R* Hs;
   R* wk;
-  if (p.resident) {
+  if constexpr (RES) {
     const int ox = lay.off_big;
     const int oh = FitSmem<M, NT, R>::al(ox + p.tloc * XR * (int)sizeof(R));
     const int ow = FitSmem<M, NT, R>::al(oh + p.tloc * N * (int)sizeof(R));
@@ -335,8 +367,13 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   // Phase timing: diagnostics builds only (-DFFCA_PHASE_TIMING, see build.py);
   // the counters would otherwise cost live registers across the whole kernel.
 #ifdef FFCA_PHASE_TIMING
-  unsigned long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long tlast = clock64();
+  // Counters live in shared memory (reuse of the restart-RNG scratch: cold),
+  // so the probe adds no live registers to the instrumented kernel.
+  unsigned long long* tacc = reinterpret_cast<unsigned long long*>(rng);
+  if (tid == 0)
+    for (int k = 0; k < 11; ++k) tacc[k] = 0;
+  if (tid == 0) tacc[10] = clock64();
+#define tlast tacc[10]
 #define FFCA_TIC(k)                              \
   do {                                           \
     if (p.timing && tid == 0) {                  \
@@ -379,12 +416,14 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   // Fixed-order sum of the per-warp partials red[w*K + k] (issued as
   // independent loads, then added in warp order).
   auto sum_warps = [&](const double* red, int K, int k) {
+    // Branch-free: every load hits a valid slot (index clamped), then the
+    // slots beyond nwarps are masked to zero.
     double v[kMaxWarps];
 #pragma unroll
-    for (int w = 0; w < kMaxWarps; ++w) v[w] = (w < nwarps) ? red[w * K + k] : 0.0;
+    for (int w = 0; w < kMaxWarps; ++w) v[w] = red[(w < nwarps ? w : 0) * K + k];
     double s = v[0];
 #pragma unroll
-    for (int w = 1; w < kMaxWarps; ++w) s += v[w];
+    for (int w = 1; w < kMaxWarps; ++w) s += (w < nwarps) ? v[w] : 0.0;
     return s;
   };
 
@@ -392,15 +431,25 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   // first: U from x and the current W; else U = stored U (times us[m] after
   // the reduction).  Leaves Q_m packed in res[0, M^3), sum_t U r per channel
   // in res[M^3 + m] and sum log2 sigma^2 in res[M^3 + M] (warp 0 visible).
-  auto pass_a = [&](bool first, bool want_q, bool want_nll) {
+  // finish (EM): first completes H row N-1 of the iteration from the stored
+  // Phi and Linv (em_update_lh's last H update, fastfca.cpp:95-97), so the
+  // last EM sweep and the next pass A share one trip over the frames.
+  auto pass_a = [&](bool first, bool want_q, bool want_nll, bool finish) {
     constexpr int MSPLIT = S::MSPLIT, MG = S::MG, KQ = S::KQ, KA = S::KA;
     const int gs = nthreads / MSPLIT;
-    const int g = tid / gs, lt = tid - g * gs;
+    // g must fold to 0 for MSPLIT == 1: a runtime channel offset would index
+    // the register-resident loadings dynamically (local memory).
+    const int g = MSPLIT == 1 ? 0 : tid / gs, lt = tid - g * gs;
     const int m0 = g * MG;
+    const int jf = N - 1;
     Uniform<M * NT, HOIST, R> le;
     le.load(Le);
     WU wr;
     if (first) wr.load(reinterpret_cast<const R*>(Wr));
+    R linv[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) linv[m] = finish ? Linv[m] : R(0);
+    const bool need_w = (want_nll && !first) || finish;
     R acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) acc[k] = R(0);
@@ -415,11 +464,22 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         const int tt = ok[f] ? t : tb;  // always a valid record
         ld_rec<XR>(xs + tt * XR, xv[f]);
         load_h(tt, h[f]);
-        if (want_nll && !first) {
+        if (need_w) {
           R w[WR];
           ld_rec<WR>(wk + tt * WR, w);
 #pragma unroll
           for (int m = 0; m < M; ++m) u[f][m] = w[m];
+          if (finish) {
+            R s = linv[0] * w[M];
+#pragma unroll
+            for (int m = 1; m < M; ++m) s += linv[m] * w[M + m];
+            R hn = s * R(1.0 / M);
+            hn = hn > tiny<R>() ? hn : tiny<R>();  // fastfca.cpp:96-97
+#pragma unroll
+            for (int k = 0; k < NT; ++k)
+              if (k == jf) h[f][k] = hn;
+            if (ok[f] && g == 0) Hs[tt * N + jf] = hn;
+          }
         }
       }
 #pragma unroll
@@ -516,8 +576,10 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   // n == 0: U = |W^H x|^2 (stored); n >= 1: finish source n-1 (H row from the
   // stored Phi and the new L column); n < N: Phi of source n (stored) and its
   // L reduction sum_t Phi / H_true (fastfca.cpp:85-97).  Ends with the per-warp
-  // partials in red and one barrier.
-  auto em_sweep = [&](int n, double* red) {
+  // partials in red and one barrier.  phis (the last sweep, balance on): also
+  // reduce sum_t Phi(m) -- the mean of H row N-1 then follows from the new L
+  // column without a sweep of its own (see balance_all).
+  auto em_sweep = [&](int n, double* red, bool phis) {
     Uniform<M * NT, HOIST, R> le;
     le.load(Le);
     WU wr;
@@ -525,9 +587,9 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     R linv[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) linv[m] = Linv[m];
-    R acc[M + 1];
+    R acc[2 * M + 1];
 #pragma unroll
-    for (int k = 0; k <= M; ++k) acc[k] = R(0);
+    for (int k = 0; k <= 2 * M; ++k) acc[k] = R(0);
     const int j = n - 1;
     // FU frames per trip: loads, independent arithmetic chains, then stores.
     for (int tb = tid; tb < Tl; tb += FU * nthreads) {
@@ -580,6 +642,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
             const R phi = gg * (gg * w[f][m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
             w[f][M + m] = phi;
             acc[m] += phi * ihn;
+            if (phis) acc[M + 1 + m] += phi;
           }
         }
       }
@@ -598,14 +661,21 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       }
     }
     FFCA_TIC(4);
-    warp_reduce_store<M + 1>(acc, red + warp * (M + 1), lane);
+    if (phis) {
+      warp_reduce_store<2 * M + 1>(acc, red + warp * (2 * M + 1), lane);
+    } else {
+      R a1[M + 1];
+#pragma unroll
+      for (int k = 0; k <= M; ++k) a1[k] = acc[k];
+      warp_reduce_store<M + 1>(a1, red + warp * (M + 1), lane);
+    }
     __syncthreads();
   };
 
   // ------------------------------------------------------ MM sweeps --
   // L update: num/den reductions over t for sources [n0, n0+nc).
   auto mm_l_sweep = [&](int n0, int ncnt, bool compute_u, double* red) {
-    constexpr int NCMAX = (16 / M) > 0 ? (16 / M) : 1;
+    constexpr int NCMAX = MmChunk<M, NT>::value;
     constexpr int K = 2 * M * NCMAX;
     Uniform<M * NT, HOIST, R> le;
     le.load(Le);
@@ -748,7 +818,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   };
   auto logdet_w0 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm0, ld); };
   auto logdet_w1 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm1, ld); };
-  auto run_ip = [&](unsigned long long seed) {
+  auto run_ip = [&](unsigned long long seed, bool with_logdet) {
     int bad = -1;
     bool ok = true;
     if constexpr (M > 4) {
@@ -763,13 +833,89 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     }
     __syncwarp();
     for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
+    if constexpr (M <= 2) {
+      // log|det W|^2 of the IP output for the next trace entry: a few cycles
+      // at this size, so it rides in the serial section.
+      if (with_logdet) {
+        __syncwarp();
+        double ld = 0.0;
+        const bool lok = logdet_w0(Wlg, ld);
+        if (lane == 0) {
+          sc->ldok = lok ? 1 : 0;
+          sc->logdet0 = ld;
+        }
+      }
+    }
+  };
+
+  // ---- balance_scales (fastfca.cpp:127-142), computed by EVERY warp
+  //      (lane-parallel: mu_n per source lane, s_m per channel lane) from
+  //      values no warp modifies after the last sweep's barrier; results go to
+  //      the other parity buffer (Ld, hsc, hinv) or are written with the same
+  //      bits by every warp (Le, us, wsc, logs).  No serial section, no
+  //      barrier.  The W column scales wsc are applied to the fp64 master by
+  //      warp 0 in the next serial section (nothing reads W before it).
+  //      phi_mean: the mean of H row N-1 follows from the last EM sweep's
+  //      sums, (1/(M T)) sum_m (sum_t Phi(m)) / L(m, N-1) -- the row itself is
+  //      stored by the next pass A (fastfca.cpp:95-97).
+  auto balance_all = [&](bool on, bool phi_mean) {
+    const int nx = par ^ 1;
+    double* hscn = hsc0 + nx * NT;
+    double* hinvn = hinv0 + nx * NT;
+    double* Ldn = Ld0 + nx * (M * NT);
+    for (int n = lane; n < N; n += 32) {
+      double mu;
+      if (phi_mean && n == N - 1) {
+        double c = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) c += psum[m] * fast_rcp(Ld[m + n * M]);
+        mu = c * (invT / double(M));
+      } else {
+        mu = hsumv[n] * invT;
+      }
+      const bool v = on && mu > 0.0 && isfinite(mu);
+      hscn[n] = v ? fast_rcp(mu) : 1.0;
+      hinvn[n] = v ? mu : 1.0;
+    }
+    __syncwarp();
+    double ls = 0.0;
+    if (lane < M) {
+      const int m = lane;
+      double s = 0.0;
+      for (int n = 0; n < N; ++n) s += Ld[m + n * M] * hinvn[n];
+      s *= 1.0 / double(N);
+      const bool v = on && s > 0.0 && isfinite(s);
+      us[m] = v ? fast_rcp(s) : 1.0;  // U and L-row scale 1/s
+      wsc[m] = v ? rsqrt(s) : 1.0;    // W column scale
+      if (v) ls = SMath<R>::log_wide(s);
+    }
+    __syncwarp();
+    for (int k = lane; k < M * N; k += 32) {
+      const int m = k % M, n = k / M;
+      const double l = Ld[k] * hinvn[n] * us[m];  // L(m,n) mu_n / s_m
+      Ldn[k] = l;
+      Le[k] = narrow_pos<R>(l * hscn[n]);
+    }
+    __syncwarp();  // converged before the shuffles
+    // sum_m log s_m over the lowest Pow2Ceil(M) lanes (fixed order).
+#pragma unroll
+    for (int o = Pow2Ceil<M>::value / 2; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    const double lsum = ls;
+    if (lane == 0) sc->logs = lsum;
+    par = nx;
+    Ld = Ldn;
+    hsc = hscn;
+    hinv = hinvn;
+    __syncwarp();
   };
 
   // -------------------------------------------------------------- driver --
   const bool record = p.record != 0;
   const bool silent = !(power > 0.0);
+  const bool bal = p.normalize && update_loading;
+  const int ldwarp = nwarps - 1;  // M > 2: log-det of the IP output, off the serial path
   FFCA_TIC(9);
-  pass_a(true, p.iters > 0 && !silent, record);
+  pass_a(true, p.iters > 0 && !silent, record, false);
   FFCA_TIC(1);
   if (warp == 0) {
     if (record) {
@@ -794,46 +940,61 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     }
     __syncwarp();
     // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
-    if (!sc->stop && p.iters > 0) run_ip(p.seed);
+    if (!sc->stop && p.iters > 0) run_ip(p.seed, record);
   }
   __syncthreads();
   if (!sc->stop) {
     for (int it = 0; it < p.iters; ++it) {
+      if constexpr (M > 2) {
+        if (record && warp == ldwarp) {
+          double ld = 0.0;
+          const bool ok = logdet_w1(Wlg, ld);
+          if (lane == 0) {
+            sc->ldok = ok ? 1 : 0;
+            sc->logdet0 = ld;
+          }
+          __syncwarp();
+        }
+      }
       // ---- L/H updates (the IP sweep of this iteration already ran)
       if (p.flavor == 0) {
-        for (int n = 0; n <= N; ++n) {
+        for (int n = 0; n < N; ++n) {
+          const bool phis = bal && n == N - 1;
+          const int K = phis ? 2 * M + 1 : M + 1;
           double* red = redb + (n & 1) * nwarps * kred;
-          em_sweep(n, red);
+          em_sweep(n, red, phis);
           FFCA_TIC(5);
           // Every warp sums the partials (lane k holds value k) and applies
           // the identical update; each shared value below is written with the
           // same bits by every warp and is not read in its old state after
           // the barrier.
-          double tot = (lane <= M) ? sum_warps(red, M + 1, lane) : 0.0;
+          double tot = (lane < K) ? sum_warps(red, K, lane) : 0.0;
           if constexpr (CL) {
             // CTA totals -> cluster totals (rank order); every warp reads them.
-            if (warp == 0 && lane <= M) res[lane] = tot;
+            if (warp == 0 && lane < K) res[lane] = tot;
             __syncwarp();
-            cluster_sum(res, M + 1, res, true);
-            tot = (lane <= M) ? res[lane] : 0.0;
+            cluster_sum(res, K, res, true);
+            tot = (lane < K) ? res[lane] : 0.0;
             __syncwarp();
           }
-          if (n >= 1) {
-            const double hs = __shfl_sync(0xffffffffu, tot, M);
-            if (tid == 0) hsumv[n - 1] = hs;
-          }
-          if (n < N && lane < M) {
+          // Shuffles while the warp is converged: the H row n-1 sum and (last
+          // sweep) sum_t Phi(m) on lane m.
+          const double hs = __shfl_sync(0xffffffffu, tot, M);
+          const double ps = __shfl_down_sync(0xffffffffu, tot, M + 1);
+          FFCA_TIC(8);
+          if (lane < M) {
             // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
-            // (fastfca.cpp:92-94).  Sweep n+1 stores the true H row n, so
-            // Le(:, n) becomes the new L column (no hsc).
+            // (fastfca.cpp:92-94).  The next sweep (or pass A) stores the true
+            // H row n, so Le(:, n) becomes the new L column (no hsc).
             const int m = lane;
-            const double l =
-                update_loading ? fmax(tot * invT * hinv[n], 1e-300) : Ld[m + n * M];
+            const double l = update_loading ? fmax(tot * invT * hinv[n], 1e-300) : Ld[m + n * M];
             const R lr = narrow_pos<R>(l);
             Ld[m + n * M] = l;
-            Le[m + n * M] = lr;
+            if (!phis) Le[m + n * M] = lr;  // with phis the balance rewrites all of Le
             Linv[m] = rcp_fast(lr);
+            if (phis) psum[m] = ps;
           }
+          if (lane == 0 && n >= 1) hsumv[n - 1] = hs;
           __syncwarp();
           FFCA_TIC(6);
         }
@@ -875,84 +1036,42 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         if (tid == 0) {
           for (int k = 0; k < N; ++k) hsumv[k] = res[k];
         }
+        __syncthreads();
+        FFCA_TIC(5);
       }
-      __syncthreads();
-      FFCA_TIC(5);
-      // ---- balance_scales (fastfca.cpp:127-142), lane-parallel in warp 0:
-      //      mu_n per source lane, s_m per channel lane, then the L and W
-      //      scalings.  Warp 1 meanwhile takes log|det W|^2 of the unscaled W
-      //      (copy Wlg); scaling column m by s_m^{-1/2} adds -log s_m.
-      const bool bal = p.normalize && update_loading;
+      balance_all(bal, p.flavor == 0);
+      FFCA_TIC(7);
+      const bool more = it + 1 < p.iters;
+      // EM: pass A also stores H row N-1, so it runs after the last iteration too.
+      if (more || record || p.flavor == 0) pass_a(false, more, record, p.flavor == 0);
+      FFCA_TIC(1);
       if (warp == 0) {
-        for (int n = lane; n < N; n += 32) {  // every H row is stored true here
-          const double mu = hsumv[n] * invT;
-          const bool v = bal && mu > 0.0 && isfinite(mu);
-          hsc[n] = v ? fast_rcp(mu) : 1.0;
-          hinv[n] = v ? mu : 1.0;
-        }
-        __syncwarp();
-        double lsum = 0.0;
-        for (int m = lane; m < M; m += 32) {
-          double s = 0.0;
-          for (int n = 0; n < N; ++n) s += Ld[m + n * M] * hinv[n];
-          s *= 1.0 / double(N);
-          const bool v = bal && s > 0.0 && isfinite(s);
-          us[m] = v ? fast_rcp(s) : 1.0;  // U and L-row scale 1/s
-          wsc[m] = v ? rsqrt(s) : 1.0;    // W column scale
-          if (v) lsum += log(s);
-        }
-        __syncwarp();
-        for (int k = lane; k < M * N; k += 32) {
-          const int m = k % M, n = k / M;
-          const double l = Ld[k] * hinv[n] * us[m];  // L(m,n) mu_n / s_m
-          Ld[k] = l;
-          Le[k] = narrow_pos<R>(l * hsc[n]);
-        }
+        // Balance W column scales on the fp64 master (fastfca.cpp:139-141).
         for (int k = lane; k < M * M; k += 32) {
           double2 w = Wd[k];
           const double c = wsc[k / M];
           w.x *= c;
           w.y *= c;
           Wd[k] = w;
-          Wr[k] = mkc<R>(R(w.x), R(w.y));
         }
-        lsum = warp_sum(lsum);
-        if (lane == 0) sc->logs = lsum;
-      } else if (warp == 1 && record) {
-        double ld = 0.0;
-        const bool ok = logdet_w1(Wlg, ld);
-        if (lane == 0) {
-          sc->ldok = ok ? 1 : 0;
-          sc->logdet0 = ld;
-        }
-      }
-      FFCA_TIC(7);
-      __syncthreads();
-      FFCA_TIC(8);
-      if (sc->stop) break;
-      const bool more = it + 1 < p.iters;
-      if (more || record) {
-        pass_a(false, more, record);
-        FFCA_TIC(1);
-        if (warp == 0) {
-          if (lane == 0 && record) {
-            if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
-              sc->status = kStatusSingularW;
-              sc->stop = 1;
-            }
-            if (lead)
-              p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
-                  nll_from_res(sc->logdet0 - sc->logs);
+        __syncwarp();
+        if (lane == 0 && record) {
+          if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
+            sc->status = kStatusSingularW;
+            sc->stop = 1;
           }
-          __syncwarp();
-          // Next iteration's IP sweep, fused into the pass-A serial section.
-          if (more && !sc->stop) run_ip(p.seed + (unsigned long long)(it + 1));
+          if (lead)
+            p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] =
+                nll_from_res(sc->logdet0 - sc->logs);
         }
-        FFCA_TIC(2);
-        __syncthreads();
-        FFCA_TIC(3);
-        if (sc->stop) break;
+        __syncwarp();
+        // Next iteration's IP sweep, fused into the pass-A serial section.
+        if (more && !sc->stop) run_ip(p.seed + (unsigned long long)(it + 1), record);
       }
+      FFCA_TIC(2);
+      __syncthreads();
+      FFCA_TIC(3);
+      if (sc->stop) break;
     }
   }
 #undef FFCA_NK
@@ -965,11 +1084,12 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   }
   bool pending = false;
   for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
-  if (p.resident || pending)
+  if (RES || pending)
     for (int k = tid; k < N * Tl; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
 #ifdef FFCA_PHASE_TIMING
   if (p.timing && tid == 0)
     for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];
+#undef tlast
 #endif
   if (tid == 0 && lead) p.status[b] = sc->status;
 }

@@ -11,18 +11,25 @@
 // reductions); beyond 16 CTAs the bin streams from global memory.
 #pragma once
 
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace ffca {
 
-template <int M, int NT, bool EXACT, typename R, bool CL>
+template <int M, int NT, bool EXACT, typename R, bool CL, bool RES>
 int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev_max) {
-  const int threads = fit_threads(M, fp.tloc, Launch<M>::threads);
+  int threads = fit_threads(M, fp.tloc, Launch<M>::threads);
+  if (const char* e = getenv("FFCA_FIT_THREADS")) {  // tuning experiments only
+    const int v = atoi(e);
+    const int per = (M <= 4) ? 32 : 32 * M;
+    if (v >= per && v <= Launch<M>::threads && v % per == 0) threads = v;
+  }
   const int nwarps = threads / 32;
-  const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.tloc, fp.nc, fp.resident != 0);
+  const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.tloc, fp.nc, RES);
   if (lay.total > dev_max)
     return ffca_set_err(FFCA_CUDA_ERROR, "ffca: fit kernel shared memory exceeds the device limit");
-  auto kern = fit_kernel<M, NT, EXACT, R, CL>;
+  auto kern = fit_kernel<M, NT, EXACT, R, CL, RES>;
   FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
   if constexpr (CL) {
     if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -61,9 +68,7 @@ int pick_cluster(const FitParams& fp, int budget) {
 
 template <int M, int NT, bool EXACT, typename R>
 int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
-  int nc = 16 / M;
-  if (nc < 1) nc = 1;
-  fp.nc = nc;
+  fp.nc = MmChunk<M, NT>::value;
   int dev_max = 0;
   cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   if (dev_max <= 0) dev_max = 227 * 1024;
@@ -73,22 +78,28 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   if (C == 1) {
     fp.resident = 1;
     fp.tloc = fp.T;
-    return launch_fit_cfg<M, NT, EXACT, R, false>(ctx, fp, st, 1, dev_max);
+    return launch_fit_cfg<M, NT, EXACT, R, false, true>(ctx, fp, st, 1, dev_max);
   }
   if (C > 1) {
     if constexpr (!EXACT) {
       fp.resident = 1;
       fp.tloc = (fp.T + C - 1) / C;
-      return launch_fit_cfg<M, NT, EXACT, R, true>(ctx, fp, st, C, dev_max);
+      return launch_fit_cfg<M, NT, EXACT, R, true, true>(ctx, fp, st, C, dev_max);
     }
   }
-  // Streaming: the bin's records stay in global memory (L2/HBM).
-  fp.resident = 0;
-  fp.tloc = fp.T;
-  fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
-  if (!fp.work)
-    return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
-  return launch_fit_cfg<M, NT, EXACT, R, false>(ctx, fp, st, 1, dev_max);
+  // Streaming: the bin's records stay in global memory (L2/HBM).  Only the
+  // guarded variants get here (needs_cluster routes large bins to them).
+  if constexpr (!EXACT) {
+    fp.resident = 0;
+    fp.tloc = fp.T;
+    fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
+    if (!fp.work)
+      return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
+    return launch_fit_cfg<M, NT, EXACT, R, false, false>(ctx, fp, st, 1, dev_max);
+  } else {
+    (void)err;
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca: internal: exact-N variant selected for a large bin");
+  }
 }
 
 // Large bins go to the guarded (cluster-capable) variants.

@@ -29,6 +29,15 @@ struct SMath<float> {
   __device__ static __forceinline__ double log_d(float x) {
     return double(flog2_ftz(x)) * 0.69314718055994531;
   }
+  // log of a positive normal double to fp32 relative accuracy over the full
+  // double range: exponent + SFU log2 of the mantissa in [1, 2).
+  __device__ static __forceinline__ double log_wide(double x) {
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) & 0x7ff;
+    if (e == 0 || e == 0x7ff) return log(x);
+    const float m = float(__hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo));
+    return (double(e - 1023) + double(flog2_ftz(m))) * 0.69314718055994531;
+  }
 };
 
 template <>
@@ -50,6 +59,7 @@ struct SMath<double> {
   __device__ static __forceinline__ double rsq(double x) { return rsqrt(x); }
   __device__ static __forceinline__ double sq(double x) { return sqrt(x); }
   __device__ static __forceinline__ double log_d(double x) { return log(x); }
+  __device__ static __forceinline__ double log_wide(double x) { return log(x); }
 };
 
 __device__ __forceinline__ double fast_rcp(double x) { return SMath<double>::rcp(x); }
@@ -160,22 +170,106 @@ __device__ __forceinline__ bool log_abs_det2(const double2* w, double& out) {
 // Cold path of ip_update_w: one seeded perturbation of a column
 // (fastfca.cpp:66-69).  The generator is seeded lazily on the first restart
 // of the sweep and its state lives in shared scratch.
-static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64* rng,
-                                               bool* seeded, PolarNormal* gauss,
+static __device__ __noinline__ void ip_perturb(double2* wcol, int m, RestartRng* rr, bool first,
                                                unsigned long long seed, int bin) {
-  if (!*seeded) {
-    rng->seed(mix_seed(seed, bin));
-    *seeded = true;
+  if (first) {  // a fresh generator + distribution per sweep (fastfca.cpp:40-41)
+    rr->mt.seed(mix_seed(seed, bin));
+    rr->gauss.saved = 0.0;
+    rr->gauss.has_saved = false;
   }
   double cn = 0.0;
   for (int r = 0; r < m; ++r) cn += cabs2(wcol[r]);
   const double mag = 1e-8 * (sqrt(cn) + 1.0);
   for (int r = 0; r < m; ++r) {
-    const double im = (*gauss)(*rng);  // g++ evaluates Complex(g(), g()) right to left
-    const double re = (*gauss)(*rng);
+    const double im = rr->gauss(rr->mt);  // g++ evaluates Complex(g(), g()) right to left
+    const double re = rr->gauss(rr->mt);
     wcol[r].x += mag * re;
     wcol[r].y += mag * im;
   }
+}
+
+// M = 2 IP sweep in closed form on the Hermitian structure of Q (real
+// diagonal, Q(1,0) = conj Q(0,1)): A = W^H Q_k, w = A^{-1} e_k from the 2x2
+// adjugate, the residual test, w /= sqrt(w^H Q_k w) -- the same steps as the
+// general path below with the zero imaginary parts and the symmetric half
+// folded away, so the per-column dependency chain is ~15 FP ops + 2 MUFU.
+template <typename SR>
+__device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, double invT,
+                                             unsigned long long seed, int bin, RestartRng* rr,
+                                             int& bad_col) {
+  using SC = cplx_t<SR>;
+  SR qd0[2], qd1[2];
+  SC qo[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double* p = qraw + 4 * c;
+    qd0[c] = SR(p[0] * invT);
+    qd1[c] = SR(p[3] * invT);
+    qo[c] = mkc<SR>(SR(p[1] * invT), SR(p[2] * invT));  // Q(0,1)
+  }
+  SC wr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+  bool restarted = false;
+#pragma unroll
+  for (int col = 0; col < 2; ++col) {
+    const SR q00 = qd0[col], q11 = qd1[col];
+    const SC q01 = qo[col];
+    for (int attempt = 0;; ++attempt) {
+      // A(r, c) = sum_k conj(W(k, r)) Q(k, c), Q(1, 0) = conj(q01).
+      SC a[4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const SC u0 = wr[2 * r], u1 = wr[2 * r + 1];  // column r of W
+        // conj(u0) q00 + conj(u1) conj(q01)
+        a[r] = mkc<SR>(u0.x * q00 + (u1.x * q01.x - u1.y * q01.y),
+                       -u0.y * q00 - (u1.x * q01.y + u1.y * q01.x));
+        // conj(u0) q01 + conj(u1) q11
+        a[r + 2] = mkc<SR>((u0.x * q01.x + u0.y * q01.y) + u1.x * q11,
+                           (u0.x * q01.y - u0.y * q01.x) - u1.y * q11);
+      }
+      const SC det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
+      const SR s = SMath<SR>::rcp(cabs2(det));
+      const SC idet = mkc<SR>(det.x * s, -det.y * s);
+      SC wm[2];
+      if (col == 0) {
+        wm[0] = cmul(a[3], idet);
+        wm[1] = cmul(mkc<SR>(-a[1].x, -a[1].y), idet);
+      } else {
+        wm[0] = cmul(mkc<SR>(-a[2].x, -a[2].y), idet);
+        wm[1] = cmul(a[0], idet);
+      }
+      const SR anorm = (cabs2(a[0]) + cabs2(a[1])) + (cabs2(a[2]) + cabs2(a[3]));
+      const SR wn = cabs2(wm[0]) + cabs2(wm[1]);
+      const bool fin = isfinite(wm[0].x) && isfinite(wm[0].y) && isfinite(wm[1].x) && isfinite(wm[1].y);
+      SC r0 = cadd(cmul(a[0], wm[0]), cmul(a[2], wm[1]));
+      SC r1 = cadd(cmul(a[1], wm[0]), cmul(a[3], wm[1]));
+      if (col == 0) r0.x -= SR(1); else r1.x -= SR(1);
+      const SR rn = cabs2(r0) + cabs2(r1);
+      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
+      // w^H Q w = q00 |w0|^2 + q11 |w1|^2 + 2 Re(conj(w0) q01 w1)
+      const SC qw1 = cmul(q01, wm[1]);
+      const SR en = (q00 * cabs2(wm[0]) + q11 * cabs2(wm[1])) +
+                    SR(2) * (wm[0].x * qw1.x + wm[0].y * qw1.y);
+      if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en)) {
+        const SR sc = SMath<SR>::rsq(en);
+        wr[2 * col] = mkc<SR>(wm[0].x * sc, wm[0].y * sc);
+        wr[2 * col + 1] = mkc<SR>(wm[1].x * sc, wm[1].y * sc);
+        w[2 * col] = make_double2(double(wr[2 * col].x), double(wr[2 * col].y));
+        w[2 * col + 1] = make_double2(double(wr[2 * col + 1].x), double(wr[2 * col + 1].y));
+        break;
+      }
+      if (attempt >= 1) {
+        bad_col = col;
+        return false;
+      }
+      ip_perturb(w + 2 * col, 2, rr, !restarted, seed, bin);
+      restarted = true;
+      wr[2 * col] = mkc<SR>(SR(w[2 * col].x), SR(w[2 * col].y));
+      wr[2 * col + 1] = mkc<SR>(SR(w[2 * col + 1].x), SR(w[2 * col + 1].y));
+    }
+  }
+  return true;
 }
 
 // ip_update_w (fastfca.cpp:36-72) on the reduced weighted covariances.
@@ -184,15 +278,18 @@ static __device__ __noinline__ void ip_perturb(double2* wcol, int m, Mt19937_64*
 // master W (updated in place).
 template <int M, typename SR>
 __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
-                                          unsigned long long seed, int bin, Mt19937_64* rng,
+                                          unsigned long long seed, int bin, RestartRng* rr,
                                           int& bad_col) {
+  if constexpr (M == 2) return ip_update_m2<SR>(w, qraw, invT, seed, bin, rr, bad_col);
   using SC = cplx_t<SR>;
-  bool seeded = false;
-  PolarNormal gauss{0.0, false};
+  bool restarted = false;
   SC wr[M * M];
 #pragma unroll
   for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
-#pragma unroll 1
+  // Unrolled for M <= 3: every register-array index is a compile-time
+  // constant (a rolled column loop indexes wr[] dynamically and demotes it to
+  // local memory); M = 4 keeps the rolled loop (the unrolled body spills).
+#pragma unroll(M <= 3 ? M : 1)
   for (int col = 0; col < M; ++col) {
     SC q[M * M];
     const double* p = qraw + col * M * M;
@@ -282,7 +379,8 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
         bad_col = col;
         return false;
       }
-      ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
+      ip_perturb(w + col * M, M, rr, !restarted, seed, bin);
+      restarted = true;
 #pragma unroll
       for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
     }
@@ -372,15 +470,14 @@ __device__ bool warp_log_abs_det2(const double2* w, cplx_t<SR>* scratch, int lan
 // ip_update_w (fastfca.cpp:36-72) by one warp.  scratch: 3*M*M + 2*M complex.
 template <int M, typename SR>
 __device__ bool ip_update_warp(double2* w, const double* qraw, double invT,
-                               unsigned long long seed, int bin, Mt19937_64* rng,
+                               unsigned long long seed, int bin, RestartRng* rng,
                                cplx_t<SR>* scratch, int lane, int& bad_col) {
   using SC = cplx_t<SR>;
   SC* Q = scratch;              // M x M
   SC* A = Q + M * M;            // M x (M+1) augmented, eliminated in place
   SC* A0 = A + M * (M + 1);     // M x M, W^H Q kept for the residual
   SC* Wc = A0 + M * M;          // M x M compute-type copy of W
-  bool seeded = false;
-  PolarNormal gauss{0.0, false};
+  bool restarted = false;
   for (int e = lane; e < M * M; e += 32) Wc[e] = mkc<SR>(SR(w[e].x), SR(w[e].y));
   for (int col = 0; col < M; ++col) {
     const double* p = qraw + col * M * M;
@@ -436,7 +533,8 @@ __device__ bool ip_update_warp(double2* w, const double* qraw, double invT,
         bad_col = col;
         return false;
       }
-      if (lane == 0) ip_perturb(w + col * M, M, rng, &seeded, &gauss, seed, bin);
+      if (lane == 0) ip_perturb(w + col * M, M, rng, !restarted, seed, bin);
+      restarted = true;
       __syncwarp();
       for (int e = lane; e < M * M; e += 32) Wc[e] = mkc<SR>(SR(w[e].x), SR(w[e].y));
       __syncwarp();
