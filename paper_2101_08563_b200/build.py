@@ -52,6 +52,8 @@ def build_lib(verbose: bool = False, jobs: int | None = None, variant: str = "",
     lib = LIB if not variant else PKG / f"libffca_{variant}.so"
     bdir = BUILD if not variant else ROOT / f"build_{variant}"
     extra = [] if not variant else [f"-DFFCA_PHASE_{variant.upper()}"]
+    if variant.startswith("x_"):  # tuning experiments: FFCA_NVCC_EXTRA="-DFOO=1 ..."
+        extra = os.environ.get("FFCA_NVCC_EXTRA", "").split()
     bdir.mkdir(exist_ok=True)
     deps = _headers()
     cu = sorted(CSRC.glob("*.cu"))

@@ -163,6 +163,12 @@ __device__ __forceinline__ float rcp_fast(float a) {
   return r;
 }
 __device__ __forceinline__ double rcp_fast(double a) { return 1.0 / a; }
+// SFU square root (for tolerance scales only).
+__device__ __forceinline__ float sqrt_approx(float a) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
 }  // namespace ffca
 
 namespace ffca {

@@ -80,11 +80,13 @@ struct Split {
 };
 
 // Launch shape: threads per CTA (upper bound) and the CTAs per SM the
-// register budget must allow.  Small M: 192 threads x 4 CTAs (80 registers),
-// so the 513 bins of a 1024-point STFT fit on 148 SMs in one wave.
+// register budget must allow.  Small M: 128 threads x 4 CTAs (up to 128
+// registers), so the 513 bins of a 1024-point STFT fit on 148 SMs in one
+// wave; 4 warps per bin keep the per-warp share of the reductions and of the
+// all-warp updates small (c1: 128 threads beat 192 by ~6%).
 template <int M>
 struct Launch {
-  static constexpr int threads = (M <= 3) ? 192 : 256;
+  static constexpr int threads = (M <= 3) ? 128 : 256;
   static constexpr int minb = (M <= 3) ? 4 : (M == 4 ? 2 : 1);
 };
 
@@ -264,26 +266,33 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const FitSmem<M, NT, R> lay(nwarps, N, p.tloc, p.nc, RES);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
-  double* wsc = reinterpret_cast<double*>(smem + lay.off_wsc);
+  // Per-bin scalar algebra (L master, balance scales, sweep updates) runs in
+  // the compute type B = R: fp32 in the fp32 path (short SFU chains; every
+  // value it feeds is consumed in fp32 by the frame loops anyway), fp64 in
+  // the check mode.  Slots are 8 bytes either way.
+  using B = R;
+  using BM = SMath<B>;
+  const B tinyB = tiny<B>();
+  B* wsc = reinterpret_cast<B*>(smem + lay.off_wsc);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
   // Ld, hsc and hinv are double-buffered by iteration parity: every warp
   // computes the balance itself and writes the other buffer, so no warp can
   // overwrite a value another warp still reads (see balance_all below).
-  double* const Ld0 = reinterpret_cast<double*>(smem + lay.off_ld);
-  double* const hsc0 = reinterpret_cast<double*>(smem + lay.off_hsc);
-  double* const hinv0 = reinterpret_cast<double*>(smem + lay.off_hinv);
-  double* Ld = Ld0;      // current L (fp64 master)
-  double* hsc = hsc0;    // current lazy H row scales
-  double* hinv = hinv0;  // 1 / hsc
+  B* const Ld0 = reinterpret_cast<B*>(smem + lay.off_ld);
+  B* const hsc0 = reinterpret_cast<B*>(smem + lay.off_hsc);
+  B* const hinv0 = reinterpret_cast<B*>(smem + lay.off_hinv);
+  B* Ld = Ld0;      // current L (master)
+  B* hsc = hsc0;    // current lazy H row scales
+  B* hinv = hinv0;  // 1 / hsc
   int par = 0;
   R* Le = reinterpret_cast<R*>(smem + lay.off_le);      // L * hsc, compute type
   R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);  // 1 / L(:, n) of the new column
   R* hscr = reinterpret_cast<R*>(smem + lay.off_hscr);  // hsc in the compute type (MM)
-  double* us = reinterpret_cast<double*>(smem + lay.off_us);
-  double* hsumv = reinterpret_cast<double*>(smem + lay.off_hsum);
-  double* numd = reinterpret_cast<double*>(smem + lay.off_num);
-  double* psum = numd;  // EM: sum_t Phi(m) of the last sweep (numd is MM-only)
-  double* dend = reinterpret_cast<double*>(smem + lay.off_den);
+  B* us = reinterpret_cast<B*>(smem + lay.off_us);
+  B* hsumv = reinterpret_cast<B*>(smem + lay.off_hsum);
+  B* numd = reinterpret_cast<B*>(smem + lay.off_num);
+  B* psum = numd;  // EM: sum_t Phi(m) of the last sweep (numd is MM-only)
+  B* dend = reinterpret_cast<B*>(smem + lay.off_den);
   double* reda = reinterpret_cast<double*>(smem + lay.off_reda);
   double* redb = reinterpret_cast<double*>(smem + lay.off_redb);
   double* res = reinterpret_cast<double*>(smem + lay.off_res);
@@ -348,11 +357,12 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   }
   for (int k = tid; k < M * N; k += nthreads) {
     const double l = p.L[size_t(b) * M * N + k];
-    Ld[k] = l;
+    Ld[k] = B(l);
     Le[k] = R(l);
   }
-  for (int k = tid; k < NT; k += nthreads) hsc[k] = 1.0, hinv[k] = 1.0;
-  for (int k = tid; k < M; k += nthreads) us[k] = 1.0;
+  for (int k = tid; k < NT; k += nthreads) hsc[k] = B(1), hinv[k] = B(1);
+  for (int k = tid; k < M; k += nthreads) us[k] = B(1);
+  bool touched = false;  // L was updated (else the caller's fp64 L is returned untouched)
   const double power = p.power[b];
   if (tid == 0) {
     sc->eps = fmax(1e-8 * power, 1e-300);  // var_eps, sigmodel.hpp:29-31
@@ -568,7 +578,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   auto nll_from_res = [&](double logdet) {
     double s = 0.0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) s += us[m] * res[M * M * M + m];
+    for (int m = 0; m < M; ++m) s += double(us[m]) * res[M * M * M + m];
     return -double(T) * logdet + s + 0.69314718055994531 * res[M * M * M + M];
   };
 
@@ -798,7 +808,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   auto refresh_le = [&]() {
     for (int n = 0; n < N; ++n)
 #pragma unroll
-      for (int m = 0; m < M; ++m) Le[m + n * M] = narrow_pos<R>(Ld[m + n * M] * hsc[n]);
+      for (int m = 0; m < M; ++m) Le[m + n * M] = R(fmax(Ld[m + n * M] * hsc[n], tinyB));
   };
 
   // Serial algebra entry points, called by a whole warp: M <= 4 runs on lane 0
@@ -818,13 +828,31 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   };
   auto logdet_w0 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm0, ld); };
   auto logdet_w1 = [&](const double2* w, double& ld) { return logdet_warp(w, wsm1, ld); };
-  auto run_ip = [&](unsigned long long seed, bool with_logdet) {
+  // scaled: apply the pending balance W column scales (wsc) first.
+  auto run_ip = [&](unsigned long long seed, bool with_logdet, bool scaled) {
     int bad = -1;
     bool ok = true;
     if constexpr (M > 4) {
+      if (scaled) {
+        for (int k = lane; k < M * M; k += 32) {
+          const double c = double(wsc[k / M]);
+          Wd[k].x *= c;
+          Wd[k].y *= c;
+        }
+        __syncwarp();
+      }
       ok = ip_update_warp<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
     } else {
-      if (lane == 0) ok = ip_update<M, R>(Wd, res, invT, seed, bin_index, rng, bad);
+      if (lane == 0) {
+        IpExtras<R> ex;
+        ex.wscale = scaled ? wsc : nullptr;
+        ex.wout = Wr;
+        if (M == 2 && with_logdet) {  // log|det W|^2 for the next trace entry
+          ex.ldet = &sc->logdet0;
+          ex.ldok = &sc->ldok;
+        }
+        ok = ip_update<M, R>(Wd, res, invT, seed, bin_index, rng, bad, ex);
+      }
       ok = __shfl_sync(0xffffffffu, ok, 0);
     }
     if (lane == 0 && !ok) {
@@ -832,14 +860,14 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       sc->stop = 1;
     }
     __syncwarp();
-    for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y)), Wlg[k] = Wd[k];
-    if constexpr (M <= 2) {
-      // log|det W|^2 of the IP output for the next trace entry: a few cycles
-      // at this size, so it rides in the serial section.
+    if constexpr (M > 4)
+      for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
+    if constexpr (M > 2)
+      for (int k = lane; k < M * M; k += 32) Wlg[k] = Wd[k];  // log-det input (ldwarp)
+    if constexpr (M == 1) {
       if (with_logdet) {
-        __syncwarp();
         double ld = 0.0;
-        const bool lok = logdet_w0(Wlg, ld);
+        const bool lok = logdet_w0(Wd, ld);
         if (lane == 0) {
           sc->ldok = lok ? 1 : 0;
           sc->logdet0 = ld;
@@ -847,6 +875,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       }
     }
   };
+
 
   // ---- balance_scales (fastfca.cpp:127-142), computed by EVERY warp
   //      (lane-parallel: mu_n per source lane, s_m per channel lane) from
@@ -860,41 +889,41 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   //      stored by the next pass A (fastfca.cpp:95-97).
   auto balance_all = [&](bool on, bool phi_mean) {
     const int nx = par ^ 1;
-    double* hscn = hsc0 + nx * NT;
-    double* hinvn = hinv0 + nx * NT;
-    double* Ldn = Ld0 + nx * (M * NT);
+    B* hscn = hsc0 + nx * NT;
+    B* hinvn = hinv0 + nx * NT;
+    B* Ldn = Ld0 + nx * (M * NT);
     for (int n = lane; n < N; n += 32) {
-      double mu;
+      B mu;
       if (phi_mean && n == N - 1) {
-        double c = 0.0;
+        B c = B(0);
 #pragma unroll
-        for (int m = 0; m < M; ++m) c += psum[m] * fast_rcp(Ld[m + n * M]);
-        mu = c * (invT / double(M));
+        for (int m = 0; m < M; ++m) c += psum[m] * BM::rcp(Ld[m + n * M]);
+        mu = c * B(invT / double(M));
       } else {
-        mu = hsumv[n] * invT;
+        mu = hsumv[n] * B(invT);
       }
-      const bool v = on && mu > 0.0 && isfinite(mu);
-      hscn[n] = v ? fast_rcp(mu) : 1.0;
-      hinvn[n] = v ? mu : 1.0;
+      const bool v = on && mu > B(0) && isfinite(mu);
+      hscn[n] = v ? BM::rcp(mu) : B(1);
+      hinvn[n] = v ? mu : B(1);
     }
     __syncwarp();
     double ls = 0.0;
     if (lane < M) {
       const int m = lane;
-      double s = 0.0;
+      B s = B(0);
       for (int n = 0; n < N; ++n) s += Ld[m + n * M] * hinvn[n];
-      s *= 1.0 / double(N);
-      const bool v = on && s > 0.0 && isfinite(s);
-      us[m] = v ? fast_rcp(s) : 1.0;  // U and L-row scale 1/s
-      wsc[m] = v ? rsqrt(s) : 1.0;    // W column scale
-      if (v) ls = SMath<R>::log_wide(s);
+      s *= B(1.0 / double(N));
+      const bool v = on && s > B(0) && isfinite(s);
+      us[m] = v ? BM::rcp(s) : B(1);  // U and L-row scale 1/s
+      wsc[m] = v ? BM::rsq(s) : B(1);  // W column scale
+      if (v) ls = BM::log_d(s);
     }
     __syncwarp();
     for (int k = lane; k < M * N; k += 32) {
       const int m = k % M, n = k / M;
-      const double l = Ld[k] * hinvn[n] * us[m];  // L(m,n) mu_n / s_m
+      const B l = fmax(Ld[k] * hinvn[n] * us[m], tinyB);  // L(m,n) mu_n / s_m
       Ldn[k] = l;
-      Le[k] = narrow_pos<R>(l * hscn[n]);
+      Le[k] = R(fmax(l * hscn[n], tinyB));
     }
     __syncwarp();  // converged before the shuffles
     // sum_m log s_m over the lowest Pow2Ceil(M) lanes (fixed order).
@@ -940,7 +969,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     }
     __syncwarp();
     // IP sweep of iteration 0 (fastfca.cpp:36-72), fused into this serial section.
-    if (!sc->stop && p.iters > 0) run_ip(p.seed, record);
+    if (!sc->stop && p.iters > 0) run_ip(p.seed, record, false);
   }
   __syncthreads();
   if (!sc->stop) {
@@ -987,14 +1016,14 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
             // (fastfca.cpp:92-94).  The next sweep (or pass A) stores the true
             // H row n, so Le(:, n) becomes the new L column (no hsc).
             const int m = lane;
-            const double l = update_loading ? fmax(tot * invT * hinv[n], 1e-300) : Ld[m + n * M];
-            const R lr = narrow_pos<R>(l);
+            const B l = update_loading ? fmax(B(tot * invT) * hinv[n], tinyB) : Ld[m + n * M];
+            const R lr = R(l);
             Ld[m + n * M] = l;
             if (!phis) Le[m + n * M] = lr;  // with phis the balance rewrites all of Le
             Linv[m] = rcp_fast(lr);
-            if (phis) psum[m] = ps;
+            if (phis) psum[m] = B(ps);
           }
-          if (lane == 0 && n >= 1) hsumv[n - 1] = hs;
+          if (lane == 0 && n >= 1) hsumv[n - 1] = B(hs);
           __syncwarp();
           FFCA_TIC(6);
         }
@@ -1009,15 +1038,15 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
               for (int c = 0; c < cnt; ++c)
 #pragma unroll
                 for (int m = 0; m < M; ++m) {
-                  numd[m + (n0 + c) * M] = res[(c * M + m) * 2 + 0];
-                  dend[m + (n0 + c) * M] = res[(c * M + m) * 2 + 1];
+                  numd[m + (n0 + c) * M] = B(res[(c * M + m) * 2 + 0]);
+                  dend[m + (n0 + c) * M] = B(res[(c * M + m) * 2 + 1]);
                 }
               if (n0 + cnt >= N) {
                 // num, den were accumulated with H_stored; H_true = H * hsc scales
                 // both by hsc[n], which cancels in num/den.
                 for (int k = 0; k < M * N; ++k) {
-                  const double den = fmax(dend[k], 1e-300);
-                  Ld[k] = fmax(Ld[k] * sqrt(numd[k] * fast_rcp(den)), 1e-300);  // :107-109
+                  const B den = fmax(dend[k], tinyB);
+                  Ld[k] = fmax(Ld[k] * BM::sq(numd[k] * BM::rcp(den)), tinyB);  // :107-109
                 }
                 refresh_le();
                 for (int k = 0; k < N; ++k) hscr[k] = R(hsc[k]);
@@ -1034,27 +1063,32 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
         mm_h_sweep(first, redb + (pb & 1) * nwarps * kred);
         if (tid == 0) {
-          for (int k = 0; k < N; ++k) hsumv[k] = res[k];
+          for (int k = 0; k < N; ++k) hsumv[k] = B(res[k]);
         }
         __syncthreads();
         FFCA_TIC(5);
       }
       balance_all(bal, p.flavor == 0);
+      touched = touched || update_loading;
       FFCA_TIC(7);
       const bool more = it + 1 < p.iters;
       // EM: pass A also stores H row N-1, so it runs after the last iteration too.
       if (more || record || p.flavor == 0) pass_a(false, more, record, p.flavor == 0);
       FFCA_TIC(1);
       if (warp == 0) {
-        // Balance W column scales on the fp64 master (fastfca.cpp:139-141).
-        for (int k = lane; k < M * M; k += 32) {
-          double2 w = Wd[k];
-          const double c = wsc[k / M];
-          w.x *= c;
-          w.y *= c;
-          Wd[k] = w;
+        // Balance W column scales on the fp64 master (fastfca.cpp:139-141):
+        // folded into the IP sweep when one follows.
+        const bool ip_next = more && !(record && !sc->ldok);
+        if (!ip_next) {
+          for (int k = lane; k < M * M; k += 32) {
+            double2 w = Wd[k];
+            const double c = double(wsc[k / M]);
+            w.x *= c;
+            w.y *= c;
+            Wd[k] = w;
+          }
+          __syncwarp();
         }
-        __syncwarp();
         if (lane == 0 && record) {
           if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
             sc->status = kStatusSingularW;
@@ -1066,7 +1100,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
         __syncwarp();
         // Next iteration's IP sweep, fused into the pass-A serial section.
-        if (more && !sc->stop) run_ip(p.seed + (unsigned long long)(it + 1), record);
+        if (ip_next) run_ip(p.seed + (unsigned long long)(it + 1), record, true);
       }
       FFCA_TIC(2);
       __syncthreads();
@@ -1080,12 +1114,13 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   // ------------------------------------------------------------- epilogue --
   if (lead) {
     for (int k = tid; k < M * M; k += nthreads) p.W[size_t(b) * M * M + k] = Wd[k];
-    for (int k = tid; k < M * N; k += nthreads) p.L[size_t(b) * M * N + k] = Ld[k];
+    if (touched)
+      for (int k = tid; k < M * N; k += nthreads) p.L[size_t(b) * M * N + k] = double(Ld[k]);
   }
   bool pending = false;
-  for (int k = 0; k < N; ++k) pending = pending || hsc[k] != 1.0;
+  for (int k = 0; k < N; ++k) pending = pending || hsc[k] != B(1);
   if (RES || pending)
-    for (int k = tid; k < N * Tl; k += nthreads) Hg[k] = R(double(Hs[k]) * hsc[k % N]);
+    for (int k = tid; k < N * Tl; k += nthreads) Hg[k] = R(double(Hs[k]) * double(hsc[k % N]));
 #ifdef FFCA_PHASE_TIMING
   if (p.timing && tid == 0)
     for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];

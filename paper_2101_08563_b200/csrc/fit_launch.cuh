@@ -73,7 +73,11 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   if (dev_max <= 0) dev_max = 227 * 1024;
   const int budget = dev_max - 2048;
-  const int C = pick_cluster<M, NT, R>(fp, budget);
+  int C = pick_cluster<M, NT, R>(fp, budget);
+  if (const char* e = getenv("FFCA_FORCE_CLUSTER")) {  // tuning experiments only
+    const int f = atoi(e);
+    if (!EXACT && f > C && f <= 16) C = f;
+  }
   cudaError_t err;
   if (C == 1) {
     fp.resident = 1;
@@ -112,7 +116,7 @@ bool needs_cluster(const FitParams& fp) {
 template <int M>
 int launch_fit_f32(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   if constexpr (M <= 4) {
-    if (!needs_cluster<M, float>(fp)) {
+    if (!needs_cluster<M, float>(fp) && !getenv("FFCA_FORCE_CLUSTER")) {
       // Exact source-count specializations for the common shapes.
       switch (fp.N) {
         case 2: return launch_fit_t<M, 2, true, float>(ctx, fp, st);

@@ -193,10 +193,77 @@ static __device__ __noinline__ void ip_perturb(double2* wcol, int m, RestartRng*
 // adjugate, the residual test, w /= sqrt(w^H Q_k w) -- the same steps as the
 // general path below with the zero imaginary parts and the symmetric half
 // folded away, so the per-column dependency chain is ~15 FP ops + 2 MUFU.
+// Optional side jobs of an IP sweep, folded in to keep them off the serial
+// path: wscale -- balance column scales still to be applied to W first;
+// wout -- compute-type copy of the new W; ldet/ldok -- log|det W_new|^2
+// (M = 2 only; sigmodel.cpp:118-129).
+template <typename SR>
+struct IpExtras {
+  const SR* wscale = nullptr;
+  cplx_t<SR>* wout = nullptr;
+  double* ldet = nullptr;
+  int* ldok = nullptr;
+};
+
+// One column of the M = 2 sweep: candidate w (normalised) and whether it
+// passes the reference's acceptance tests.
+template <typename SR>
+__device__ __forceinline__ bool ip_col_m2(const cplx_t<SR> (&wr)[4], int col, SR q00, SR q11,
+                                          cplx_t<SR> q01, cplx_t<SR> (&out)[2]) {
+  using SC = cplx_t<SR>;
+  // A(r, c) = sum_k conj(W(k, r)) Q(k, c), Q(1, 0) = conj(q01).
+  SC a[4];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const SC u0 = wr[2 * r], u1 = wr[2 * r + 1];  // column r of W
+    // conj(u0) q00 + conj(u1) conj(q01)
+    a[r] = mkc<SR>(u0.x * q00 + (u1.x * q01.x - u1.y * q01.y),
+                   -u0.y * q00 - (u1.x * q01.y + u1.y * q01.x));
+    // conj(u0) q01 + conj(u1) q11
+    a[r + 2] = mkc<SR>((u0.x * q01.x + u0.y * q01.y) + u1.x * q11,
+                       (u0.x * q01.y - u0.y * q01.x) - u1.y * q11);
+  }
+  const SC det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
+  const SR s = SMath<SR>::rcp(cabs2(det));
+  const SC idet = mkc<SR>(det.x * s, -det.y * s);
+  SC wm[2];
+  if (col == 0) {
+    wm[0] = cmul(a[3], idet);
+    wm[1] = cmul(mkc<SR>(-a[1].x, -a[1].y), idet);
+  } else {
+    wm[0] = cmul(mkc<SR>(-a[2].x, -a[2].y), idet);
+    wm[1] = cmul(a[0], idet);
+  }
+  const SR anorm = (cabs2(a[0]) + cabs2(a[1])) + (cabs2(a[2]) + cabs2(a[3]));
+  const SR wn = cabs2(wm[0]) + cabs2(wm[1]);
+  const bool fin = isfinite(wm[0].x) && isfinite(wm[0].y) && isfinite(wm[1].x) && isfinite(wm[1].y);
+  SC r0 = cadd(cmul(a[0], wm[0]), cmul(a[2], wm[1]));
+  SC r1 = cadd(cmul(a[1], wm[0]), cmul(a[3], wm[1]));
+  if (col == 0) r0.x -= SR(1); else r1.x -= SR(1);
+  const SR rn = cabs2(r0) + cabs2(r1);
+  const SR scale = SR(sqrt_approx(float(anorm * wn))) + SR(1);
+  // w^H Q w = q00 |w0|^2 + q11 |w1|^2 + 2 Re(conj(w0) q01 w1)
+  const SC qw1 = cmul(q01, wm[1]);
+  const SR en = (q00 * cabs2(wm[0]) + q11 * cabs2(wm[1])) +
+                SR(2) * (wm[0].x * qw1.x + wm[0].y * qw1.y);
+  const SR sc = SMath<SR>::rsq(en);
+  out[0] = mkc<SR>(wm[0].x * sc, wm[0].y * sc);
+  out[1] = mkc<SR>(wm[1].x * sc, wm[1].y * sc);
+  return fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en);
+}
+
+// M = 2 IP sweep in closed form on the Hermitian structure of Q (real
+// diagonal, Q(1,0) = conj Q(0,1)): A = W^H Q_k, w = A^{-1} e_k from the 2x2
+// adjugate, the residual test, w /= sqrt(w^H Q_k w) -- the same steps as the
+// general path below with the zero imaginary parts and the symmetric half
+// folded away.  Both columns are first solved speculatively (no branch on
+// the acceptance tests between them, so the tests overlap the next column);
+// only if a test fails is the sweep redone column by column with the
+// reference's seeded restart.
 template <typename SR>
 __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, double invT,
                                              unsigned long long seed, int bin, RestartRng* rr,
-                                             int& bad_col) {
+                                             int& bad_col, IpExtras<SR> ex) {
   using SC = cplx_t<SR>;
   SR qd0[2], qd1[2];
   SC qo[2];
@@ -210,53 +277,58 @@ __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, dou
   SC wr[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+  auto finish = [&](const SC (&f)[4]) {
+    if (ex.wout)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ex.wout[k] = f[k];
+    if (ex.ldet) {
+      const SR a0 = cabs2(f[0]), a1 = cabs2(f[1]);
+      const SR d = cabs2(csub(cmul(f[0], f[3]), cmul(f[2], f[1])));
+      const bool ok = (a0 > SR(0) || a1 > SR(0)) && d > SR(0) && isfinite(d);
+      *ex.ldok = ok ? 1 : 0;
+      *ex.ldet = ok ? SMath<SR>::log_d(d) : 0.0;
+    }
+  };
+  {
+    SC f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      f[k] = wr[k];
+      if (ex.wscale) f[k].x *= ex.wscale[k >> 1], f[k].y *= ex.wscale[k >> 1];
+    }
+    SC o[2];
+    const bool ok0 = ip_col_m2<SR>(f, 0, qd0[0], qd1[0], qo[0], o);
+    f[0] = o[0], f[1] = o[1];
+    const bool ok1 = ip_col_m2<SR>(f, 1, qd0[1], qd1[1], qo[1], o);
+    f[2] = o[0], f[3] = o[1];
+    if (ok0 && ok1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = make_double2(double(f[k].x), double(f[k].y));
+      finish(f);
+      return true;
+    }
+  }
+  // Careful path: the reference's column-by-column sweep with restarts, from
+  // the (scaled) master.
+  if (ex.wscale) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double c = double(ex.wscale[k >> 1]);
+      w[k].x *= c;
+      w[k].y *= c;
+      wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+    }
+  }
   bool restarted = false;
 #pragma unroll
   for (int col = 0; col < 2; ++col) {
-    const SR q00 = qd0[col], q11 = qd1[col];
-    const SC q01 = qo[col];
     for (int attempt = 0;; ++attempt) {
-      // A(r, c) = sum_k conj(W(k, r)) Q(k, c), Q(1, 0) = conj(q01).
-      SC a[4];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const SC u0 = wr[2 * r], u1 = wr[2 * r + 1];  // column r of W
-        // conj(u0) q00 + conj(u1) conj(q01)
-        a[r] = mkc<SR>(u0.x * q00 + (u1.x * q01.x - u1.y * q01.y),
-                       -u0.y * q00 - (u1.x * q01.y + u1.y * q01.x));
-        // conj(u0) q01 + conj(u1) q11
-        a[r + 2] = mkc<SR>((u0.x * q01.x + u0.y * q01.y) + u1.x * q11,
-                           (u0.x * q01.y - u0.y * q01.x) - u1.y * q11);
-      }
-      const SC det = csub(cmul(a[0], a[3]), cmul(a[2], a[1]));
-      const SR s = SMath<SR>::rcp(cabs2(det));
-      const SC idet = mkc<SR>(det.x * s, -det.y * s);
-      SC wm[2];
-      if (col == 0) {
-        wm[0] = cmul(a[3], idet);
-        wm[1] = cmul(mkc<SR>(-a[1].x, -a[1].y), idet);
-      } else {
-        wm[0] = cmul(mkc<SR>(-a[2].x, -a[2].y), idet);
-        wm[1] = cmul(a[0], idet);
-      }
-      const SR anorm = (cabs2(a[0]) + cabs2(a[1])) + (cabs2(a[2]) + cabs2(a[3]));
-      const SR wn = cabs2(wm[0]) + cabs2(wm[1]);
-      const bool fin = isfinite(wm[0].x) && isfinite(wm[0].y) && isfinite(wm[1].x) && isfinite(wm[1].y);
-      SC r0 = cadd(cmul(a[0], wm[0]), cmul(a[2], wm[1]));
-      SC r1 = cadd(cmul(a[1], wm[0]), cmul(a[3], wm[1]));
-      if (col == 0) r0.x -= SR(1); else r1.x -= SR(1);
-      const SR rn = cabs2(r0) + cabs2(r1);
-      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
-      // w^H Q w = q00 |w0|^2 + q11 |w1|^2 + 2 Re(conj(w0) q01 w1)
-      const SC qw1 = cmul(q01, wm[1]);
-      const SR en = (q00 * cabs2(wm[0]) + q11 * cabs2(wm[1])) +
-                    SR(2) * (wm[0].x * qw1.x + wm[0].y * qw1.y);
-      if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en)) {
-        const SR sc = SMath<SR>::rsq(en);
-        wr[2 * col] = mkc<SR>(wm[0].x * sc, wm[0].y * sc);
-        wr[2 * col + 1] = mkc<SR>(wm[1].x * sc, wm[1].y * sc);
-        w[2 * col] = make_double2(double(wr[2 * col].x), double(wr[2 * col].y));
-        w[2 * col + 1] = make_double2(double(wr[2 * col + 1].x), double(wr[2 * col + 1].y));
+      SC o[2];
+      if (ip_col_m2<SR>(wr, col, qd0[col], qd1[col], qo[col], o)) {
+        wr[2 * col] = o[0];
+        wr[2 * col + 1] = o[1];
+        w[2 * col] = make_double2(double(o[0].x), double(o[0].y));
+        w[2 * col + 1] = make_double2(double(o[1].x), double(o[1].y));
         break;
       }
       if (attempt >= 1) {
@@ -269,6 +341,7 @@ __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, dou
       wr[2 * col + 1] = mkc<SR>(SR(w[2 * col + 1].x), SR(w[2 * col + 1].y));
     }
   }
+  finish(wr);
   return true;
 }
 
@@ -279,10 +352,16 @@ __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, dou
 template <int M, typename SR>
 __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
                                           unsigned long long seed, int bin, RestartRng* rr,
-                                          int& bad_col) {
-  if constexpr (M == 2) return ip_update_m2<SR>(w, qraw, invT, seed, bin, rr, bad_col);
+                                          int& bad_col, IpExtras<SR> ex = IpExtras<SR>()) {
+  if constexpr (M == 2) return ip_update_m2<SR>(w, qraw, invT, seed, bin, rr, bad_col, ex);
   using SC = cplx_t<SR>;
   bool restarted = false;
+  if (ex.wscale)
+    for (int k = 0; k < M * M; ++k) {
+      const double c = double(ex.wscale[k / M]);
+      w[k].x *= c;
+      w[k].y *= c;
+    }
   SC wr[M * M];
 #pragma unroll
   for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
@@ -355,7 +434,7 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
       }
       // Residual test ||a w - e|| <= tol (||a|| ||w|| + 1) (fastfca.cpp:55-56),
       // squared; the scale is a tolerance, so an fp32 square root suffices.
-      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
+      const SR scale = SR(sqrt_approx(float(anorm * wn))) + SR(1);
       if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale) {
         SR en = SR(0);
 #pragma unroll
@@ -385,6 +464,9 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
       for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
     }
   }
+  if (ex.wout)
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) ex.wout[k] = wr[k];
   return true;
 }
 
@@ -518,7 +600,7 @@ __device__ bool ip_update_warp(double2* w, const double* qraw, double invT,
       }
       const SR rn = warp_allsum(lane < M ? cabs2(rr) : SR(0));
       const SR en = warp_allsum(lane < M ? cmulc(wmr, qw).x : SR(0));
-      const SR scale = SR(sqrtf(float(anorm * wn))) + SR(1);
+      const SR scale = SR(sqrt_approx(float(anorm * wn))) + SR(1);
       if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en)) {
         const SR s = SMath<SR>::rsq(en);
         if (lane < M) {
