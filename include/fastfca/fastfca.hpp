@@ -52,6 +52,15 @@ std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>&
                                                 const FastFcaOptions& opts = {},
                                                 const GpuOptions& gpu = {});
 
+// Determined ICA mode (fastfca.hpp:76-78, fastfca.cpp:241-264): sources ==
+// dim, L = identity, H = floored decorrelated powers of w_init (computed on
+// the GPU), then IP+MM with the loadings fixed.
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit = {});
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit,
+                              const GpuOptions& gpu);
+
 // Decomposed multichannel Wiener filter (fastfca.cpp:205-223).
 std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params);
 std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params,

@@ -54,6 +54,8 @@ struct FastFcaParams {  // sigmodel.hpp:72-78
 // Negative log-likelihood (sigmodel.cpp:155-162, 215-222) evaluated on the GPU
 // in fp64 (check-mode kernels); per-bin values are summed in bin order.
 double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& params);
+// |W^H x|^2 of bin i (sigmodel.cpp:93-107), on the GPU (fp64).
+RMat decorrelated_powers(const SampleCovSet& covs, int i, const CMat& w);
 double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RMat& loading,
                         const RMat& act);
 

@@ -96,6 +96,25 @@ int ffca_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts, co
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status);
 
+/* ica_mode_fit (fastfca.hpp:76-78, fastfca.cpp:241-264): determined ICA mode.
+ * dims->sources must equal dims->dim (else FFCA_INVALID_ARGUMENT with the
+ * reference's message).  W: w_init on entry, the fitted W on return; L, H are
+ * outputs only (L = identity, H = floored decorrelated powers of w_init, then
+ * IP+MM with the loadings fixed).  opts->flavor / fix_loadings /
+ * normalize_scales are ignored (the mode fixes them), and so is
+ * opts->precision: this mode always runs the fp64 kernels (at its fixed point
+ * H tracks |w^H x|^2 and the 1/H weights amplify fp32 cancellation, so an
+ * fp32 trajectory cannot follow the reference's).  The rest as ffca_fit. */
+int ffca_ica_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts, const double* x,
+                 const double* power, double* W, double* L, double* H, double* nll,
+                 double* nll_slots, int32_t* bin_status);
+
+/* decorrelated_powers (sigmodel.cpp:93-107): out [batch][bins][frames][dim]
+ * = |W^H x|^2 per bin (the Eigen col-major dim x frames matrix), floored as
+ * floor_positive(u, floor_rel) (sigmodel.cpp:10-15) when floor_rel >= 0. */
+int ffca_decorrelated_powers(ffca_ctx* ctx, const ffca_dims* dims, int precision, const double* x,
+                             const double* W, double floor_rel, double* out);
+
 /* fastfca_separate (fastfca.hpp:65-66, fastfca.cpp:205-223). */
 int ffca_separate(ffca_ctx* ctx, const ffca_dims* dims, int precision, const double* x,
                   const double* W, const double* L, const double* H, double* images);

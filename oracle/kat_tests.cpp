@@ -611,6 +611,74 @@ TEST(fit_worker_count_invariance) {
   for (int i = 0; i < 6; ++i) CHECK(rel_err(a.params.decorr[i], b.params.decorr[i]) == 0.0);
 }
 
+// test_fastfca.cpp:452-490: determined ICA mode separates an instantaneous
+// 2x2 mixture of AR(1) log-power sources (same generator draws).
+TEST(ica_mode_unmixes_determined_mixture) {
+  // Shipped-eps behaviour only: without eps the fixed one-hot loadings let H
+  // converge onto U exactly and the IP system goes singular (the reference
+  // ships with eps, which is what this test exercises).
+  if (kNoEps) return;
+  std::mt19937 rng(77);
+  const int m = 2, bins = 4, frames = 600;
+  CMat mixing = random_complex(m, m, rng);
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < m; ++c) mixing(r, c) = (r == c ? 1.0 : 0.0) + 0.6 * mixing(r, c);
+  std::vector<CMat> f(bins, CMat(m, frames));
+  for (int i = 0; i < bins; ++i) {
+    RMat logh(m, frames);
+    for (int n = 0; n < m; ++n) {
+      double state = randn(rng);
+      for (int j = 0; j < frames; ++j) {
+        state = 0.97 * state + std::sqrt(1 - 0.97 * 0.97) * randn(rng);
+        logh(n, j) = 1.5 * state;
+      }
+    }
+    for (int j = 0; j < frames; ++j) {
+      std::vector<Complex> y(m);
+      for (int n = 0; n < m; ++n) y[n] = std::exp(0.5 * logh(n, j)) * crandn(rng);
+      for (int r = 0; r < m; ++r) {
+        Complex acc = 0.0;
+        for (int n = 0; n < m; ++n) acc += mixing(r, n) * y[n];
+        f[i](r, j) = acc;
+      }
+    }
+  }
+  SampleCovSet covs;
+  covs.dim = m;
+  covs.bins = bins;
+  covs.frames = frames;
+  covs.snapshots = f;
+  for (int i = 0; i < bins; ++i) {
+    double s = 0.0;
+    for (const Complex& v : f[i].a) s += std::norm(v);
+    covs.power_scale.push_back(s / (double(frames) * m));
+  }
+  std::vector<CMat> w_init(bins, CMat::identity(m));
+  const FastFcaFitResult fit = ica_mode_fit(covs, m, 80, w_init);
+  check_trace_monotone(fit.nll);
+  double leak_total = 0.0;
+  for (int i = 0; i < bins; ++i) {
+    const CMat& w = fit.params.decorr[i];
+    double e[2][2];
+    for (int r = 0; r < m; ++r)
+      for (int c = 0; c < m; ++c) {
+        Complex g = 0.0;  // (W^H mixing)(r, c)
+        for (int k = 0; k < m; ++k) g += std::conj(w(k, r)) * mixing(k, c);
+        e[r][c] = std::norm(g);
+      }
+    const double direct = std::max(e[0][0] + e[1][1], e[0][1] + e[1][0]);
+    leak_total += 1.0 - direct / (e[0][0] + e[0][1] + e[1][0] + e[1][1]);
+  }
+  CHECK(leak_total / bins <= 0.05);
+  bool threw = false;
+  try {
+    ica_mode_fit(covs, m + 1, 1, w_init);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+}
+
 int main(int argc, char** argv) {
   const std::string only = argc > 1 ? argv[1] : "";
   for (const Entry& e : tests()) {

@@ -479,6 +479,31 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
   return result;
 }
 
+// fastfca.cpp:241-264
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit,
+                              std::vector<double>* slots_out) {
+  if (sources != covs.dim)
+    throw std::invalid_argument("ica_mode_fit: requires as many sources as channels");
+  if (static_cast<int>(w_init.size()) != covs.bins)
+    throw std::invalid_argument("ica_mode_fit: one W per frequency required");
+  FastFcaParams params;
+  params.dim = covs.dim;
+  params.bins = covs.bins;
+  params.frames = covs.frames;
+  params.sources = sources;
+  params.decorr = w_init;
+  for (int i = 0; i < covs.bins; ++i) {
+    params.loading.push_back(RMat::identity(covs.dim));  // dim == sources
+    RMat u = decorrelated_powers(covs, i, w_init[i]);
+    floor_positive(u);
+    params.act.push_back(u);
+  }
+  FastFcaOptions opts;
+  opts.fix_loadings = true;
+  return fastfca_fit(covs, params, LhFlavor::mm, iters, fit, opts, slots_out);
+}
+
 // fastfca.cpp:193-203
 CMat fastfca_mwf(const FastFcaParams& p, int i, int j, int n) {
   const int m = p.dim;

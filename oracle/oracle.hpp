@@ -145,6 +145,11 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
                              std::vector<double>* slots_out = nullptr);  // fastfca.cpp:146-191
 // slots_out (optional): the per-bin nll_slots matrix, [(iters+1)][bins]
 // (fastfca.cpp:155-156), which the driver sums in bin order.
+// Determined ICA mode (fastfca.cpp:241-264): L = identity, H = floored
+// decorrelated powers of w_init, IP+MM with the loadings fixed.
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit = {},
+                              std::vector<double>* slots_out = nullptr);
 CMat fastfca_mwf(const FastFcaParams& p, int i, int j, int n);     // fastfca.cpp:193-203
 // Separated images, [n][i] -> dim x frames (fastfca.cpp:205-223).
 std::vector<std::vector<CMat>> fastfca_separate(const SampleCovSet& covs,

@@ -36,6 +36,8 @@ def lib() -> C.CDLL:
         L.oracle_ip_update_w.argtypes = [i, i, i, P, P, P, P, u64, P, i]
         L.oracle_lh_update.argtypes = [i, i, i, i, P, P, P, i, d, P, i]
         L.oracle_source_gain.argtypes = [i, i, i, P, P, i, P, P, i]
+        L.oracle_ica_fit.argtypes = [i, i, i, i, P, P, P, P, i, i, u64, i, P, P, i]
+        L.oracle_decorrelated_powers.argtypes = [i, i, i, P, P, d, P, P, i]
         _lib = L
     return _lib
 
@@ -104,6 +106,32 @@ def fit(x, W, L, H, iters, flavor=0, record_trace=True, seed=0, normalize_scales
     if not batched:
         return Wo[0], Lo[0], Ho[0], nll[0], (sl[0] if slots else None), secs.value
     return Wo, Lo, Ho, nll, sl, secs.value
+
+
+def ica_fit(x, W_init, iters, record_trace=True, seed=0, workers=1):
+    """ica_mode_fit (fastfca.cpp:241-264) on one mixture x [F,M,T] from W_init
+    [F,M,M].  Returns (W, L, H, nll)."""
+    F, M, T = x.shape
+    xr = _xref(x)
+    Wr = np.array(np.swapaxes(W_init, -1, -2), dtype=np.complex128, order="C", copy=True)
+    Lr = np.zeros((F, M, M))
+    Hr = np.zeros((F, T, M))
+    nll = np.zeros(iters + 1)
+    _call(lib().oracle_ica_fit, F, M, M, T, _p(xr), _p(Wr), _p(Lr), _p(Hr), int(iters),
+          int(record_trace), int(seed), int(workers), _p(nll))
+    return (np.swapaxes(Wr, -1, -2), np.swapaxes(Lr, -1, -2), np.swapaxes(Hr, -1, -2), nll)
+
+
+def decorrelated_powers(x, W, floor_rel=1e-12):
+    """|W^H x|^2 per bin (sigmodel.cpp:93-107), floored as floor_positive
+    (sigmodel.cpp:10-15) unless floor_rel is None.  Returns [F,M,T]."""
+    F, M, T = x.shape
+    xr = _xref(x)
+    Wr = np.array(np.swapaxes(W, -1, -2), dtype=np.complex128, order="C", copy=True)
+    out = np.zeros((F, T, M))
+    _call(lib().oracle_decorrelated_powers, F, M, T, _p(xr), _p(Wr),
+          -1.0 if floor_rel is None else float(floor_rel), _p(out))
+    return np.swapaxes(out, -1, -2)
 
 
 def nll_bins(x, W, L, H) -> np.ndarray:

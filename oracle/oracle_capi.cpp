@@ -127,6 +127,45 @@ int oracle_fit(int batch, int bins, int dim, int sources, int frames, const doub
   });
 }
 
+// ica_mode_fit (fastfca.cpp:241-264) on one mixture: W in = w_init, out = the
+// fitted W; L out [bins][dim*dim]; H out [bins][dim*frames].
+int oracle_ica_fit(int bins, int dim, int sources, int frames, const double* x, double* W,
+                   double* L, double* H, int iters, int record_trace, uint64_t seed, int workers,
+                   double* nll, char* err, int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet covs = sample_covs(dim, bins, frames, cx(x));
+    std::vector<CMat> w_init(bins, CMat(dim, dim));
+    for (int i = 0; i < bins; ++i)
+      std::memcpy(static_cast<void*>(w_init[i].data()), W + size_t(i) * dim * dim * 2,
+                  sizeof(Complex) * dim * dim);
+    FitOptions fo;
+    fo.workers = workers;
+    fo.record_trace = record_trace != 0;
+    fo.seed = seed;
+    const FastFcaFitResult r = ica_mode_fit(covs, sources, iters, w_init, fo);
+    store_params(r.params, W, L, H);
+    if (record_trace && nll)
+      for (int t = 0; t <= iters; ++t) nll[t] = r.nll[t];
+  });
+}
+
+// decorrelated_powers + floor_positive per bin (sigmodel.cpp:10-15, 93-107):
+// out [bins][dim*frames] (Eigen col-major dim x frames).
+int oracle_decorrelated_powers(int bins, int dim, int frames, const double* x, const double* W,
+                               double floor_rel, double* out, char* err, int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet covs = sample_covs(dim, bins, frames, cx(x));
+    for (int i = 0; i < bins; ++i) {
+      CMat w(dim, dim);
+      std::memcpy(static_cast<void*>(w.data()), W + size_t(i) * dim * dim * 2,
+                  sizeof(Complex) * dim * dim);
+      RMat u = decorrelated_powers(covs, i, w);
+      if (floor_rel >= 0.0) floor_positive(u, floor_rel);
+      std::memcpy(out + size_t(i) * dim * frames, u.data(), sizeof(double) * dim * frames);
+    }
+  });
+}
+
 // fastfca_nll_freq per bin (sigmodel.cpp:155-162): out[bins].
 int oracle_nll_bins(int bins, int dim, int sources, int frames, const double* x, const double* W,
                     const double* L, const double* H, double* out, char* err, int errlen) {

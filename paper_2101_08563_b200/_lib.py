@@ -26,7 +26,7 @@ EXPORTS = (
     "ffca_version", "ffca_last_error", "ffca_device_count", "ffca_ctx_create",
     "ffca_ctx_destroy", "ffca_fit", "ffca_separate", "ffca_nll_bins", "ffca_power_scale",
     "ffca_fit_device", "ffca_separate_device", "ffca_power_scale_device",
-    "ffca_last_launch_count", "ffca_debug_set_timing",
+    "ffca_last_launch_count", "ffca_debug_set_timing", "ffca_ica_fit", "ffca_decorrelated_powers",
 )
 
 
@@ -80,6 +80,8 @@ def lib() -> C.CDLL:
         L.ffca_separate.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P, P, P]
         L.ffca_nll_bins.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P, P, P]
         L.ffca_power_scale.argtypes = [P, C.POINTER(Dims), P, P]
+        L.ffca_ica_fit.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
+        L.ffca_decorrelated_powers.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, C.c_double, P]
         L.ffca_fit_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
         L.ffca_separate_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -193,6 +193,55 @@ def fastfca_fit(covs: SampleCovSet, init: FastFcaParams, flavor: int, iters: int
                             status)
 
 
+def ica_mode_fit(covs: SampleCovSet, sources: int, iters: int, w_init: np.ndarray,
+                 fit: FitOptions | None = None, *, precision: str = "fp32",
+                 device: int | None = None) -> FastFcaFitResult:
+    """fastfca.cpp:241-264 on the GPU: determined ICA mode (L = identity, H =
+    floored decorrelated powers of w_init, IP+MM with the loadings fixed)."""
+    fit = fit or FitOptions()
+    if sources != covs.dim:
+        raise InvalidArgument("ica_mode_fit: requires as many sources as channels")
+    w_init = np.asarray(w_init)
+    if w_init.shape[0] != covs.bins:
+        raise InvalidArgument("ica_mode_fit: one W per frequency required")
+    if iters < 0:
+        raise InvalidArgument("fastfca_fit: negative iteration count")
+    F, M, T = covs.bins, covs.dim, covs.frames
+    x = _x_ref(covs.snapshots)
+    W = np.array(np.swapaxes(w_init, -1, -2), dtype=np.complex128, order="C", copy=True)
+    L = np.zeros((F, M, M))
+    H = np.zeros((F, T, M))
+    d = _lib.Dims(1, F, M, M, T)
+    o = _lib.FitOpts(_lib.FLAVOR_MM, int(iters), int(bool(fit.record_trace)), int(fit.seed), 1, 1,
+                     _prec(precision))
+    nll = np.zeros(iters + 1) if fit.record_trace else None
+    status = np.zeros(F, np.int32)
+    power = np.ascontiguousarray(covs.power_scale, dtype=np.float64)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_ica_fit(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power),
+                                       _lib.ptr(W), _lib.ptr(L), _lib.ptr(H), _lib.ptr(nll), None,
+                                       _lib.ptr(status)))
+    return FastFcaFitResult(_params_from_ref(W, L, H), list(nll) if nll is not None else [],
+                            status)
+
+
+def decorrelated_powers(covs: SampleCovSet, w: np.ndarray, *, floor_rel: float | None = None,
+                        precision: str = "fp64", device: int | None = None) -> np.ndarray:
+    """|W^H x|^2 for every bin (sigmodel.cpp:93-107), w [bins, dim, dim];
+    floor_positive(u, floor_rel) (sigmodel.cpp:10-15) when floor_rel is given.
+    Returns [bins, dim, frames]."""
+    F, M, T = covs.bins, covs.dim, covs.frames
+    x = _x_ref(covs.snapshots)
+    W = np.array(np.swapaxes(w, -1, -2), dtype=np.complex128, order="C", copy=True)
+    out = np.empty((F, T, M))
+    d = _lib.Dims(1, F, M, M, T)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_decorrelated_powers(
+        ctx.handle, d, _prec(precision), _lib.ptr(x), _lib.ptr(W),
+        -1.0 if floor_rel is None else float(floor_rel), _lib.ptr(out)))
+    return np.ascontiguousarray(np.swapaxes(out, -1, -2))
+
+
 def fastfca_separate(spec: Spectrogram, params: FastFcaParams, *, precision: str = "fp32",
                      device: int | None = None) -> list[Spectrogram]:
     """fastfca.cpp:205-223: decorrelate, per-channel Wiener gains, project back."""

@@ -49,6 +49,54 @@ __global__ void power_kernel(const C* __restrict__ x, double* __restrict__ out, 
   }
 }
 
+// decorrelated_powers (sigmodel.cpp:93-107, snapshot branch :96) followed by
+// floor_positive (sigmodel.cpp:10-15) when floor_rel >= 0: U(m, t) =
+// |w_m^H x_t|^2, then U = max(U, rel * mean(U)) (1e-300 if the mean is not
+// positive).  One CTA per problem; out is [p][t][m] fp64 (the Eigen
+// col-major M x T matrix of each bin).  ica_mode_fit's H init.
+template <typename R>
+__global__ void __launch_bounds__(256) decorrelated_powers_kernel(
+    const cplx_t<R>* __restrict__ x, const double2* __restrict__ W, int M, int T, double floor_rel,
+    double* __restrict__ out) {
+  using C = cplx_t<R>;
+  __shared__ C w[64];
+  __shared__ double red[32];
+  __shared__ double fl;
+  const int p = blockIdx.x;
+  for (int k = threadIdx.x; k < M * M; k += blockDim.x) {
+    const double2 v = W[size_t(p) * M * M + k];
+    w[k] = mkc<R>(R(v.x), R(v.y));
+  }
+  __syncthreads();
+  const C* xp = x + size_t(p) * T * M;
+  double* op = out + size_t(p) * T * M;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    C xv[8];
+    for (int c = 0; c < M; ++c) xv[c] = xp[size_t(t) * M + c];
+    for (int m = 0; m < M; ++m) {
+      C y = cmulc(w[m * M], xv[0]);  // conj(W(0, m)) x_0 + ...
+      for (int c = 1; c < M; ++c) y = cadd(y, cmulc(w[c + m * M], xv[c]));
+      const double u = double(cabs2(y));
+      op[size_t(t) * M + m] = u;
+      s += u;
+    }
+  }
+  if (floor_rel < 0.0) return;
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int k = 0; k < int(blockDim.x >> 5); ++k) tot += red[k];
+    const double mean = tot / (double(T) * M);
+    fl = mean > 0.0 ? floor_rel * mean : 1e-300;
+  }
+  __syncthreads();
+  const double f = fl;
+  for (int k = threadIdx.x; k < T * M; k += blockDim.x) op[k] = fmax(op[k], f);
+}
+
 // ------------------------------------------------------------ separation --
 // fastfca_separate (fastfca.cpp:205-223): y = W^H x; per source
 // g_n = L_n H_n / floor_positive(L H) (source_gain :74-78, sigmodel.cpp:10-15,

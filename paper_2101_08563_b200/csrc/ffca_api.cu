@@ -134,17 +134,20 @@ int stage_inputs(ffca_ctx* ctx, size_t P, int M, int N, int T, const double* x, 
   return FFCA_OK;
 }
 
+// ica: ica_mode_fit (fastfca.cpp:241-264) -- H and L are outputs: L is the
+// identity, H the floored decorrelated powers of the W init, computed here
+// on the device; the fit then runs IP+MM with the loadings fixed.
 template <typename R>
 int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
              const double* power, double* W, double* L, double* H, double* nll,
-             double* nll_slots, int32_t* bin_status) {
+             double* nll_slots, int32_t* bin_status, bool ica = false) {
   const int P = d->batch * d->bins, M = d->dim, N = d->sources, T = d->frames;
   cudaStream_t st = ctx->stream;
   cudaError_t err;
   void* xs = nullptr;
   void* hs = nullptr;
   double* hd = nullptr;
-  int rc = stage_inputs<R>(ctx, P, M, N, T, x, H, &xs, &hs, &hd, st);
+  int rc = stage_inputs<R>(ctx, P, M, N, T, x, ica ? nullptr : H, &xs, &hs, &hd, st);
   if (rc) return rc;
   double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
   double* dL = static_cast<double*>(ctx->get(kL, size_t(P) * M * N * 8, &err));
@@ -155,6 +158,23 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   int* dstat = static_cast<int*>(ctx->get(kStat, size_t(P) * 4, &err));
   if (!dW || !dL || !dpow || !dnll || !dstat) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
   FFCA_CUDA(cudaMemcpyAsync(dW, W, size_t(P) * M * M * 16, cudaMemcpyHostToDevice, st));
+  if (ica) {
+    // L = identity (fastfca.cpp:257); a constant, written on the host.
+    for (int p = 0; p < P; ++p)
+      for (int k = 0; k < M * N; ++k) L[size_t(p) * M * N + k] = (k % M == k / M) ? 1.0 : 0.0;
+    const size_t nh = size_t(P) * T * N;
+    hd = static_cast<double*>(ctx->get(kH, nh * 8, &err));
+    hs = ctx->get(kHs, nh * sizeof(R), &err);
+    if (!hd || !hs) return set_err(FFCA_CUDA_ERROR, "ffca: H alloc failed");
+    decorrelated_powers_kernel<R><<<P, 256, 0, st>>>(static_cast<const cplx_t<R>*>(xs),
+                                                      reinterpret_cast<const double2*>(dW), M, T,
+                                                      1e-12 /* kPowerFloorRel */, hd);
+    ctx->launches++;
+    FFCA_CUDA(cudaGetLastError());
+    convert_kernel<double, R><<<grid_for(nh, 256), 256, 0, st>>>(hd, static_cast<R*>(hs), nh);
+    ctx->launches++;
+    FFCA_CUDA(cudaGetLastError());
+  }
   FFCA_CUDA(cudaMemcpyAsync(dL, L, size_t(P) * M * N * 8, cudaMemcpyHostToDevice, st));
   if (power) {
     FFCA_CUDA(cudaMemcpyAsync(dpow, power, size_t(P) * 8, cudaMemcpyHostToDevice, st));
@@ -206,6 +226,10 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
     if (s == kStatusSingularW) return set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
   }
   if (bin_status) std::memcpy(bin_status, stat.data(), size_t(P) * 4);
+  if (ica && iters == 0) {
+    FFCA_CUDA(cudaMemcpyAsync(H, hd, size_t(P) * T * N * 8, cudaMemcpyDeviceToHost, st));
+    FFCA_CUDA(cudaStreamSynchronize(st));
+  }
   if (iters > 0) {
     const size_t nh = size_t(P) * T * N;
     unpack_h_kernel<R><<<grid_for(nh, 256), 256, 0, st>>>(static_cast<const R*>(hs), hd, dstat,
@@ -303,6 +327,71 @@ int ffca_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   if (o->precision == FFCA_PREC_FP64)
     return fit_host<double>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status);
   return fit_host<float>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status);
+}
+
+int ffca_ica_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
+                 const double* power, double* W, double* L, double* H, double* nll,
+                 double* nll_slots, int32_t* bin_status) {
+  if (!ctx || !d || !o) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: null argument");
+  if (d->batch < 1 || d->bins < 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: empty shape");
+  if (d->sources != d->dim)  // fastfca.cpp:244-246
+    return set_err(FFCA_INVALID_ARGUMENT, "ica_mode_fit: requires as many sources as channels");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
+  if (rc) return rc;
+  if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
+  if (!x || !W || !L || !H) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: null buffer");
+  if (o->record_trace && !nll && !nll_slots)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: record_trace needs an nll buffer");
+  ctx->launches = 0;
+  DeviceGuard g(ctx->device);
+  ffca_fit_opts m = *o;
+  m.flavor = FFCA_FLAVOR_MM;  // fastfca.cpp:262-263
+  m.fix_loadings = 1;
+  m.normalize_scales = 1;
+  // Always the fp64 kernels: at the determined-mode fixed point H tracks
+  // U = |w^H x|^2 and the 1/U weights amplify fp32 cancellation in w^H x
+  // (measured: the fp32 trajectory leaves the fp64 one by 5e-4 after 20
+  // iterations and the IP system then goes singular where the reference
+  // converges), so `precision` does not apply to this mode.
+  return fit_host<double>(ctx, d, &m, x, power, W, L, H, nll, nll_slots, bin_status, true);
+}
+
+int ffca_decorrelated_powers(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,
+                             const double* W, double floor_rel, double* out) {
+  if (!ctx || !d || !x || !W || !out)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_decorrelated_powers: null argument");
+  if (d->batch < 1 || d->bins < 1)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_decorrelated_powers: empty shape");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->dim, d->frames);
+  if (rc) return rc;
+  ctx->launches = 0;
+  DeviceGuard g(ctx->device);
+  const int P = d->batch * d->bins, M = d->dim, T = d->frames;
+  cudaStream_t st = ctx->stream;
+  cudaError_t err;
+  void* xs = nullptr;
+  void* hs = nullptr;
+  double* hd = nullptr;
+  double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
+  double* dout = static_cast<double*>(ctx->get(kH, size_t(P) * T * M * 8, &err));
+  if (!dW || !dout) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dW, W, size_t(P) * M * M * 16, cudaMemcpyHostToDevice, st));
+  if (precision == FFCA_PREC_FP64) {
+    rc = stage_inputs<double>(ctx, P, M, M, T, x, nullptr, &xs, &hs, &hd, st);
+    if (rc) return rc;
+    decorrelated_powers_kernel<double><<<P, 256, 0, st>>>(
+        static_cast<const double2*>(xs), reinterpret_cast<const double2*>(dW), M, T, floor_rel, dout);
+  } else {
+    rc = stage_inputs<float>(ctx, P, M, M, T, x, nullptr, &xs, &hs, &hd, st);
+    if (rc) return rc;
+    decorrelated_powers_kernel<float><<<P, 256, 0, st>>>(
+        static_cast<const float2*>(xs), reinterpret_cast<const double2*>(dW), M, T, floor_rel, dout);
+  }
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  FFCA_CUDA(cudaMemcpyAsync(out, dout, size_t(P) * T * M * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  return FFCA_OK;
 }
 
 int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,

@@ -357,8 +357,8 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   }
   for (int k = tid; k < M * N; k += nthreads) {
     const double l = p.L[size_t(b) * M * N + k];
-    Ld[k] = B(l);
-    Le[k] = R(l);
+    Ld[k] = narrow_pos<B>(l);
+    Le[k] = narrow_pos<R>(l);
   }
   for (int k = tid; k < NT; k += nthreads) hsc[k] = B(1), hinv[k] = B(1);
   for (int k = tid; k < M; k += nthreads) us[k] = B(1);
@@ -921,9 +921,15 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     __syncwarp();
     for (int k = lane; k < M * N; k += 32) {
       const int m = k % M, n = k / M;
-      const B l = fmax(Ld[k] * hinvn[n] * us[m], tinyB);  // L(m,n) mu_n / s_m
+      // L(m,n) mu_n / s_m; exact zeros stay zero (ica_mode_fit's one-hot
+      // loadings), a positive value that underflows the compute type
+      // becomes its smallest normal.
+      const B l0 = Ld[k];
+      B l = l0 * hinvn[n] * us[m];
+      l = (l0 > B(0) && !(l > B(0))) ? tinyB : l;
       Ldn[k] = l;
-      Le[k] = R(fmax(l * hscn[n], tinyB));
+      const B le = l * hscn[n];
+      Le[k] = R((l > B(0) && !(le > B(0))) ? tinyB : le);
     }
     __syncwarp();  // converged before the shuffles
     // sum_m log s_m over the lowest Pow2Ceil(M) lanes (fixed order).

@@ -188,11 +188,6 @@ static __device__ __noinline__ void ip_perturb(double2* wcol, int m, RestartRng*
   }
 }
 
-// M = 2 IP sweep in closed form on the Hermitian structure of Q (real
-// diagonal, Q(1,0) = conj Q(0,1)): A = W^H Q_k, w = A^{-1} e_k from the 2x2
-// adjugate, the residual test, w /= sqrt(w^H Q_k w) -- the same steps as the
-// general path below with the zero imaginary parts and the symmetric half
-// folded away, so the per-column dependency chain is ~15 FP ops + 2 MUFU.
 // Optional side jobs of an IP sweep, folded in to keep them off the serial
 // path: wscale -- balance column scales still to be applied to W first;
 // wout -- compute-type copy of the new W; ldet/ldok -- log|det W_new|^2
@@ -252,6 +247,40 @@ __device__ __forceinline__ bool ip_col_m2(const cplx_t<SR> (&wr)[4], int col, SR
   return fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en);
 }
 
+// The reference's M = 2 sweep in fp64, column by column with the seeded
+// restart (fastfca.cpp:36-72): the cold fallback of ip_update_m2.
+static __device__ __noinline__ bool ip_m2_careful(double2* w, const double* qraw, double invT,
+                                                  unsigned long long seed, int bin,
+                                                  RestartRng* rr, int& bad_col) {
+  double2 wr[4];
+  for (int k = 0; k < 4; ++k) wr[k] = w[k];
+  bool restarted = false;
+  for (int col = 0; col < 2; ++col) {
+    const double* p = qraw + 4 * col;
+    const double q00 = p[0] * invT, q11 = p[3] * invT;
+    const double2 q01 = make_double2(p[1] * invT, p[2] * invT);
+    for (int attempt = 0;; ++attempt) {
+      double2 o[2];
+      if (ip_col_m2<double>(wr, col, q00, q11, q01, o)) {
+        wr[2 * col] = o[0];
+        wr[2 * col + 1] = o[1];
+        w[2 * col] = o[0];
+        w[2 * col + 1] = o[1];
+        break;
+      }
+      if (attempt >= 1) {
+        bad_col = col;
+        return false;
+      }
+      ip_perturb(w + 2 * col, 2, rr, !restarted, seed, bin);
+      restarted = true;
+      wr[2 * col] = w[2 * col];
+      wr[2 * col + 1] = w[2 * col + 1];
+    }
+  }
+  return true;
+}
+
 // M = 2 IP sweep in closed form on the Hermitian structure of Q (real
 // diagonal, Q(1,0) = conj Q(0,1)): A = W^H Q_k, w = A^{-1} e_k from the 2x2
 // adjugate, the residual test, w /= sqrt(w^H Q_k w) -- the same steps as the
@@ -308,39 +337,22 @@ __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, dou
       return true;
     }
   }
-  // Careful path: the reference's column-by-column sweep with restarts, from
-  // the (scaled) master.
+  // Careful path, in fp64 whatever SR is: the reference's arithmetic and
+  // 1e-8 residual test, column by column with the seeded restart, from the
+  // (scaled) master.  In the fp32 path this catches ill-conditioned systems
+  // (e.g. ICA mode, where H converges onto U) that fp32 cannot resolve to
+  // the fp32 tolerance but the reference's fp64 solve accepts.
   if (ex.wscale) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const double c = double(ex.wscale[k >> 1]);
       w[k].x *= c;
       w[k].y *= c;
-      wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
     }
   }
-  bool restarted = false;
+  if (!ip_m2_careful(w, qraw, invT, seed, bin, rr, bad_col)) return false;
 #pragma unroll
-  for (int col = 0; col < 2; ++col) {
-    for (int attempt = 0;; ++attempt) {
-      SC o[2];
-      if (ip_col_m2<SR>(wr, col, qd0[col], qd1[col], qo[col], o)) {
-        wr[2 * col] = o[0];
-        wr[2 * col + 1] = o[1];
-        w[2 * col] = make_double2(double(o[0].x), double(o[0].y));
-        w[2 * col + 1] = make_double2(double(o[1].x), double(o[1].y));
-        break;
-      }
-      if (attempt >= 1) {
-        bad_col = col;
-        return false;
-      }
-      ip_perturb(w + 2 * col, 2, rr, !restarted, seed, bin);
-      restarted = true;
-      wr[2 * col] = mkc<SR>(SR(w[2 * col].x), SR(w[2 * col].y));
-      wr[2 * col + 1] = mkc<SR>(SR(w[2 * col + 1].x), SR(w[2 * col + 1].y));
-    }
-  }
+  for (int k = 0; k < 4; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
   finish(wr);
   return true;
 }
@@ -349,14 +361,16 @@ __device__ __forceinline__ bool ip_update_m2(double2* w, const double* qraw, dou
 // qraw[m*M*M + ...] holds sum_t x x^H / sigma2_m packed as: (a,a) real,
 // (a,b) a<b real part at a*M+b and imaginary part at b*M+a.  w is the fp64
 // master W (updated in place).
-template <int M, typename SR>
-__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
-                                          unsigned long long seed, int bin, RestartRng* rr,
-                                          int& bad_col, IpExtras<SR> ex = IpExtras<SR>()) {
-  if constexpr (M == 2) return ip_update_m2<SR>(w, qraw, invT, seed, bin, rr, bad_col, ex);
+// SPEC: speculative pass -- registers only, no restart; returns false on the
+// first failed acceptance test without touching w (the caller then reruns
+// the sweep the reference's way).
+template <int M, typename SR, bool SPEC>
+__device__ __forceinline__ bool ip_update_gen(double2* w, const double* qraw, double invT,
+                                              unsigned long long seed, int bin, RestartRng* rr,
+                                              int& bad_col, IpExtras<SR> ex) {
   using SC = cplx_t<SR>;
   bool restarted = false;
-  if (ex.wscale)
+  if (!SPEC && ex.wscale)
     for (int k = 0; k < M * M; ++k) {
       const double c = double(ex.wscale[k / M]);
       w[k].x *= c;
@@ -364,7 +378,10 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
     }
   SC wr[M * M];
 #pragma unroll
-  for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+  for (int k = 0; k < M * M; ++k) {
+    wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+    if (SPEC && ex.wscale) wr[k].x *= ex.wscale[k / M], wr[k].y *= ex.wscale[k / M];
+  }
   // Unrolled for M <= 3: every register-array index is a compile-time
   // constant (a rolled column loop indexes wr[] dynamically and demotes it to
   // local memory); M = 4 keeps the rolled loop (the unrolled body spills).
@@ -449,11 +466,13 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
 #pragma unroll
           for (int r = 0; r < M; ++r) {
             wr[r + col * M] = mkc<SR>(wm[r].x * s, wm[r].y * s);
-            w[r + col * M] = make_double2(double(wr[r + col * M].x), double(wr[r + col * M].y));
+            if (!SPEC)
+              w[r + col * M] = make_double2(double(wr[r + col * M].x), double(wr[r + col * M].y));
           }
           break;
         }
       }
+      if (SPEC) return false;
       if (attempt >= 1) {
         bad_col = col;
         return false;
@@ -464,10 +483,48 @@ __device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double
       for (int k = 0; k < M * M; ++k) wr[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
     }
   }
+  if (SPEC)
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) w[k] = make_double2(double(wr[k].x), double(wr[k].y));
   if (ex.wout)
 #pragma unroll
     for (int k = 0; k < M * M; ++k) ex.wout[k] = wr[k];
   return true;
+}
+
+// The reference's sweep in fp64 (cold fallback of the fp32 path).
+template <int M>
+__device__ __noinline__ bool ip_update_f64(double2* w, const double* qraw, double invT,
+                                           unsigned long long seed, int bin, RestartRng* rr,
+                                           int& bad_col) {
+  return ip_update_gen<M, double, false>(w, qraw, invT, seed, bin, rr, bad_col,
+                                         IpExtras<double>());
+}
+
+// ip_update_w (fastfca.cpp:36-72).  fp32 path: a speculative fp32 sweep; if
+// any column fails its acceptance test, the sweep is redone from the master W
+// in fp64 with the reference's 1e-8 residual test and seeded restart.
+template <int M, typename SR>
+__device__ __forceinline__ bool ip_update(double2* w, const double* qraw, double invT,
+                                          unsigned long long seed, int bin, RestartRng* rr,
+                                          int& bad_col, IpExtras<SR> ex = IpExtras<SR>()) {
+  if constexpr (M == 2) {
+    return ip_update_m2<SR>(w, qraw, invT, seed, bin, rr, bad_col, ex);
+  } else if constexpr (sizeof(SR) == 4) {
+    if (ip_update_gen<M, SR, true>(w, qraw, invT, seed, bin, rr, bad_col, ex)) return true;
+    if (ex.wscale)
+      for (int k = 0; k < M * M; ++k) {
+        const double c = double(ex.wscale[k / M]);
+        w[k].x *= c;
+        w[k].y *= c;
+      }
+    if (!ip_update_f64<M>(w, qraw, invT, seed, bin, rr, bad_col)) return false;
+    if (ex.wout)
+      for (int k = 0; k < M * M; ++k) ex.wout[k] = mkc<SR>(SR(w[k].x), SR(w[k].y));
+    return true;
+  } else {
+    return ip_update_gen<M, SR, false>(w, qraw, invT, seed, bin, rr, bad_col, ex);
+  }
 }
 
 // ------------------------------------------------ warp-cooperative (M > 4) --

@@ -199,7 +199,76 @@ double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RM
   return fastfca_nll(c1, one);
 }
 
+RMat decorrelated_powers(const SampleCovSet& covs, int i, const CMat& w) {
+  if (i < 0 || i >= covs.bins || int(covs.snapshots.size()) != covs.bins)
+    throw std::invalid_argument("decorrelated_powers: bin out of range or no snapshots");
+  if (w.rows() != covs.dim || w.cols() != covs.dim)
+    throw std::invalid_argument("decorrelated_powers: W shape mismatch");
+  const int M = covs.dim, T = covs.blocks;
+  ffca_dims d{1, 1, M, M, T, 0, 0};
+  RMat u(M, T);
+  raise(ffca_decorrelated_powers(context(0), &d, FFCA_PREC_FP64,
+                                 reinterpret_cast<const double*>(covs.snapshots[i].data()),
+                                 reinterpret_cast<const double*>(w.data()), -1.0, u.data()));
+  return u;
+}
+
 // ---------------------------------------------------------------- fastfca --
+
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit) {
+  return ica_mode_fit(covs, sources, iters, w_init, fit, GpuOptions{});
+}
+
+FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
+                              const std::vector<CMat>& w_init, const FitOptions& fit,
+                              const GpuOptions& gpu) {
+  // fastfca.cpp:244-249
+  if (sources != covs.dim)
+    throw std::invalid_argument("ica_mode_fit: requires as many sources as channels");
+  if (static_cast<int>(w_init.size()) != covs.bins)
+    throw std::invalid_argument("ica_mode_fit: one W per frequency required");
+  if (!covs.has_snapshots() || int(covs.snapshots.size()) != covs.bins ||
+      covs.power_scale.size() != covs.bins)
+    throw std::invalid_argument("ica_mode_fit: covariance set has no snapshots (block_size > 1)");
+  if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
+  const int F = covs.bins, M = covs.dim, T = covs.blocks;
+  for (const CMat& w : w_init)
+    if (w.rows() != M || w.cols() != M) throw std::invalid_argument("ica_mode_fit: W shape mismatch");
+  FastFcaFitResult result;
+  FastFcaParams& p = result.params;
+  p.dim = M;
+  p.bins = F;
+  p.frames = T;
+  p.sources = sources;
+  p.decorr = w_init;
+  p.loading.assign(F, RMat::Zero(M, sources));
+  p.act.assign(F, RMat::Zero(sources, T));
+  ffca_fit_opts o = fit_opts(LhFlavor::mm, iters, fit, FastFcaOptions{}, gpu);
+  std::vector<double> slots(fit.record_trace ? size_t(iters + 1) * F : 0);
+  over_devices(gpu.devices, F, [&](int dev, int lo, int hi) {
+    Packed pk;
+    pack_bins(covs, p, lo, hi, pk);  // x, power, W init (L, H are outputs)
+    const int n = hi - lo;
+    std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
+    ffca_dims d{1, n, M, sources, T, lo, F};
+    raise(ffca_ica_fit(context(dev), &d, &o, pk.x.data(), pk.power.data(), pk.W.data(),
+                       pk.L.data(), pk.H.data(), nullptr, fit.record_trace ? sl.data() : nullptr,
+                       nullptr));
+    unpack_bins(pk, lo, hi, p);
+    for (int t = 0; fit.record_trace && t <= iters; ++t)
+      for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
+  });
+  if (fit.record_trace) {  // fastfca.cpp:186-189, bin order
+    result.nll.assign(iters + 1, 0.0);
+    for (int t = 0; t <= iters; ++t) {
+      double s = 0.0;
+      for (int i = 0; i < F; ++i) s += slots[size_t(t) * F + i];
+      result.nll[t] = s;
+    }
+  }
+  return result;
+}
 
 FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
                              int iters, const FitOptions& fit, const FastFcaOptions& opts) {
