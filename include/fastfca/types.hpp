@@ -35,6 +35,7 @@ class Dense {
  public:
   Dense() = default;
   Dense(long rows, long cols) : r_(rows), c_(cols), a_(size_t(rows * cols), T(0)) {}
+  explicit Dense(long n) : Dense(n, 1) {}  // column vector (Eigen::VectorX*(n))
   static Dense Zero(long rows, long cols) { return Dense(rows, cols); }
   static Dense Zero(long n) { return Dense(n, 1); }
   static Dense Ones(long rows, long cols) {

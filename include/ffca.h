@@ -41,6 +41,9 @@ extern "C" {
 #define FFCA_PREC_FP32 0 /* complex64 / fp32 data path, fp64 reductions and solves */
 #define FFCA_PREC_FP64 1 /* fp64 check mode */
 
+#define FFCA_STFT_CENTERED 0    /* StftPadding::centered (stft.hpp:30-37) */
+#define FFCA_STFT_FULL_FRAMES 1 /* StftPadding::full_frames */
+
 /* Per-bin status words written by the fit. */
 #define FFCA_BIN_OK 0
 #define FFCA_BIN_SILENT 1       /* power(i) <= 0: init kept (fastfca.cpp:165-170) */
@@ -150,6 +153,34 @@ int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int 
 /* power_scale from device x (complex64/complex128, [P][frames][dim]): out [P]. */
 int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, int precision,
                             const void* x_dev, double* out, void* stream);
+
+/* ---- STFT front end / iSTFT back end (stft.hpp:40-56, stft.cpp:12-128) ----
+ * sqrt-Hann window, 50 % overlap (shift == frame_len / 2, frame_len a power
+ * of two <= 4096), fp64 FFTs on the GPU.  Layouts are the reference's:
+ * samples [length][channels] (MultichannelWave::samples, Eigen col-major
+ * channels x length); spec [bins][frames][channels] (Spectrogram::f[b]) with
+ * bins = frame_len/2 + 1 -- which is also the fit's x layout [P][T][M], so
+ * ffca_stft_device output feeds ffca_fit_device directly. */
+
+/* stft_frame_count (stft.cpp:41-49); -1 (and ffca_last_error) on error. */
+long long ffca_stft_frame_count(long long length, int frame_len, int shift, int padding);
+
+/* stft (stft.cpp:51-83): spec [bins][frames][channels] complex128. */
+int ffca_stft(ffca_ctx* ctx, int channels, long long length, int frame_len, int shift, int padding,
+              const double* samples, double* spec);
+
+/* istft (stft.cpp:85-128): samples [out_len][channels]. */
+int ffca_istft(ffca_ctx* ctx, int channels, int bins, int frames, int frame_len, int shift,
+               int padding, long long out_len, const double* spec, double* samples);
+
+/* Device-resident variants: samples fp32/fp64 and spec complex64/complex128
+ * by `precision` (the FFTs themselves run in fp64); asynchronous on stream. */
+int ffca_stft_device(ffca_ctx* ctx, int channels, long long length, int frame_len, int shift,
+                     int padding, int precision, const void* samples_dev, void* x_dev,
+                     void* stream);
+int ffca_istft_device(ffca_ctx* ctx, int channels, int frames, int frame_len, int shift,
+                      int padding, long long out_len, int precision, const void* spec_dev,
+                      void* samples_dev, void* stream);
 
 /* Number of kernels the last call on this context launched (bench evidence). */
 int ffca_last_launch_count(const ffca_ctx* ctx);

@@ -27,7 +27,9 @@ EXPORTS = (
     "ffca_ctx_destroy", "ffca_fit", "ffca_separate", "ffca_nll_bins", "ffca_power_scale",
     "ffca_fit_device", "ffca_separate_device", "ffca_power_scale_device",
     "ffca_last_launch_count", "ffca_debug_set_timing", "ffca_ica_fit", "ffca_decorrelated_powers",
+    "ffca_stft_frame_count", "ffca_stft", "ffca_istft", "ffca_stft_device", "ffca_istft_device",
 )
+STFT_CENTERED, STFT_FULL_FRAMES = 0, 1
 
 
 class FfcaError(RuntimeError):
@@ -82,6 +84,13 @@ def lib() -> C.CDLL:
         L.ffca_power_scale.argtypes = [P, C.POINTER(Dims), P, P]
         L.ffca_ica_fit.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
         L.ffca_decorrelated_powers.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, C.c_double, P]
+        i, ll = C.c_int, C.c_longlong
+        L.ffca_stft_frame_count.argtypes = [ll, i, i, i]
+        L.ffca_stft_frame_count.restype = ll
+        L.ffca_stft.argtypes = [P, i, ll, i, i, i, P, P]
+        L.ffca_istft.argtypes = [P, i, i, i, i, i, i, ll, P, P]
+        L.ffca_stft_device.argtypes = [P, i, ll, i, i, i, i, P, P, P]
+        L.ffca_istft_device.argtypes = [P, i, i, i, i, i, ll, i, P, P, P]
         L.ffca_fit_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
         L.ffca_separate_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -57,6 +57,25 @@ class Spectrogram:  # stft.hpp:21-29; f[i] is channels x frames
 
 
 @dataclass
+class MultichannelWave:  # stft.hpp:12-17
+    samples: np.ndarray  # float [channels, length]
+    sample_rate: float = 0.0
+
+    @property
+    def channels(self) -> int:
+        return self.samples.shape[0]
+
+    @property
+    def length(self) -> int:
+        return self.samples.shape[1]
+
+
+class StftPadding:  # stft.hpp:30-37
+    centered = 0
+    full_frames = 1
+
+
+@dataclass
 class SampleCovSet:  # sigmodel.hpp:48-56, block_size == 1 snapshot branch
     snapshots: np.ndarray    # complex [bins, dim, frames]
     power_scale: np.ndarray  # [bins]
@@ -240,6 +259,50 @@ def decorrelated_powers(covs: SampleCovSet, w: np.ndarray, *, floor_rel: float |
         ctx.handle, d, _prec(precision), _lib.ptr(x), _lib.ptr(W),
         -1.0 if floor_rel is None else float(floor_rel), _lib.ptr(out)))
     return np.ascontiguousarray(np.swapaxes(out, -1, -2))
+
+
+# ------------------------------------------------------------------- stft --
+def sqrt_hann_window(frame_len: int) -> np.ndarray:
+    """stft.cpp:33-39 (a constant table)."""
+    k = np.arange(frame_len)
+    return np.sqrt(0.5 - 0.5 * np.cos(2.0 * np.pi * k / frame_len))
+
+
+def stft_frame_count(length: int, frame_len: int, shift: int,
+                     pad: int = StftPadding.centered) -> int:
+    """stft.cpp:41-49."""
+    n = _lib.lib().ffca_stft_frame_count(int(length), int(frame_len), int(shift), int(pad))
+    if n < 0:
+        raise InvalidArgument(_lib.lib().ffca_last_error().decode())
+    return int(n)
+
+
+def stft(wave: MultichannelWave, frame_len: int, shift: int, pad: int = StftPadding.centered,
+         *, device: int | None = None) -> Spectrogram:
+    """stft.cpp:51-83 on the GPU (fp64 FFTs)."""
+    C, n = wave.samples.shape
+    s = np.ascontiguousarray(np.asarray(wave.samples, np.float64).T)  # [length][channels]
+    if frame_len > 0 and not (frame_len & (frame_len - 1)) and shift * 2 == frame_len and n >= frame_len:
+        frames = stft_frame_count(n, frame_len, shift, pad)
+    else:
+        frames = 1  # the library raises the reference's error
+    out = np.empty((frame_len // 2 + 1 if frame_len > 0 else 1, frames, C), np.complex128)
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_stft(ctx.handle, C, n, int(frame_len), int(shift), int(pad),
+                                    _lib.ptr(s), _lib.ptr(out)))
+    return Spectrogram(np.ascontiguousarray(np.swapaxes(out, 1, 2)))
+
+
+def istft(spec: Spectrogram, frame_len: int, shift: int, out_len: int, sample_rate: float,
+          pad: int = StftPadding.centered, *, device: int | None = None) -> MultichannelWave:
+    """stft.cpp:85-128 on the GPU."""
+    x = np.ascontiguousarray(np.swapaxes(spec.f, 1, 2), dtype=np.complex128)  # [bins][frames][C]
+    out = np.zeros((out_len, spec.channels))
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().ffca_istft(ctx.handle, spec.channels, spec.bins, spec.frames,
+                                     int(frame_len), int(shift), int(pad), int(out_len),
+                                     _lib.ptr(x), _lib.ptr(out)))
+    return MultichannelWave(np.ascontiguousarray(out.T), sample_rate)
 
 
 def fastfca_separate(spec: Spectrogram, params: FastFcaParams, *, precision: str = "fp32",

@@ -4,6 +4,7 @@
 // the ABI takes, and one host thread per device for frequency sharding.
 // All arithmetic runs in libffca.so's sm_100a kernels.
 
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -141,6 +142,58 @@ void over_devices(const std::vector<int>& devs, int count, Fn fn) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------- stft --
+
+RVec sqrt_hann_window(int frame_len) {  // stft.cpp:33-39 (a constant table)
+  RVec w(frame_len);
+  for (int k = 0; k < frame_len; ++k) w(k) = std::sqrt(0.5 - 0.5 * std::cos(2.0 * M_PI * k / frame_len));
+  return w;
+}
+
+int stft_frame_count(long length, int frame_len, int shift, StftPadding pad) {
+  const long long n = ffca_stft_frame_count(
+      length, frame_len, shift, pad == StftPadding::centered ? FFCA_STFT_CENTERED : FFCA_STFT_FULL_FRAMES);
+  if (n < 0) throw std::invalid_argument(ffca_last_error());
+  return static_cast<int>(n);
+}
+
+Spectrogram stft(const MultichannelWave& wave, int frame_len, int shift, StftPadding pad) {
+  const int C = wave.channels();
+  const long len = wave.length();
+  const int padding = pad == StftPadding::centered ? FFCA_STFT_CENTERED : FFCA_STFT_FULL_FRAMES;
+  // Validation order and messages follow stft.cpp:52-57.
+  if (frame_len <= 0 || (frame_len & (frame_len - 1)) != 0)
+    throw std::invalid_argument("stft: frame length must be a power of two");
+  if (shift * 2 != frame_len) throw std::invalid_argument("stft: shift must be frame_len/2");
+  if (len < frame_len) throw std::invalid_argument("stft: signal shorter than one frame");
+  const int bins = frame_len / 2 + 1;
+  const int frames = stft_frame_count(len, frame_len, shift, pad);
+  std::vector<double> spec(size_t(bins) * frames * C * 2);
+  raise(ffca_stft(context(0), C, len, frame_len, shift, padding,
+                  reinterpret_cast<const double*>(wave.samples.data()), spec.data()));
+  Spectrogram out = Spectrogram::zero(C, bins, frames);
+  for (int b = 0; b < bins; ++b)
+    std::memcpy(static_cast<void*>(out.f[b].data()), spec.data() + size_t(b) * frames * C * 2,
+                sizeof(double) * frames * C * 2);
+  return out;
+}
+
+MultichannelWave istft(const Spectrogram& spec, int frame_len, int shift, long out_len,
+                       double sample_rate, StftPadding pad) {
+  const int padding = pad == StftPadding::centered ? FFCA_STFT_CENTERED : FFCA_STFT_FULL_FRAMES;
+  const int C = spec.channels;
+  std::vector<double> in(size_t(spec.bins) * spec.frames * C * 2);
+  for (int b = 0; b < spec.bins && b < int(spec.f.size()); ++b)
+    std::memcpy(in.data() + size_t(b) * spec.frames * C * 2, spec.f[b].data(),
+                sizeof(double) * spec.frames * C * 2);
+  MultichannelWave wave;
+  wave.sample_rate = sample_rate;
+  wave.samples = RMat::Zero(C, out_len);
+  raise(ffca_istft(context(0), C, spec.bins, spec.frames, frame_len, shift, padding, out_len,
+                   in.data(), wave.samples.data()));
+  return wave;
+}
 
 // --------------------------------------------------------------- sigmodel --
 

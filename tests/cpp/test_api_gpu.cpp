@@ -267,6 +267,32 @@ int main() {
       for (int k = 0; k < 3; ++k) m = std::max(m, std::abs(u(k, t) - uo(k, t)) / (uo(k, t) + 1e-300));
     CHECK(m <= 1e-12);
   }
+  // ---- stft / istft (stft.cpp:51-128) round trip through the C++ API.
+  {
+    fastfca::MultichannelWave w;
+    w.sample_rate = 16000;
+    w.samples = RMat::Zero(2, 4097);
+    std::mt19937 r2(23);
+    std::uniform_real_distribution<double> d(-0.5, 0.5);
+    for (long t = 0; t < 4097; ++t)
+      for (int ch = 0; ch < 2; ++ch) w.samples(ch, t) = d(r2);
+    const fastfca::Spectrogram s = fastfca::stft(w, 512, 256);
+    CHECK(s.bins == 257 && s.frames == fastfca::stft_frame_count(4097, 512, 256,
+                                                                fastfca::StftPadding::centered));
+    const fastfca::MultichannelWave back = fastfca::istft(s, 512, 256, 4097, 16000);
+    double m = 0.0;
+    for (long t = 0; t < 4097; ++t)
+      for (int ch = 0; ch < 2; ++ch) m = std::max(m, std::abs(back.samples(ch, t) - w.samples(ch, t)));
+    CHECK(m < 1e-10);
+    CHECK(fastfca::stft_frame_count(8 * 16000, 1024, 512, fastfca::StftPadding::full_frames) == 249);
+    bool threw = false;
+    try {
+      fastfca::stft(w, 1000, 500);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
