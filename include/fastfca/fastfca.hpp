@@ -61,6 +61,10 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
                               const std::vector<CMat>& w_init, const FitOptions& fit,
                               const GpuOptions& gpu);
 
+// Block-stationary statistics; block_size == 1 reproduces sample_covs
+// (fastfca.hpp:80-81, fastfca.cpp:266-268).
+SampleCovSet piecewise_prepare(const Spectrogram& spec, int block_size);
+
 // Decomposed multichannel Wiener filter (fastfca.cpp:205-223).
 std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params);
 std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params,

@@ -1,11 +1,13 @@
 // sigmodel.hpp -- observation statistics and parameter containers of the
-// FastFCA C++ API (reference proj/include/fastfca/sigmodel.hpp:19-111), for
-// the block_size == 1 snapshot path the GPU fit runs.
+// FastFCA C++ API (reference proj/include/fastfca/sigmodel.hpp:19-111).
 //
-// Deviation: sample_covs does not materialise the per-(i, j) rank-one
+// block_size == 1 keeps the snapshots the GPU fit reads.  Deviation: for
+// block_size == 1 sample_covs does not materialise the per-(i, j) rank-one
 // matrices `mats` (F*T M x M heap matrices, ~17 GB at BASELINE config 3); the
 // reference's hot path never reads them when snapshots exist
-// (fastfca.cpp:25-28, sigmodel.cpp:95-96).  `mats` stays in the struct, empty.
+// (fastfca.cpp:25-28, sigmodel.cpp:95-96).  block_size B > 1 fills `mats`
+// with the B-frame block covariances (computed on the GPU) and the fit runs
+// the block-stationary kernels on them.
 #pragma once
 
 #include <algorithm>
@@ -30,18 +32,23 @@ struct FitOptions {  // sigmodel.hpp:34-38
   std::uint64_t seed = 0;      // recovery restarts only
 };
 
-struct SampleCovSet {  // sigmodel.hpp:48-56 (block_size == 1)
+struct SampleCovSet {  // sigmodel.hpp:48-56
   int dim = 0, bins = 0, blocks = 0, frames = 0, block_size = 1;
-  std::vector<std::vector<CMat>> mats;  // not materialised (see header note)
-  std::vector<CMat> snapshots;          // [i], dim x frames
+  std::vector<std::vector<CMat>> mats;  // [i][jb], block_size > 1 (see header note)
+  std::vector<CMat> snapshots;          // [i], dim x frames (block_size == 1)
   RVec power_scale;                     // [i], mean per-channel data power
   bool has_snapshots() const { return !snapshots.empty(); }
-  double power(int i) const { return power_scale(i); }
+  double power(int i) const {  // sigmodel.cpp:50-55
+    if (i < long(power_scale.size())) return power_scale(i);
+    double trace_sum = 0.0;
+    for (const CMat& m : mats[i])
+      for (long k = 0; k < m.rows(); ++k) trace_sum += std::real(m(k, k));
+    return trace_sum / (static_cast<double>(blocks) * dim);
+  }
 };
 
-// Snapshots + power_scale (sigmodel.cpp:17-48); the power reduction runs on
-// the GPU.  block_size != 1 throws std::invalid_argument (block-stationary
-// statistics are outside the GPU path).
+// sample_covs (sigmodel.cpp:17-48) on the GPU: snapshots + power_scale for
+// block_size == 1; the block covariances `mats` + power_scale for B > 1.
 SampleCovSet sample_covs(const Spectrogram& spec, int block_size = 1);
 
 struct FastFcaParams {  // sigmodel.hpp:72-78
@@ -58,5 +65,9 @@ double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& params);
 RMat decorrelated_powers(const SampleCovSet& covs, int i, const CMat& w);
 double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RMat& loading,
                         const RMat& act);
+
+// Expands block-level parameters to frame level (sigmodel.hpp:96-101,
+// sigmodel.cpp:164-196): column j of H takes block min(j / B, blocks - 1).
+FastFcaParams expand_block_params(const FastFcaParams& params, int block_size, int frames);
 
 }  // namespace fastfca

@@ -112,6 +112,41 @@ int ffca_ica_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts
                  const double* power, double* W, double* L, double* H, double* nll,
                  double* nll_slots, int32_t* bin_status);
 
+/* ---- block-stationary input (SampleCovSet with block_size B > 1) ----
+ * sample_covs(spec, B) / piecewise_prepare (sigmodel.cpp:17-48,
+ * fastfca.cpp:266-268): the F x J block covariances mats[i][jb] = (1/width)
+ * sum x x^H over B consecutive frames (J = ceil(T/B), the last block ragged).
+ * Host layout of `mats`: [batch][bins][blocks][dim*dim] complex (re, im
+ * doubles), each block an Eigen col-major dim x dim matrix (X(r,c) at
+ * r + c*dim) -- SampleCovSet::mats[i][jb].  The *_covs entry points take
+ * such a set (dims->frames = J blocks) and run the same kernels as their
+ * snapshot counterparts on packed Hermitian records (weighted_cov
+ * fastfca.cpp:29-32, decorrelated_powers sigmodel.cpp:97-105). */
+
+/* sample_covs(spec, block_size): x as in ffca_fit (dims->frames = T); mats
+ * (nullable) [batch][bins][J][dim*dim]; power (nullable) [batch][bins] =
+ * SampleCovSet::power_scale (sigmodel.cpp:43-44). */
+int ffca_block_covs(ffca_ctx* ctx, const ffca_dims* dims, int block_size, const double* x,
+                    double* mats, double* power);
+
+/* fastfca_fit / ica_mode_fit on block covariances (dims->frames = J); H is
+ * sources x J per bin.  power may be NULL: SampleCovSet::power() then falls
+ * back to the block traces (sigmodel.cpp:50-55). */
+int ffca_fit_covs(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts,
+                  const double* mats, const double* power, double* W, double* L, double* H,
+                  double* nll, double* nll_slots, int32_t* bin_status);
+int ffca_ica_fit_covs(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts,
+                      const double* mats, const double* power, double* W, double* L, double* H,
+                      double* nll, double* nll_slots, int32_t* bin_status);
+
+/* fastfca_nll_freq per bin and decorrelated_powers (max(0, Re w^H X w),
+ * floored when floor_rel >= 0) on block covariances. */
+int ffca_nll_bins_covs(ffca_ctx* ctx, const ffca_dims* dims, int precision, const double* mats,
+                       const double* W, const double* L, const double* H, double* out);
+int ffca_decorrelated_powers_covs(ffca_ctx* ctx, const ffca_dims* dims, int precision,
+                                  const double* mats, const double* W, double floor_rel,
+                                  double* out);
+
 /* decorrelated_powers (sigmodel.cpp:93-107): out [batch][bins][frames][dim]
  * = |W^H x|^2 per bin (the Eigen col-major dim x frames matrix), floored as
  * floor_positive(u, floor_rel) (sigmodel.cpp:10-15) when floor_rel >= 0. */
@@ -144,6 +179,21 @@ int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_
                     int sources, int frames, const ffca_fit_opts* opts, const void* x_dev,
                     const double* power, double* W, double* L, void* H_dev, double* nll_slots,
                     int32_t* status, void* stream);
+
+/* Block-stationary device path.  rec_dev: [P][blocks][dim*dim] packed
+ * Hermitian records in the compute type (fp32 / fp64 by precision):
+ * [a*dim+a] = X_aa, [a*dim+c] = Re X_ac, [c*dim+a] = Im X_ac for a < c.
+ * ffca_block_covs_device builds them from device x [P][frames][dim]
+ * (sample_covs with block_size, blocks = ceil(frames/block_size)) and writes
+ * power_scale into power (nullable); ffca_fit_covs_device is
+ * ffca_fit_device on them (H_dev [P][blocks][sources]). */
+int ffca_block_covs_device(ffca_ctx* ctx, int problems, int dim, int frames, int block_size,
+                           int precision, const void* x_dev, void* rec_dev, double* power,
+                           void* stream);
+int ffca_fit_covs_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset,
+                         int dim, int sources, int blocks, const ffca_fit_opts* opts,
+                         const void* rec_dev, const double* power, double* W, double* L,
+                         void* H_dev, double* nll_slots, int32_t* status, void* stream);
 
 /* images_dev: [sources][P][frames][dim] complex64 / complex128. */
 int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int frames,

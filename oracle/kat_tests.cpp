@@ -97,7 +97,9 @@ struct Spec {
   int dim, bins, frames;
   std::vector<Complex> x;
   Complex& at(int i, int m, int j) { return x[(size_t(i) * frames + j) * dim + m]; }
-  SampleCovSet covs() const { return sample_covs(dim, bins, frames, x.data()); }
+  SampleCovSet covs(int block_size = 1, bool with_mats = false) const {
+    return sample_covs(dim, bins, frames, x.data(), block_size, with_mats);
+  }
 };
 
 Spec sample_jd_model(const FastFcaParams& truth, std::mt19937& rng) {
@@ -128,8 +130,6 @@ Spec random_spec(int dim, int bins, int frames, std::mt19937& rng) {
   }
   return s;
 }
-
-double is_divergence(double a, double b) { return a / b - std::log(a / b) - 1.0; }
 
 double is_cost(const RMat& u, const RMat& loading, const RMat& act) {  // test_fastfca.cpp:48-56
   RMat lh = matmul(loading, act);
@@ -524,35 +524,38 @@ TEST(fastfca_nll_scalar_unit) {
   CHECK(approx(fastfca_nll(s.covs(), p), 9.0, 1e-12));
 }
 
-// test_sigmodel.cpp:188-208 (B = 1 branch) with the test's own generator
+// test_sigmodel.cpp:188-208 (B = 1 and B = 3) with the test's own generator
 // (test_sigmodel.cpp:22-36: W = I + 0.4 CN, L, H log-uniform on [0.1, 10]).
 TEST(fastfca_nll_equals_fca_nll_jd) {
   std::mt19937 rng(35);
-  const Spec s = random_spec(3, 4, 12, rng);
-  const SampleCovSet covs = s.covs();
-  FastFcaParams fp;
-  fp.dim = 3, fp.bins = 4, fp.frames = 12, fp.sources = 2;
-  for (int i = 0; i < 4; ++i) {
-    CMat w = random_complex(3, 3, rng);
-    for (auto& z : w.a) z *= 0.4;
-    for (int k = 0; k < 3; ++k) w(k, k) += 1.0;
-    fp.decorr.push_back(w);
-    fp.loading.push_back(random_positive(3, 2, rng));
-    fp.act.push_back(random_positive(2, 12, rng));
+  for (int block : {1, 3}) {
+    const Spec s = random_spec(3, 4, 12, rng);
+    const SampleCovSet covs = s.covs(block);
+    const int J = covs.blocks;
+    FastFcaParams fp;
+    fp.dim = 3, fp.bins = 4, fp.frames = J, fp.sources = 2;
+    for (int i = 0; i < 4; ++i) {
+      CMat w = random_complex(3, 3, rng);
+      for (auto& z : w.a) z *= 0.4;
+      for (int k = 0; k < 3; ++k) w(k, k) += 1.0;
+      fp.decorr.push_back(w);
+      fp.loading.push_back(random_positive(3, 2, rng));
+      fp.act.push_back(random_positive(2, J, rng));
+    }
+    auto fca_of = [&](const FastFcaParams& p) {
+      const auto scms = reconstruct_scms(p);
+      double acc = 0.0;
+      for (int i = 0; i < p.bins; ++i) acc += fca_nll_freq(covs, i, scms[i], p.act[i]);
+      return acc;
+    };
+    CHECK(approx(fastfca_nll(covs, fp), fca_of(fp), eps_tol(1e-9, 1e-7)));
+    FastFcaParams fp2 = fp;
+    for (int i = 0; i < 4; ++i) {
+      for (double& v : fp2.loading[i].a) v *= 1.7;
+      fp2.act[i] = random_positive(2, J, rng);
+    }
+    CHECK(approx(fastfca_nll(covs, fp2), fca_of(fp2), eps_tol(1e-9, 1e-7)));
   }
-  auto fca_of = [&](const FastFcaParams& p) {
-    const auto scms = reconstruct_scms(p);
-    double acc = 0.0;
-    for (int i = 0; i < p.bins; ++i) acc += fca_nll_freq(covs, i, scms[i], p.act[i]);
-    return acc;
-  };
-  CHECK(approx(fastfca_nll(covs, fp), fca_of(fp), eps_tol(1e-9, 1e-7)));
-  FastFcaParams fp2 = fp;
-  for (int i = 0; i < 4; ++i) {
-    for (double& v : fp2.loading[i].a) v *= 1.7;
-    fp2.act[i] = random_positive(2, 12, rng);
-  }
-  CHECK(approx(fastfca_nll(covs, fp2), fca_of(fp2), eps_tol(1e-9, 1e-7)));
 }
 
 // test_sigmodel.cpp:210-224
@@ -647,6 +650,7 @@ TEST(ica_mode_unmixes_determined_mixture) {
   covs.dim = m;
   covs.bins = bins;
   covs.frames = frames;
+  covs.blocks = frames;
   covs.snapshots = f;
   for (int i = 0; i < bins; ++i) {
     double s = 0.0;
@@ -677,6 +681,205 @@ TEST(ica_mode_unmixes_determined_mixture) {
     threw = true;
   }
   CHECK(threw);
+}
+
+// ------------------------------------------------ block-stationary input --
+
+// test_fastfca.cpp:63-78: a single-bin set of diagonal block covariances
+// (no power_scale: power() falls back to the traces, sigmodel.cpp:50-55).
+SampleCovSet diagonal_covset(int dim, int frames, std::mt19937& rng) {
+  SampleCovSet covs;
+  covs.dim = dim;
+  covs.bins = 1;
+  covs.blocks = frames;
+  covs.frames = frames;
+  covs.block_size = dim;
+  covs.mats.resize(1);
+  for (int j = 0; j < frames; ++j) {
+    CMat d(dim, dim);
+    for (int k = 0; k < dim; ++k) d(k, k) = Complex(0.2 + std::abs(randn(rng)), 0);
+    covs.mats[0].push_back(d);
+  }
+  return covs;
+}
+
+CMat outer_mean(const Spec& s, int i, int j0, int width) {
+  CMat r(s.dim, s.dim);
+  for (int j = j0; j < j0 + width; ++j)
+    for (int c = 0; c < s.dim; ++c)
+      for (int a = 0; a < s.dim; ++a)
+        r(a, c) += s.x[(size_t(i) * s.frames + j) * s.dim + a] *
+                   std::conj(s.x[(size_t(i) * s.frames + j) * s.dim + c]);
+  for (auto& z : r.a) z /= double(width);
+  return r;
+}
+
+// test_sigmodel.cpp:79-95
+TEST(sample_covs_block_averaging) {
+  std::mt19937 rng(32);
+  const Spec s = random_spec(2, 3, 11, rng);  // 11 = 2 full blocks of 4 + 3
+  const SampleCovSet covs = s.covs(4);
+  CHECK(covs.blocks == 3);
+  for (int i = 0; i < 3; ++i)
+    for (int jb = 0; jb < 3; ++jb) {
+      const int j0 = jb * 4, width = std::min(4, 11 - j0);
+      CHECK(rel_err(covs.mats[i][jb], outer_mean(s, i, j0, width)) < 1e-12);
+    }
+  bool t1 = false, t2 = false;
+  try { sample_covs(2, 0, 0, nullptr, 1); } catch (const std::invalid_argument&) { t1 = true; }
+  try { s.covs(0); } catch (const std::invalid_argument&) { t2 = true; }
+  CHECK(t1);
+  CHECK(t2);
+}
+
+// test_sigmodel.cpp:225-254: on PD block covariances (B = M) the likelihood
+// splits into ajd divergence + IS mismatch + sum(ln det Xhat + M).
+TEST(fastfca_nll_block_decomposition) {
+  std::mt19937 rng(37);
+  const int m = 3;
+  const Spec s = random_spec(m, 3, 4 * m, rng);
+  const SampleCovSet covs = s.covs(m);
+  FastFcaParams p;
+  p.dim = m, p.bins = 3, p.frames = covs.blocks, p.sources = 2;
+  for (int i = 0; i < 3; ++i) {  // random_fastfca_params (test_sigmodel.cpp:22-36)
+    CMat w = random_complex(m, m, rng);
+    for (auto& z : w.a) z *= 0.4;
+    for (int k = 0; k < m; ++k) w(k, k) += 1.0;
+    p.decorr.push_back(w);
+    p.loading.push_back(random_positive(m, 2, rng));
+    p.act.push_back(random_positive(2, covs.blocks, rng));
+  }
+  double ajd = 0.0, is_mismatch = 0.0, data_term = 0.0;
+  for (int i = 0; i < covs.bins; ++i) {
+    const CMat& w = p.decorr[i];
+    const RMat u = decorrelated_powers(covs, i, w);
+    for (int j = 0; j < covs.blocks; ++j) {
+      const CMat a = matmul(matmul(adjoint(w), covs.mats[i][j]), w);
+      CMat d(m, m);
+      for (int k = 0; k < m; ++k) d(k, k) = a(k, k);
+      ajd += logdet_divergence(a, d);
+      for (int k = 0; k < m; ++k) {
+        double s2 = var_eps(covs.power(i));
+        for (int n = 0; n < 2; ++n) s2 += p.loading[i](k, n) * p.act[i](n, j);
+        is_mismatch += is_divergence(u(k, j), s2);
+      }
+      data_term += logdet_hpd(covs.mats[i][j]) + m;
+    }
+  }
+  CHECK(approx(fastfca_nll(covs, p), ajd + is_mismatch + data_term, 1e-8));
+}
+
+// test_fastfca.cpp:124-134 on the reference's own diagonal block set.
+TEST(ip_keeps_diagonal_blocks) {
+  std::mt19937 rng(63);
+  const SampleCovSet covs = diagonal_covset(3, 40, rng);
+  CMat w = CMat::identity(3);
+  const RMat loading = random_positive(3, 2, rng);
+  const RMat act = random_positive(2, 40, rng);
+  ip_update_w(covs, 0, w, loading, act);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      if (r != c) CHECK(std::abs(w(r, c)) < 1e-12);
+}
+
+// test_fastfca.cpp:368-372
+TEST(ajd_cost_zero_on_diagonal) {
+  std::mt19937 rng(75);
+  const SampleCovSet covs = diagonal_covset(3, 10, rng);
+  CHECK(std::abs(ajd_cost(CMat::identity(3), covs, 0)) < 1e-12);
+}
+
+// test_fastfca.cpp:424-450: along an IP+MM trajectory on B = M blocks the
+// recorded NLL equals ajd_cost + IS term + data term.
+TEST(decomposition_identity_along_fit) {
+  std::mt19937 rng(76);
+  const int m = 2;
+  Spec s{m, 2, 8 * m, std::vector<Complex>(size_t(m) * 2 * 8 * m)};
+  for (int i = 0; i < 2; ++i) {
+    const CMat r = random_complex(m, 8 * m, rng);
+    for (int j = 0; j < 8 * m; ++j)
+      for (int k = 0; k < m; ++k) s.at(i, k, j) = r(k, j);
+  }
+  const SampleCovSet covs = s.covs(m);
+  FastFcaParams p = random_params(m, 2, covs.blocks, 2, rng);
+  for (int t = 0; t < 6; ++t) {
+    const FastFcaFitResult fit = fastfca_fit(covs, p, LhFlavor::mm, 1);
+    p = fit.params;
+    double lhs = 0.0;
+    for (int i = 0; i < 2; ++i) {
+      const RMat u = decorrelated_powers(covs, i, p.decorr[i]);
+      double is_term = 0.0, data_term = 0.0;
+      for (int j = 0; j < covs.blocks; ++j) {
+        for (int k = 0; k < m; ++k) {
+          double s2 = var_eps(covs.power(i));
+          for (int n = 0; n < 2; ++n) s2 += p.loading[i](k, n) * p.act[i](n, j);
+          is_term += is_divergence(u(k, j), s2);
+        }
+        data_term += logdet_hpd(covs.mats[i][j]) + m;
+      }
+      lhs += ajd_cost(p.decorr[i], covs, i) + is_term + data_term;
+    }
+    CHECK(approx(lhs, fit.nll.back(), 1e-8));
+  }
+}
+
+// test_fastfca.cpp:493-502
+TEST(ica_mode_keeps_diagonal_blocks) {
+  std::mt19937 rng(78);
+  const SampleCovSet covs = diagonal_covset(2, 30, rng);
+  const std::vector<CMat> w_init(1, CMat::identity(2));
+  const FastFcaFitResult fit = ica_mode_fit(covs, 2, 10, w_init);
+  const CMat& w = fit.params.decorr[0];
+  CHECK(std::abs(w(0, 1)) < 1e-12);
+  CHECK(std::abs(w(1, 0)) < 1e-12);
+}
+
+// test_fastfca.cpp:504-539
+TEST(piecewise_prepare_block_conventions) {
+  std::mt19937 rng(79);
+  Spec s{3, 2, 12, std::vector<Complex>(3 * 2 * 12)};
+  for (int i = 0; i < 2; ++i) {
+    const CMat r = random_complex(3, 12, rng);
+    for (int j = 0; j < 12; ++j)
+      for (int k = 0; k < 3; ++k) s.at(i, k, j) = r(k, j);
+  }
+  {  // B = 1 reproduces the plain sample covariances
+    const SampleCovSet a = piecewise_prepare(3, 2, 12, s.x.data(), 1);
+    const SampleCovSet b = s.covs(1, true);
+    CHECK(a.blocks == b.blocks);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 12; ++j) CHECK(rel_err(a.mats[i][j], b.mats[i][j]) == 0.0);
+  }
+  {  // B = J collapses to the global sample covariance
+    const SampleCovSet a = piecewise_prepare(3, 2, 12, s.x.data(), 12);
+    CHECK(a.blocks == 1);
+    for (int i = 0; i < 2; ++i) CHECK(rel_err(a.mats[i][0], outer_mean(s, i, 0, 12)) < 1e-12);
+  }
+  {  // B = M gives PD blocks with a finite diagonality cost
+    const SampleCovSet a = piecewise_prepare(3, 2, 12, s.x.data(), 3);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < a.blocks; ++j) CHECK(is_positive_definite(a.mats[i][j]));
+    CMat w = random_complex(3, 3, rng);
+    for (auto& z : w.a) z *= 0.2;
+    for (int k = 0; k < 3; ++k) w(k, k) += 1.0;
+    const double cost = ajd_cost(w, a, 0);
+    CHECK(std::isfinite(cost));
+    CHECK(cost >= 0.0);
+  }
+}
+
+// sigmodel.cpp:164-196: expand_block_params replicates block columns, the
+// ragged tail block covering the remaining frames.
+TEST(expand_block_params_replicates) {
+  std::mt19937 rng(80);
+  FastFcaParams p = random_params(2, 2, 3, 2, rng);
+  const FastFcaParams e = expand_block_params(p, 4, 11);
+  CHECK(e.frames == 11);
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 11; ++j)
+      for (int n = 0; n < 2; ++n) CHECK(e.act[i](n, j) == p.act[i](n, std::min(j / 4, 2)));
+  const FastFcaParams same = expand_block_params(p, 1, 3);
+  CHECK(same.act[0].a == p.act[0].a);
 }
 
 int main(int argc, char** argv) {

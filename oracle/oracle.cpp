@@ -147,39 +147,111 @@ void floor_positive(RMat& m, double rel) {
   for (double& v : m.a) v = std::max(v, floor);
 }
 
-// sigmodel.cpp:17-48, block_size == 1: snapshots[i] = spec.f[i] (:45),
-// power_scale[i] = sum_j tr(x_j x_j^H) / (T * M) (:33-44).
-SampleCovSet sample_covs(int dim, int bins, int frames, const Complex* x) {
+// sigmodel.cpp:17-48: snapshots[i] = spec.f[i] for block_size == 1 (:45);
+// mats[i][jb] = (1/width) sum_{j in block} x_j x_j^H (:34-41), built for
+// block_size > 1 (or on request); power_scale[i] = sum_jb tr(mats[i][jb]) /
+// (blocks * M) (:33-44) -- for block_size == 1 the trace of x x^H is |x|^2.
+SampleCovSet sample_covs(int dim, int bins, int frames, const Complex* x, int block_size,
+                         bool with_mats) {
   if (bins == 0 || frames == 0 || dim == 0)
     throw std::invalid_argument("sample_covs: empty spectrogram");
+  if (block_size < 1) throw std::invalid_argument("sample_covs: block size must be >= 1");
   SampleCovSet covs;
   covs.dim = dim;
   covs.bins = bins;
   covs.frames = frames;
-  covs.snapshots.resize(bins);
+  covs.block_size = block_size;
+  covs.blocks = (frames + block_size - 1) / block_size;
+  const bool mats = block_size > 1 || with_mats;
+  if (mats) covs.mats.resize(bins);
+  if (block_size == 1) covs.snapshots.resize(bins);
   covs.power_scale.assign(bins, 0.0);
   for (int i = 0; i < bins; ++i) {
-    CMat& s = covs.snapshots[i];
-    s = CMat(dim, frames);
     const Complex* xi = x + size_t(i) * frames * dim;
     double trace_sum = 0.0;
-    for (int j = 0; j < frames; ++j) {
-      double tr = 0.0;
-      for (int m = 0; m < dim; ++m) {
-        s(m, j) = xi[size_t(j) * dim + m];
-        tr += std::real(s(m, j) * std::conj(s(m, j)));
+    if (mats) {
+      covs.mats[i].resize(covs.blocks);
+      for (int jb = 0; jb < covs.blocks; ++jb) {
+        const int j0 = jb * block_size;
+        const int width = std::min(block_size, frames - j0);
+        CMat r(dim, dim);
+        for (int j = j0; j < j0 + width; ++j)
+          for (int c = 0; c < dim; ++c) {
+            const Complex xc = std::conj(xi[size_t(j) * dim + c]);
+            for (int a = 0; a < dim; ++a) r(a, c) += xi[size_t(j) * dim + a] * xc;
+          }
+        double tr = 0.0;
+        for (auto& z : r.a) z /= double(width);
+        for (int a = 0; a < dim; ++a) tr += r(a, a).real();
+        trace_sum += tr;
+        covs.mats[i][jb] = std::move(r);
       }
-      trace_sum += tr;
+    } else {
+      for (int j = 0; j < frames; ++j)
+        for (int m = 0; m < dim; ++m) trace_sum += std::norm(xi[size_t(j) * dim + m]);
     }
-    covs.power_scale[i] = trace_sum / (double(frames) * dim);
+    covs.power_scale[i] = trace_sum / (double(covs.blocks) * dim);
+    if (block_size == 1) {
+      CMat& s = covs.snapshots[i];
+      s = CMat(dim, frames);
+      for (int j = 0; j < frames; ++j)
+        for (int m = 0; m < dim; ++m) s(m, j) = xi[size_t(j) * dim + m];
+    }
   }
   return covs;
 }
 
+// sigmodel.cpp:50-55
+double SampleCovSet::power(int i) const {
+  if (i < int(power_scale.size())) return power_scale[i];
+  double trace_sum = 0.0;
+  for (const CMat& m : mats[i])
+    for (int a = 0; a < m.r; ++a) trace_sum += m(a, a).real();
+  return trace_sum / (double(blocks) * dim);
+}
+
+// fastfca.cpp:266-268
+SampleCovSet piecewise_prepare(int dim, int bins, int frames, const Complex* x, int block_size) {
+  return sample_covs(dim, bins, frames, x, block_size, true);
+}
+
+// sigmodel.cpp:164-176 (replicate_columns) and :188-196.
+FastFcaParams expand_block_params(const FastFcaParams& p, int block_size, int frames) {
+  if (block_size == 1 && frames == p.frames) return p;
+  FastFcaParams out = p;
+  out.frames = frames;
+  for (int i = 0; i < p.bins; ++i) {
+    const RMat& h = p.act[i];
+    RMat e(h.r, frames);
+    for (int j = 0; j < frames; ++j) {
+      const int jb = std::min(j / block_size, h.c - 1);
+      for (int n = 0; n < h.r; ++n) e(n, j) = h(n, jb);
+    }
+    out.act[i] = std::move(e);
+  }
+  return out;
+}
+
 // sigmodel.cpp:93-107 (snapshot branch :96): U = |W^H X|^2.
 RMat decorrelated_powers(const SampleCovSet& covs, int i, const CMat& w) {
-  const CMat& x = covs.snapshots[i];
   const int m = covs.dim;
+  if (!covs.has_snapshots()) {  // :97-105: u(k, j) = max(0, Re w_k^H X_j w_k)
+    RMat u(m, covs.blocks);
+    for (int j = 0; j < covs.blocks; ++j) {
+      const CMat& xm = covs.mats[i][j];
+      for (int k = 0; k < m; ++k) {
+        Complex acc = 0.0;
+        for (int r = 0; r < m; ++r) {
+          Complex xw = 0.0;
+          for (int c = 0; c < m; ++c) xw += xm(r, c) * w(c, k);
+          acc += std::conj(w(r, k)) * xw;
+        }
+        u(k, j) = std::max(0.0, acc.real());
+      }
+    }
+    return u;
+  }
+  const CMat& x = covs.snapshots[i];
   RMat u(m, x.c);
   for (int j = 0; j < x.c; ++j)
     for (int k = 0; k < m; ++k) {
@@ -212,12 +284,12 @@ double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RM
   double ratio = 0.0, logs = 0.0;
   for (size_t k = 0; k < u.a.size(); ++k) ratio += u.a[k] / s2.a[k];
   for (size_t k = 0; k < s2.a.size(); ++k) logs += std::log(s2.a[k]);
-  return -covs.frames * logdet + ratio + logs;
+  return -covs.blocks * logdet + ratio + logs;
 }
 
 // sigmodel.cpp:215-222
 double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& p) {
-  if (covs.dim != p.dim || covs.bins != p.bins || covs.frames != p.frames)
+  if (covs.dim != p.dim || covs.bins != p.bins || covs.blocks != p.frames)
     throw std::invalid_argument("nll: covariance/parameter shape mismatch");
   double acc = 0.0;
   for (int i = 0; i < covs.bins; ++i)
@@ -229,9 +301,10 @@ double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& p) {
 double fca_nll_freq(const SampleCovSet& covs, int i, const std::vector<CMat>& scm_i,
                     const RMat& power_i) {
   const int m = covs.dim;
-  const CMat& xs = covs.snapshots[i];
+  const bool snap = covs.has_snapshots();
+  const CMat& xs = snap ? covs.snapshots[i] : covs.mats[i][0];
   double acc = 0.0;
-  for (int j = 0; j < xs.c; ++j) {
+  for (int j = 0; j < covs.blocks; ++j) {
     CMat x(m, m);
     for (size_t n = 0; n < scm_i.size(); ++n)
       for (size_t k = 0; k < x.a.size(); ++k) x.a[k] += power_i(int(n), j) * scm_i[n].a[k];
@@ -249,6 +322,24 @@ double fca_nll_freq(const SampleCovSet& covs, int i, const std::vector<CMat>& sc
       }
     }
     for (int k = 0; k < m; ++k) acc += 2.0 * std::log(l(k, k).real());
+    if (!snap) {  // :149-150: tr(X^-1 Xhat_j), column by column
+      const CMat& xm = covs.mats[i][j];
+      for (int c = 0; c < m; ++c) {
+        std::vector<Complex> y(m);
+        for (int k = 0; k < m; ++k) {
+          Complex s = xm(k, c);
+          for (int p = 0; p < k; ++p) s -= l(k, p) * y[p];
+          y[k] = s / l(k, k);
+        }
+        for (int k = m - 1; k >= 0; --k) {
+          Complex s = y[k];
+          for (int p = k + 1; p < m; ++p) s -= std::conj(l(p, k)) * y[p];
+          y[k] = s / l(k, k);
+        }
+        acc += y[c].real();
+      }
+      continue;
+    }
     std::vector<Complex> y(m);
     for (int k = 0; k < m; ++k) {
       Complex s = xs(k, j);
@@ -269,16 +360,25 @@ double fca_nll_freq(const SampleCovSet& covs, int i, const std::vector<CMat>& sc
 
 // -------------------------------------------------------------- fastfca --
 
-// fastfca.cpp:22-34 (snapshot branch) + symmetrize (hermitian.hpp:31-34).
+// fastfca.cpp:22-34 + symmetrize (hermitian.hpp:31-34).  Snapshot branch
+// (:25-28): q = X diag(1/s2) X^H; block branch (:30-31): q = sum_j mats_j / s2_j.
 CMat weighted_cov(const SampleCovSet& covs, int i, const double* sigma2_row, int stride) {
-  const CMat& x = covs.snapshots[i];
-  const int m = covs.dim, blocks = x.c;
+  const int m = covs.dim, blocks = covs.blocks;
   CMat q(m, m);
-  for (int j = 0; j < blocks; ++j) {
-    const double inv = 1.0 / sigma2_row[size_t(j) * stride];
-    for (int b = 0; b < m; ++b) {
-      const Complex xb = std::conj(x(b, j));
-      for (int a = 0; a < m; ++a) q(a, b) += (x(a, j) * inv) * xb;
+  if (covs.has_snapshots()) {
+    const CMat& x = covs.snapshots[i];
+    for (int j = 0; j < blocks; ++j) {
+      const double inv = 1.0 / sigma2_row[size_t(j) * stride];
+      for (int b = 0; b < m; ++b) {
+        const Complex xb = std::conj(x(b, j));
+        for (int a = 0; a < m; ++a) q(a, b) += (x(a, j) * inv) * xb;
+      }
+    }
+  } else {
+    for (int j = 0; j < blocks; ++j) {
+      const double s = sigma2_row[size_t(j) * stride];
+      const CMat& xm = covs.mats[i][j];
+      for (size_t k = 0; k < q.a.size(); ++k) q.a[k] += xm.a[k] / s;
     }
   }
   CMat out(m, m);
@@ -435,7 +535,7 @@ void balance_scales(CMat& w, RMat& loading, RMat& act) {
 FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init,
                              LhFlavor flavor, int iters, const FitOptions& fit,
                              const FastFcaOptions& opts, std::vector<double>* slots_out) {
-  if (init.dim != covs.dim || init.bins != covs.bins || init.frames != covs.frames)
+  if (init.dim != covs.dim || init.bins != covs.bins || init.frames != covs.blocks)
     throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
   FastFcaFitResult result;
   result.params = init;
@@ -490,7 +590,7 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
   FastFcaParams params;
   params.dim = covs.dim;
   params.bins = covs.bins;
-  params.frames = covs.frames;
+  params.frames = covs.blocks;
   params.sources = sources;
   params.decorr = w_init;
   for (int i = 0; i < covs.bins; ++i) {
@@ -502,6 +602,111 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
   FastFcaOptions opts;
   opts.fix_loadings = true;
   return fastfca_fit(covs, params, LhFlavor::mm, iters, fit, opts, slots_out);
+}
+
+// hermitian.hpp:74-79
+double is_divergence(double w1, double w2) {
+  if (!(w1 > 0.0) || !(w2 > 0.0))
+    throw std::domain_error("is_divergence: arguments must be positive");
+  const double r = w1 / w2;
+  return std::max(0.0, r - std::log(r) - 1.0);
+}
+
+namespace {
+CMat symmetrize(const CMat& a) {  // hermitian.hpp:31-34
+  CMat s(a.r, a.c);
+  for (int c = 0; c < a.c; ++c)
+    for (int r = 0; r < a.r; ++r) s(r, c) = (a(r, c) + std::conj(a(c, r))) / 2.0;
+  return s;
+}
+// Lower Cholesky factor (Eigen::LLT reads the lower triangle); false when not PD.
+bool llt(const CMat& x, CMat& l) {
+  const int m = x.r;
+  l = CMat(m, m);
+  for (int k = 0; k < m; ++k) {
+    double d = x(k, k).real();
+    for (int p = 0; p < k; ++p) d -= std::norm(l(k, p));
+    if (!(d > 0.0)) return false;
+    const double lkk = std::sqrt(d);
+    l(k, k) = lkk;
+    for (int r = k + 1; r < m; ++r) {
+      Complex s = x(r, k);
+      for (int p = 0; p < k; ++p) s -= l(r, p) * std::conj(l(k, p));
+      l(r, k) = s / lkk;
+    }
+  }
+  return true;
+}
+}  // namespace
+
+// hermitian.hpp:42-47
+bool is_positive_definite(const CMat& a) {
+  if (a.r != a.c) return false;
+  double mx = 0.0, dev = 0.0;
+  for (int c = 0; c < a.c; ++c)
+    for (int r = 0; r < a.r; ++r) {
+      mx = std::max(mx, std::abs(a(r, c)));
+      dev = std::max(dev, std::abs(a(r, c) - std::conj(a(c, r))));
+    }
+  if (!(dev <= 1e-10 * (1.0 + mx))) return false;
+  CMat l;
+  return llt(symmetrize(a), l);
+}
+
+double logdet_hpd(const CMat& a) {
+  CMat l;
+  if (!llt(symmetrize(a), l)) throw NumericalError("logdet_hpd: not positive definite");
+  double s = 0.0;
+  for (int k = 0; k < a.r; ++k) s += 2.0 * std::log(l(k, k).real());
+  return s;
+}
+
+// hermitian.hpp:81-102: tr(A B^-1) - ln det(A B^-1) - M (LLT of both).
+double logdet_divergence(const CMat& a, const CMat& b) {
+  if (a.r != a.c || b.r != b.c || a.r != b.r)
+    throw std::invalid_argument("logdet_divergence: dimension mismatch");
+  const int m = a.r;
+  CMat la, lb;
+  if (!llt(symmetrize(a), la) || !llt(symmetrize(b), lb))
+    throw NumericalError("logdet_divergence: argument not positive definite");
+  double tr = 0.0;  // tr(B^-1 A) column by column
+  for (int c = 0; c < m; ++c) {
+    std::vector<Complex> y(m);
+    for (int k = 0; k < m; ++k) {
+      Complex s = a(k, c);
+      for (int p = 0; p < k; ++p) s -= lb(k, p) * y[p];
+      y[k] = s / lb(k, k);
+    }
+    for (int k = m - 1; k >= 0; --k) {
+      Complex s = y[k];
+      for (int p = k + 1; p < m; ++p) s -= std::conj(lb(p, k)) * y[p];
+      y[k] = s / lb(k, k);
+    }
+    tr += y[c].real();
+  }
+  double lda = 0.0, ldb = 0.0;
+  for (int k = 0; k < m; ++k) {
+    lda += 2.0 * std::log(la(k, k).real());
+    ldb += 2.0 * std::log(lb(k, k).real());
+  }
+  return std::max(0.0, tr - (lda - ldb) - double(m));
+}
+
+// fastfca.cpp:225-239
+double ajd_cost(const CMat& w, const SampleCovSet& covs, int i,
+                const std::vector<double>& weights) {
+  if (!weights.empty() && int(weights.size()) != covs.blocks)
+    throw std::invalid_argument("ajd_cost: weight count mismatch");
+  const int m = covs.dim;
+  double acc = 0.0;
+  for (int j = 0; j < covs.blocks; ++j) {
+    const CMat t = matmul(matmul(adjoint(w), covs.mats[i][j]), w);
+    CMat d(m, m);
+    for (int k = 0; k < m; ++k) d(k, k) = t(k, k);
+    const double alpha = weights.empty() ? 1.0 : weights[j];
+    acc += alpha * logdet_divergence(t, d);
+  }
+  return acc;
 }
 
 // fastfca.cpp:193-203

@@ -81,14 +81,19 @@ struct FastFcaOptions {  // fastfca.hpp:18-21
   bool normalize_scales = true;
 };
 
-// SampleCovSet restricted to the block_size == 1 snapshot branch the hot path
-// reads (sigmodel.hpp:48-56; `mats` is omitted: fastfca.cpp:25-28 and
-// sigmodel.cpp:95-96 never touch it when snapshots exist).
+// SampleCovSet (sigmodel.hpp:48-56).  block_size == 1 keeps the snapshots
+// the hot path reads (fastfca.cpp:25-28, sigmodel.cpp:95-96) and builds the
+// rank-one `mats` only on request (sample_covs(..., with_mats)); block_size
+// B > 1 stores the block covariances mats[i][jb] = (1/width) sum x x^H over
+// B consecutive frames (sigmodel.cpp:34-41), the block-stationary input of
+// weighted_cov / decorrelated_powers (fastfca.cpp:29-32, sigmodel.cpp:98-105).
 struct SampleCovSet {
-  int dim = 0, bins = 0, frames = 0;
-  std::vector<CMat> snapshots;
-  std::vector<double> power_scale;
-  double power(int i) const { return power_scale[i]; }
+  int dim = 0, bins = 0, blocks = 0, frames = 0, block_size = 1;
+  std::vector<std::vector<CMat>> mats;  // [i][jb], dim x dim
+  std::vector<CMat> snapshots;          // [i], dim x frames (block_size == 1)
+  std::vector<double> power_scale;      // [i]
+  bool has_snapshots() const { return !snapshots.empty(); }
+  double power(int i) const;            // sigmodel.cpp:50-55
 };
 
 struct FastFcaParams {  // sigmodel.hpp:72-78
@@ -120,7 +125,12 @@ double frob(const CMat& a);
 
 // ---- hot-path restatement ----
 void floor_positive(RMat& m, double rel = kPowerFloorRel);         // sigmodel.cpp:10-15
-SampleCovSet sample_covs(int dim, int bins, int frames, const Complex* x);  // sigmodel.cpp:17-48
+SampleCovSet sample_covs(int dim, int bins, int frames, const Complex* x, int block_size = 1,
+                         bool with_mats = false);                   // sigmodel.cpp:17-48
+// piecewise_prepare (fastfca.cpp:266-268) == sample_covs(spec, block_size), mats included.
+SampleCovSet piecewise_prepare(int dim, int bins, int frames, const Complex* x, int block_size);
+// expand_block_params (sigmodel.cpp:164-196): block-level H -> frame level.
+FastFcaParams expand_block_params(const FastFcaParams& p, int block_size, int frames);
 CMat weighted_cov(const SampleCovSet& covs, int i, const double* sigma2_row,
                   int stride);                                     // fastfca.cpp:22-34
 void ip_update_w(const SampleCovSet& covs, int i, CMat& w, const RMat& loading,
@@ -150,6 +160,14 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
 FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
                               const std::vector<CMat>& w_init, const FitOptions& fit = {},
                               std::vector<double>* slots_out = nullptr);
+// hermitian.hpp:74-79, :81-102 and fastfca.cpp:225-239 (ajd_cost): used by
+// the reference's block-stationary decomposition tests.
+double is_divergence(double w1, double w2);
+double logdet_divergence(const CMat& a, const CMat& b);
+bool is_positive_definite(const CMat& a);                          // hermitian.hpp (LLT succeeds)
+double logdet_hpd(const CMat& a);                                  // ln det of a Hermitian PD matrix
+double ajd_cost(const CMat& w, const SampleCovSet& covs, int i,
+                const std::vector<double>& weights = {});
 CMat fastfca_mwf(const FastFcaParams& p, int i, int j, int n);     // fastfca.cpp:193-203
 // Separated images, [n][i] -> dim x frames (fastfca.cpp:205-223).
 std::vector<std::vector<CMat>> fastfca_separate(const SampleCovSet& covs,

@@ -38,6 +38,11 @@ def lib() -> C.CDLL:
         L.oracle_source_gain.argtypes = [i, i, i, P, P, i, P, P, i]
         L.oracle_ica_fit.argtypes = [i, i, i, i, P, P, P, P, i, i, u64, i, P, P, i]
         L.oracle_decorrelated_powers.argtypes = [i, i, i, P, P, d, P, P, i]
+        L.oracle_block_covs.argtypes = [i, i, i, i, P, P, P, P, i]
+        L.oracle_fit_covs.argtypes = [i, i, i, i, P, P, P, P, P, i, i, i, u64, i, i, i, i, P, P,
+                                      P, i]
+        L.oracle_nll_bins_covs.argtypes = [i, i, i, i, P, P, P, P, P, P, i]
+        L.oracle_decorrelated_powers_covs.argtypes = [i, i, i, P, P, d, P, P, i]
         _lib = L
     return _lib
 
@@ -162,4 +167,73 @@ def separate(x, W, L, H) -> np.ndarray:
     out = np.empty((N, F, T, M), np.complex128)
     xr = _xref(x)
     _call(lib().oracle_separate, F, M, N, T, _p(xr), _p(Wr), _p(Lr), _p(Hr), _p(out))
+    return np.swapaxes(out, -1, -2)
+
+
+# ------------------------------------------------ block-stationary input --
+def _mref(mats):
+    """[F, J, M, M] natural -> per-block Eigen col-major complex128."""
+    return np.array(np.swapaxes(mats, -1, -2), dtype=np.complex128, order="C", copy=True)
+
+
+def block_covs(x, block_size):
+    """sample_covs(spec, block_size) (sigmodel.cpp:17-48) on x [F,M,T]:
+    (mats [F, J, M, M] natural layout, power_scale [F])."""
+    F, M, T = x.shape
+    J = -(-T // block_size)
+    mats = np.zeros((F, J, M, M), np.complex128)
+    power = np.zeros(F)
+    xr = _xref(x)
+    _call(lib().oracle_block_covs, F, M, T, int(block_size), _p(xr), _p(mats), _p(power))
+    return np.swapaxes(mats, -1, -2), power
+
+
+def fit_covs(mats, W, L, H, iters, flavor=0, power=None, record_trace=True, seed=0,
+             normalize_scales=True, fix_loadings=False, workers=1, slots=False):
+    """fastfca_fit on block covariances mats [F, J, M, M] (H [F, N, J]).
+    Returns (W, L, H, nll, slots or None)."""
+    F, J, M, _ = mats.shape
+    N = L.shape[-1]
+    mr = _mref(mats)
+    Wr, Lr, Hr = _pref(W, L, H)
+    nll = np.zeros(iters + 1)
+    sl = np.zeros((iters + 1, F)) if slots else None
+    pw = None if power is None else np.ascontiguousarray(power, np.float64)
+    _call(lib().oracle_fit_covs, F, M, N, J, _p(mr), _p(pw), _p(Wr), _p(Lr), _p(Hr), int(flavor),
+          int(iters), int(record_trace), int(seed), int(normalize_scales), int(fix_loadings),
+          int(workers), 0, _p(nll), _p(sl))
+    return (np.swapaxes(Wr, -1, -2), np.swapaxes(Lr, -1, -2), np.swapaxes(Hr, -1, -2), nll, sl)
+
+
+def ica_fit_covs(mats, W_init, iters, power=None, record_trace=True, seed=0, workers=1):
+    """ica_mode_fit on block covariances.  Returns (W, L, H, nll)."""
+    F, J, M, _ = mats.shape
+    mr = _mref(mats)
+    Wr = np.array(np.swapaxes(W_init, -1, -2), dtype=np.complex128, order="C", copy=True)
+    Lr = np.zeros((F, M, M))
+    Hr = np.zeros((F, J, M))
+    nll = np.zeros(iters + 1)
+    pw = None if power is None else np.ascontiguousarray(power, np.float64)
+    _call(lib().oracle_fit_covs, F, M, M, J, _p(mr), _p(pw), _p(Wr), _p(Lr), _p(Hr), 1,
+          int(iters), int(record_trace), int(seed), 1, 1, int(workers), 1, _p(nll), None)
+    return (np.swapaxes(Wr, -1, -2), np.swapaxes(Lr, -1, -2), np.swapaxes(Hr, -1, -2), nll)
+
+
+def nll_bins_covs(mats, W, L, H) -> np.ndarray:
+    F, J, M, _ = mats.shape
+    N = L.shape[-1]
+    mr = _mref(mats)
+    Wr, Lr, Hr = _pref(W, L, H)
+    out = np.empty(F)
+    _call(lib().oracle_nll_bins_covs, F, M, N, J, _p(mr), _p(Wr), _p(Lr), _p(Hr), _p(out))
+    return out
+
+
+def decorrelated_powers_covs(mats, W, floor_rel=1e-12):
+    F, J, M, _ = mats.shape
+    mr = _mref(mats)
+    Wr = np.array(np.swapaxes(W, -1, -2), dtype=np.complex128, order="C", copy=True)
+    out = np.zeros((F, J, M))
+    _call(lib().oracle_decorrelated_powers_covs, F, M, J, _p(mr), _p(Wr),
+          -1.0 if floor_rel is None else float(floor_rel), _p(out))
     return np.swapaxes(out, -1, -2)

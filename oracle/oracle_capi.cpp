@@ -70,9 +70,109 @@ void store_params(const FastFcaParams& p, double* W, double* L, double* H) {
   }
 }
 
+// SampleCovSet from caller block covariances [bins][blocks][dim*dim] complex
+// (Eigen col-major per block); power (nullable) -> power_scale, else
+// power() falls back to the traces (sigmodel.cpp:50-55).
+SampleCovSet covs_from_mats(int bins, int dim, int blocks, const double* mats,
+                            const double* power) {
+  SampleCovSet c;
+  c.dim = dim, c.bins = bins, c.blocks = blocks, c.frames = blocks;
+  c.block_size = 0;  // unknown for a caller-built set; unused by the path
+  c.mats.resize(bins);
+  for (int i = 0; i < bins; ++i)
+    for (int j = 0; j < blocks; ++j) {
+      CMat m(dim, dim);
+      std::memcpy(static_cast<void*>(m.data()), mats + (size_t(i) * blocks + j) * dim * dim * 2,
+                  sizeof(Complex) * dim * dim);
+      c.mats[i].push_back(std::move(m));
+    }
+  if (power) c.power_scale.assign(power, power + bins);
+  return c;
+}
+
 }  // namespace
 
 extern "C" {
+
+// sample_covs(spec, block_size) (sigmodel.cpp:17-48): mats out
+// [bins][blocks][dim*dim] complex (nullable), power out [bins] (nullable).
+int oracle_block_covs(int bins, int dim, int frames, int block_size, const double* x,
+                      double* mats, double* power, char* err, int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet c = sample_covs(dim, bins, frames, cx(x), block_size, true);
+    for (int i = 0; i < bins; ++i) {
+      if (power) power[i] = c.power_scale[i];
+      if (mats)
+        for (int j = 0; j < c.blocks; ++j)
+          std::memcpy(static_cast<void*>(mats + (size_t(i) * c.blocks + j) * dim * dim * 2),
+                      c.mats[i][j].data(), sizeof(Complex) * dim * dim);
+    }
+  });
+}
+
+// fastfca_fit / ica_mode_fit on block covariances (the mats branches of
+// weighted_cov and decorrelated_powers); layouts as oracle_fit with frames =
+// blocks.  ica != 0: W in = w_init; L, H outputs; flavor etc. ignored.
+int oracle_fit_covs(int bins, int dim, int sources, int blocks, const double* mats,
+                    const double* power, double* W, double* L, double* H, int flavor, int iters,
+                    int record_trace, uint64_t seed, int normalize_scales, int fix_loadings,
+                    int workers, int ica, double* nll, double* nll_slots, char* err, int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet covs = covs_from_mats(bins, dim, blocks, mats, power);
+    FitOptions fo;
+    fo.workers = workers;
+    fo.record_trace = record_trace != 0;
+    fo.seed = seed;
+    std::vector<double> slots;
+    FastFcaFitResult r;
+    if (ica) {
+      std::vector<CMat> w_init(bins, CMat(dim, dim));
+      for (int i = 0; i < bins; ++i)
+        std::memcpy(static_cast<void*>(w_init[i].data()), W + size_t(i) * dim * dim * 2,
+                    sizeof(Complex) * dim * dim);
+      r = ica_mode_fit(covs, sources, iters, w_init, fo, nll_slots ? &slots : nullptr);
+    } else {
+      const FastFcaParams init = load_params(bins, dim, sources, blocks, W, L, H);
+      FastFcaOptions oo;
+      oo.normalize_scales = normalize_scales != 0;
+      oo.fix_loadings = fix_loadings != 0;
+      r = fastfca_fit(covs, init, flavor == 0 ? LhFlavor::em : LhFlavor::mm, iters, fo, oo,
+                      nll_slots ? &slots : nullptr);
+    }
+    store_params(r.params, W, L, H);
+    if (record_trace && nll)
+      for (int t = 0; t <= iters; ++t) nll[t] = r.nll[t];
+    if (record_trace && nll_slots)
+      std::memcpy(nll_slots, slots.data(), sizeof(double) * slots.size());
+  });
+}
+
+int oracle_nll_bins_covs(int bins, int dim, int sources, int blocks, const double* mats,
+                         const double* W, const double* L, const double* H, double* out,
+                         char* err, int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet covs = covs_from_mats(bins, dim, blocks, mats, nullptr);
+    const FastFcaParams p = load_params(bins, dim, sources, blocks, W, L, H);
+    for (int i = 0; i < bins; ++i)
+      out[i] = fastfca_nll_freq(covs, i, p.decorr[i], p.loading[i], p.act[i]);
+  });
+}
+
+int oracle_decorrelated_powers_covs(int bins, int dim, int blocks, const double* mats,
+                                    const double* W, double floor_rel, double* out, char* err,
+                                    int errlen) {
+  return guard(err, errlen, [&] {
+    const SampleCovSet covs = covs_from_mats(bins, dim, blocks, mats, nullptr);
+    for (int i = 0; i < bins; ++i) {
+      CMat w(dim, dim);
+      std::memcpy(static_cast<void*>(w.data()), W + size_t(i) * dim * dim * 2,
+                  sizeof(Complex) * dim * dim);
+      RMat u = decorrelated_powers(covs, i, w);
+      if (floor_rel >= 0.0) floor_positive(u, floor_rel);
+      std::memcpy(out + size_t(i) * dim * blocks, u.data(), sizeof(double) * dim * blocks);
+    }
+  });
+}
 
 int oracle_default_workers() { return default_workers(); }
 

@@ -28,6 +28,8 @@ EXPORTS = (
     "ffca_fit_device", "ffca_separate_device", "ffca_power_scale_device",
     "ffca_last_launch_count", "ffca_debug_set_timing", "ffca_ica_fit", "ffca_decorrelated_powers",
     "ffca_stft_frame_count", "ffca_stft", "ffca_istft", "ffca_stft_device", "ffca_istft_device",
+    "ffca_block_covs", "ffca_fit_covs", "ffca_ica_fit_covs", "ffca_nll_bins_covs",
+    "ffca_decorrelated_powers_covs", "ffca_block_covs_device", "ffca_fit_covs_device",
 )
 STFT_CENTERED, STFT_FULL_FRAMES = 0, 1
 
@@ -84,6 +86,17 @@ def lib() -> C.CDLL:
         L.ffca_power_scale.argtypes = [P, C.POINTER(Dims), P, P]
         L.ffca_ica_fit.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
         L.ffca_decorrelated_powers.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, C.c_double, P]
+        L.ffca_block_covs.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P]
+        L.ffca_fit_covs.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
+        L.ffca_ica_fit_covs.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts), P, P, P, P, P, P,
+                                        P, P]
+        L.ffca_nll_bins_covs.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, P, P, P]
+        L.ffca_decorrelated_powers_covs.argtypes = [P, C.POINTER(Dims), C.c_int, P, P, C.c_double,
+                                                    P]
+        L.ffca_block_covs_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                                             P, P]
+        L.ffca_fit_covs_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.POINTER(FitOpts), P, P, P, P, P, P, P, P]
         i, ll = C.c_int, C.c_longlong
         L.ffca_stft_frame_count.argtypes = [ll, i, i, i]
         L.ffca_stft_frame_count.restype = ll

@@ -75,28 +75,49 @@ class StftPadding:  # stft.hpp:30-37
     full_frames = 1
 
 
-@dataclass
-class SampleCovSet:  # sigmodel.hpp:48-56, block_size == 1 snapshot branch
-    snapshots: np.ndarray    # complex [bins, dim, frames]
-    power_scale: np.ndarray  # [bins]
-    block_size: int = 1
+class SampleCovSet:  # sigmodel.hpp:48-56
+    """Observation statistics.  block_size == 1: the snapshots (the hot path
+    reads them; the rank-one `mats` are not materialised).
+    block_size B > 1: mats [bins, blocks, dim, dim] complex, the B-frame block
+    covariances (sigmodel.cpp:34-41).  power_scale may be None for a
+    caller-built set: power(i) then falls back to the block traces
+    (sigmodel.cpp:50-55), computed on the GPU by the fit."""
+
+    def __init__(self, snapshots=None, power_scale=None, block_size: int = 1, mats=None,
+                 frames: int | None = None):
+        self.snapshots = None if snapshots is None else np.asarray(snapshots)
+        self.power_scale = None if power_scale is None else np.asarray(power_scale, np.float64)
+        self.block_size = int(block_size)
+        self.mats = None if mats is None else np.asarray(mats)
+        if self.snapshots is None and self.mats is None:
+            raise InvalidArgument("SampleCovSet: snapshots or mats required")
+        self._frames = frames
+
+    def has_snapshots(self) -> bool:
+        return self.snapshots is not None
 
     @property
     def dim(self) -> int:
-        return self.snapshots.shape[1]
+        return (self.snapshots if self.has_snapshots() else self.mats).shape[-2]
 
     @property
     def bins(self) -> int:
-        return self.snapshots.shape[0]
+        return (self.snapshots if self.has_snapshots() else self.mats).shape[0]
+
+    @property
+    def blocks(self) -> int:
+        return self.snapshots.shape[2] if self.has_snapshots() else self.mats.shape[1]
 
     @property
     def frames(self) -> int:
-        return self.snapshots.shape[2]
-
-    blocks = frames
+        return self._frames if self._frames is not None else self.blocks * (
+            1 if self.has_snapshots() else self.block_size)
 
     def power(self, i: int) -> float:
-        return float(self.power_scale[i])
+        if self.power_scale is not None and i < len(self.power_scale):
+            return float(self.power_scale[i])
+        tr = np.trace(self.mats[i], axis1=-2, axis2=-1).real.sum()
+        return float(tr / (self.blocks * self.dim))
 
 
 @dataclass
@@ -154,6 +175,21 @@ def _params_from_ref(W, L, H) -> FastFcaParams:
                          np.ascontiguousarray(np.swapaxes(H, -1, -2)))
 
 
+def _mats_ref(mats: np.ndarray) -> np.ndarray:
+    """[..., blocks, dim, dim] -> reference per-block Eigen col-major complex128."""
+    return np.ascontiguousarray(np.swapaxes(mats, -1, -2), dtype=np.complex128)
+
+
+def _covs_input(covs: SampleCovSet):
+    """(buffer, power or None, snapshot?) for the C-ABI fit entry points."""
+    pw = None if covs.power_scale is None else np.ascontiguousarray(covs.power_scale, np.float64)
+    if covs.has_snapshots():
+        if pw is None:
+            raise InvalidArgument("SampleCovSet: snapshots need power_scale")
+        return _x_ref(covs.snapshots), pw, True
+    return _mats_ref(covs.mats), pw, False
+
+
 def _prec(precision: str) -> int:
     if precision not in ("fp32", "fp64"):
         raise InvalidArgument(f"precision must be 'fp32' or 'fp64', not {precision!r}")
@@ -162,27 +198,49 @@ def _prec(precision: str) -> int:
 
 # ------------------------------------------------------------------- API --
 def sample_covs(spec: Spectrogram, block_size: int = 1, *, device: int | None = None) -> SampleCovSet:
-    """sigmodel.cpp:17-48 for block_size == 1 (snapshots + power_scale)."""
+    """sigmodel.cpp:17-48 on the GPU: block_size == 1 keeps the snapshots and
+    computes power_scale; block_size B > 1 computes the block covariances
+    (ceil(T/B) blocks, the last one ragged) and power_scale."""
     if spec.bins == 0 or spec.frames == 0 or spec.channels == 0:
         raise InvalidArgument("sample_covs: empty spectrogram")
     if block_size < 1:
         raise InvalidArgument("sample_covs: block size must be >= 1")
-    if block_size != 1:
-        raise InvalidArgument("sample_covs: block-stationary statistics (block_size > 1) are "
-                              "outside the GPU hot path (SURVEY §8(f) next #4)")
     x = _x_ref(spec.f)
     d = _lib.Dims(1, spec.bins, spec.channels, 1, spec.frames)
     out = np.empty(spec.bins)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().ffca_power_scale(ctx.handle, d, _lib.ptr(x), _lib.ptr(out)))
-    return SampleCovSet(np.asarray(spec.f, dtype=np.complex128), out)
+    if block_size == 1:
+        _lib.check(_lib.lib().ffca_power_scale(ctx.handle, d, _lib.ptr(x), _lib.ptr(out)))
+        return SampleCovSet(np.asarray(spec.f, dtype=np.complex128), out)
+    J = -(-spec.frames // block_size)
+    M = spec.channels
+    mats = np.empty((spec.bins, J, M, M), np.complex128)  # Eigen col-major per block
+    _lib.check(_lib.lib().ffca_block_covs(ctx.handle, d, int(block_size), _lib.ptr(x),
+                                          _lib.ptr(mats), _lib.ptr(out)))
+    return SampleCovSet(None, out, block_size, np.swapaxes(mats, -1, -2), frames=spec.frames)
+
+
+def piecewise_prepare(spec: Spectrogram, block_size: int, **kw) -> SampleCovSet:
+    """fastfca.cpp:266-268."""
+    return sample_covs(spec, block_size, **kw)
+
+
+def expand_block_params(params: "FastFcaParams", block_size: int, frames: int) -> "FastFcaParams":
+    """sigmodel.cpp:164-196: block-level H -> frame level (column j takes block
+    min(j // B, blocks - 1)).  A host-side index copy."""
+    if block_size == 1 and frames == params.frames:
+        return params
+    jb = np.minimum(np.arange(frames) // block_size, params.frames - 1)
+    return FastFcaParams(params.decorr.copy(), params.loading.copy(),
+                         np.ascontiguousarray(params.act[:, :, jb]))
 
 
 def _check_shape(covs: SampleCovSet, init: FastFcaParams, what: str) -> None:
-    if (init.dim != covs.dim or init.bins != covs.bins or init.frames != covs.frames
+    if (init.dim != covs.dim or init.bins != covs.bins or init.frames != covs.blocks
             or init.loading.shape[:2] != (covs.bins, covs.dim)
             or init.act.shape[:2] != (covs.bins, init.sources)):
         raise InvalidArgument(f"{what}: init/covariance shape mismatch")
+
 
 
 def fastfca_fit(covs: SampleCovSet, init: FastFcaParams, flavor: int, iters: int,
@@ -194,18 +252,18 @@ def fastfca_fit(covs: SampleCovSet, init: FastFcaParams, flavor: int, iters: int
     _check_shape(covs, init, "fastfca_fit")
     if iters < 0:
         raise InvalidArgument("fastfca_fit: negative iteration count")
-    x = _x_ref(covs.snapshots)
+    x, power, snap = _covs_input(covs)
     W, L, H = _params_ref(init)
     F = covs.bins
-    d = _lib.Dims(1, F, covs.dim, init.sources, covs.frames)
+    d = _lib.Dims(1, F, covs.dim, init.sources, covs.blocks)
     o = _lib.FitOpts(int(flavor), int(iters), int(bool(fit.record_trace)), int(fit.seed),
                      int(bool(opts.normalize_scales)), int(bool(opts.fix_loadings)),
                      _prec(precision))
     nll = np.zeros(iters + 1) if fit.record_trace else None
     status = np.zeros(F, np.int32)
-    power = np.ascontiguousarray(covs.power_scale, dtype=np.float64)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().ffca_fit(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power), _lib.ptr(W),
+    fn = _lib.lib().ffca_fit if snap else _lib.lib().ffca_fit_covs
+    _lib.check(fn(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power), _lib.ptr(W),
                                    _lib.ptr(L), _lib.ptr(H), _lib.ptr(nll), None,
                                    _lib.ptr(status)))
     return FastFcaFitResult(_params_from_ref(W, L, H), list(nll) if nll is not None else [],
@@ -225,8 +283,8 @@ def ica_mode_fit(covs: SampleCovSet, sources: int, iters: int, w_init: np.ndarra
         raise InvalidArgument("ica_mode_fit: one W per frequency required")
     if iters < 0:
         raise InvalidArgument("fastfca_fit: negative iteration count")
-    F, M, T = covs.bins, covs.dim, covs.frames
-    x = _x_ref(covs.snapshots)
+    F, M, T = covs.bins, covs.dim, covs.blocks
+    x, power, snap = _covs_input(covs)
     W = np.array(np.swapaxes(w_init, -1, -2), dtype=np.complex128, order="C", copy=True)
     L = np.zeros((F, M, M))
     H = np.zeros((F, T, M))
@@ -235,9 +293,9 @@ def ica_mode_fit(covs: SampleCovSet, sources: int, iters: int, w_init: np.ndarra
                      _prec(precision))
     nll = np.zeros(iters + 1) if fit.record_trace else None
     status = np.zeros(F, np.int32)
-    power = np.ascontiguousarray(covs.power_scale, dtype=np.float64)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().ffca_ica_fit(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power),
+    fn = _lib.lib().ffca_ica_fit if snap else _lib.lib().ffca_ica_fit_covs
+    _lib.check(fn(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power),
                                        _lib.ptr(W), _lib.ptr(L), _lib.ptr(H), _lib.ptr(nll), None,
                                        _lib.ptr(status)))
     return FastFcaFitResult(_params_from_ref(W, L, H), list(nll) if nll is not None else [],
@@ -249,13 +307,15 @@ def decorrelated_powers(covs: SampleCovSet, w: np.ndarray, *, floor_rel: float |
     """|W^H x|^2 for every bin (sigmodel.cpp:93-107), w [bins, dim, dim];
     floor_positive(u, floor_rel) (sigmodel.cpp:10-15) when floor_rel is given.
     Returns [bins, dim, frames]."""
-    F, M, T = covs.bins, covs.dim, covs.frames
-    x = _x_ref(covs.snapshots)
+    F, M, T = covs.bins, covs.dim, covs.blocks
+    x = _x_ref(covs.snapshots) if covs.has_snapshots() else _mats_ref(covs.mats)
     W = np.array(np.swapaxes(w, -1, -2), dtype=np.complex128, order="C", copy=True)
     out = np.empty((F, T, M))
     d = _lib.Dims(1, F, M, M, T)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().ffca_decorrelated_powers(
+    fn = (_lib.lib().ffca_decorrelated_powers if covs.has_snapshots()
+          else _lib.lib().ffca_decorrelated_powers_covs)
+    _lib.check(fn(
         ctx.handle, d, _prec(precision), _lib.ptr(x), _lib.ptr(W),
         -1.0 if floor_rel is None else float(floor_rel), _lib.ptr(out)))
     return np.ascontiguousarray(np.swapaxes(out, -1, -2))
@@ -325,12 +385,14 @@ def fastfca_nll_bins(covs: SampleCovSet, params: FastFcaParams, *, precision: st
                      device: int | None = None) -> np.ndarray:
     """fastfca_nll_freq for every bin (sigmodel.cpp:155-162)."""
     _check_shape(covs, params, "nll")
-    x = _x_ref(covs.snapshots)
+    snap = covs.has_snapshots()
+    x = _x_ref(covs.snapshots) if snap else _mats_ref(covs.mats)
     W, L, H = _params_ref(params)
     out = np.empty(covs.bins)
-    d = _lib.Dims(1, covs.bins, covs.dim, params.sources, covs.frames)
+    d = _lib.Dims(1, covs.bins, covs.dim, params.sources, covs.blocks)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().ffca_nll_bins(ctx.handle, d, _prec(precision), _lib.ptr(x),
+    fn = _lib.lib().ffca_nll_bins if snap else _lib.lib().ffca_nll_bins_covs
+    _lib.check(fn(ctx.handle, d, _prec(precision), _lib.ptr(x),
                                         _lib.ptr(W), _lib.ptr(L), _lib.ptr(H), _lib.ptr(out)))
     return out
 

@@ -137,21 +137,47 @@ int stage_inputs(ffca_ctx* ctx, size_t P, int M, int N, int T, const double* x, 
 // ica: ica_mode_fit (fastfca.cpp:241-264) -- H and L are outputs: L is the
 // identity, H the floored decorrelated powers of the W init, computed here
 // on the device; the fit then runs IP+MM with the loadings fixed.
+// Stage caller block covariances (complex128 [P][J][M*M] col-major) as packed
+// records in the compute type; power (may be null) receives the trace-based
+// SampleCovSet::power() of every problem.
+template <typename R>
+int stage_covs(ffca_ctx* ctx, size_t P, int M, int J, const double* mats, void** rec_out,
+               double* power, cudaStream_t st) {
+  cudaError_t err;
+  const size_t nm = P * J * M * M;
+  double* dm = static_cast<double*>(ctx->get(kX, nm * 16, &err));
+  R* rec = static_cast<R*>(ctx->get(kXs, nm * sizeof(R), &err));
+  if (!dm || !rec) return set_err(FFCA_CUDA_ERROR, "ffca: covariance alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dm, mats, nm * 16, cudaMemcpyHostToDevice, st));
+  pack_covs_kernel<R><<<int(P), 256, 0, st>>>(reinterpret_cast<const double2*>(dm), M, J, rec, power);
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  *rec_out = rec;
+  return FFCA_OK;
+}
+
+// blk: x is SampleCovSet::mats (complex128 [P][J][M*M] col-major, frames = J
+// blocks) -- the block-stationary input (fastfca.cpp:29-32, sigmodel.cpp:97-105).
 template <typename R>
 int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
              const double* power, double* W, double* L, double* H, double* nll,
-             double* nll_slots, int32_t* bin_status, bool ica = false) {
+             double* nll_slots, int32_t* bin_status, bool ica = false, bool blk = false) {
   const int P = d->batch * d->bins, M = d->dim, N = d->sources, T = d->frames;
   cudaStream_t st = ctx->stream;
   cudaError_t err;
   void* xs = nullptr;
   void* hs = nullptr;
   double* hd = nullptr;
-  int rc = stage_inputs<R>(ctx, P, M, N, T, x, ica ? nullptr : H, &xs, &hs, &hd, st);
+  int rc = stage_inputs<R>(ctx, P, M, N, T, blk ? nullptr : x, ica ? nullptr : H, &xs, &hs, &hd, st);
   if (rc) return rc;
   double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
   double* dL = static_cast<double*>(ctx->get(kL, size_t(P) * M * N * 8, &err));
   double* dpow = static_cast<double*>(ctx->get(kPow, size_t(P) * 8, &err));
+  if (!dpow) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  if (blk) {
+    rc = stage_covs<R>(ctx, P, M, T, x, &xs, power ? nullptr : dpow, st);
+    if (rc) return rc;
+  }
   const int iters = o->iters;
   const bool record = o->record_trace != 0;
   double* dnll = static_cast<double*>(ctx->get(kNll, size_t(iters + 1) * P * 8, &err));
@@ -166,9 +192,14 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
     hd = static_cast<double*>(ctx->get(kH, nh * 8, &err));
     hs = ctx->get(kHs, nh * sizeof(R), &err);
     if (!hd || !hs) return set_err(FFCA_CUDA_ERROR, "ffca: H alloc failed");
-    decorrelated_powers_kernel<R><<<P, 256, 0, st>>>(static_cast<const cplx_t<R>*>(xs),
-                                                      reinterpret_cast<const double2*>(dW), M, T,
-                                                      1e-12 /* kPowerFloorRel */, hd);
+    if (blk)
+      decorrelated_powers_blk_kernel<R><<<P, 256, 0, st>>>(
+          static_cast<const R*>(xs), reinterpret_cast<const double2*>(dW), M, T,
+          1e-12 /* kPowerFloorRel */, hd);
+    else
+      decorrelated_powers_kernel<R><<<P, 256, 0, st>>>(static_cast<const cplx_t<R>*>(xs),
+                                                        reinterpret_cast<const double2*>(dW), M, T,
+                                                        1e-12 /* kPowerFloorRel */, hd);
     ctx->launches++;
     FFCA_CUDA(cudaGetLastError());
     convert_kernel<double, R><<<grid_for(nh, 256), 256, 0, st>>>(hd, static_cast<R*>(hs), nh);
@@ -178,7 +209,7 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   FFCA_CUDA(cudaMemcpyAsync(dL, L, size_t(P) * M * N * 8, cudaMemcpyHostToDevice, st));
   if (power) {
     FFCA_CUDA(cudaMemcpyAsync(dpow, power, size_t(P) * 8, cudaMemcpyHostToDevice, st));
-  } else {
+  } else if (!blk) {
     power_kernel<double2><<<P, 256, 0, st>>>(static_cast<const double2*>(ctx->bufs[kX].p), dpow,
                                              M, T);
     ctx->launches++;
@@ -208,6 +239,7 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   fp.normalize = o->normalize_scales;
   fp.fix_loadings = o->fix_loadings;
   fp.seed = o->seed;
+  fp.blk = blk ? 1 : 0;
   rc = launch_fit<R>(ctx, M, fp, st);
   if (rc) return rc;
   std::vector<int> stat(P);
@@ -254,6 +286,47 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
       }
   }
   return FFCA_OK;
+}
+
+// ffca_fit / ffca_ica_fit and their block-covariance variants.
+int fit_entry(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
+              const double* power, double* W, double* L, double* H, double* nll,
+              double* nll_slots, int32_t* bin_status, bool ica, bool blk) {
+  const char* fn = ica ? "ffca_ica_fit" : "ffca_fit";
+  if (!ctx || !d || !o) return set_err(FFCA_INVALID_ARGUMENT, std::string(fn) + ": null argument");
+  if (d->batch < 1 || d->bins < 1)
+    return set_err(FFCA_INVALID_ARGUMENT, std::string(fn) + ": empty shape");
+  if (ica && d->sources != d->dim)  // fastfca.cpp:244-246
+    return set_err(FFCA_INVALID_ARGUMENT, "ica_mode_fit: requires as many sources as channels");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
+  if (rc) return rc;
+  if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
+  if (!ica && o->flavor != FFCA_FLAVOR_EM && o->flavor != FFCA_FLAVOR_MM)
+    return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: unknown flavor");
+  if (!x || !W || !L || !H) return set_err(FFCA_INVALID_ARGUMENT, std::string(fn) + ": null buffer");
+  if (o->record_trace && !nll && !nll_slots)
+    return set_err(FFCA_INVALID_ARGUMENT, std::string(fn) + ": record_trace needs an nll buffer");
+  ctx->launches = 0;
+  DeviceGuard g(ctx->device);
+  if (!ica) {
+    if (o->iters == 0 && !o->record_trace) {
+      if (bin_status) std::memset(bin_status, 0, sizeof(int32_t) * d->batch * d->bins);
+      return FFCA_OK;
+    }
+    if (o->precision == FFCA_PREC_FP64)
+      return fit_host<double>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, blk);
+    return fit_host<float>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, blk);
+  }
+  ffca_fit_opts m = *o;
+  m.flavor = FFCA_FLAVOR_MM;  // fastfca.cpp:262-263
+  m.fix_loadings = 1;
+  m.normalize_scales = 1;
+  // Always the fp64 kernels: at the determined-mode fixed point H tracks
+  // U = |w^H x|^2 and the 1/U weights amplify fp32 cancellation in w^H x
+  // (measured: the fp32 trajectory leaves the fp64 one by 5e-4 after 20
+  // iterations and the IP system then goes singular where the reference
+  // converges), so `precision` does not apply to this mode.
+  return fit_host<double>(ctx, d, &m, x, power, W, L, H, nll, nll_slots, bin_status, true, blk);
 }
 
 }  // namespace
@@ -308,52 +381,25 @@ int ffca_last_launch_count(const ffca_ctx* ctx) { return ctx ? ctx->launches : 0
 int ffca_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status) {
-  if (!ctx || !d || !o) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: null argument");
-  if (d->batch < 1 || d->bins < 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: empty shape");
-  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
-  if (rc) return rc;
-  if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
-  if (o->flavor != FFCA_FLAVOR_EM && o->flavor != FFCA_FLAVOR_MM)
-    return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: unknown flavor");
-  if (!x || !W || !L || !H) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: null buffer");
-  if (o->record_trace && !nll && !nll_slots)
-    return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit: record_trace needs an nll buffer");
-  ctx->launches = 0;
-  DeviceGuard g(ctx->device);
-  if (o->iters == 0 && !o->record_trace) {
-    if (bin_status) std::memset(bin_status, 0, sizeof(int32_t) * d->batch * d->bins);
-    return FFCA_OK;
-  }
-  if (o->precision == FFCA_PREC_FP64)
-    return fit_host<double>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status);
-  return fit_host<float>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status);
+  return fit_entry(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, false);
+}
+
+int ffca_fit_covs(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* mats,
+                  const double* power, double* W, double* L, double* H, double* nll,
+                  double* nll_slots, int32_t* bin_status) {
+  return fit_entry(ctx, d, o, mats, power, W, L, H, nll, nll_slots, bin_status, false, true);
 }
 
 int ffca_ica_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
                  const double* power, double* W, double* L, double* H, double* nll,
                  double* nll_slots, int32_t* bin_status) {
-  if (!ctx || !d || !o) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: null argument");
-  if (d->batch < 1 || d->bins < 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: empty shape");
-  if (d->sources != d->dim)  // fastfca.cpp:244-246
-    return set_err(FFCA_INVALID_ARGUMENT, "ica_mode_fit: requires as many sources as channels");
-  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
-  if (rc) return rc;
-  if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
-  if (!x || !W || !L || !H) return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: null buffer");
-  if (o->record_trace && !nll && !nll_slots)
-    return set_err(FFCA_INVALID_ARGUMENT, "ffca_ica_fit: record_trace needs an nll buffer");
-  ctx->launches = 0;
-  DeviceGuard g(ctx->device);
-  ffca_fit_opts m = *o;
-  m.flavor = FFCA_FLAVOR_MM;  // fastfca.cpp:262-263
-  m.fix_loadings = 1;
-  m.normalize_scales = 1;
-  // Always the fp64 kernels: at the determined-mode fixed point H tracks
-  // U = |w^H x|^2 and the 1/U weights amplify fp32 cancellation in w^H x
-  // (measured: the fp32 trajectory leaves the fp64 one by 5e-4 after 20
-  // iterations and the IP system then goes singular where the reference
-  // converges), so `precision` does not apply to this mode.
-  return fit_host<double>(ctx, d, &m, x, power, W, L, H, nll, nll_slots, bin_status, true);
+  return fit_entry(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, true, false);
+}
+
+int ffca_ica_fit_covs(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o,
+                      const double* mats, const double* power, double* W, double* L, double* H,
+                      double* nll, double* nll_slots, int32_t* bin_status) {
+  return fit_entry(ctx, d, o, mats, power, W, L, H, nll, nll_slots, bin_status, true, true);
 }
 
 int ffca_decorrelated_powers(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,
@@ -394,8 +440,9 @@ int ffca_decorrelated_powers(ffca_ctx* ctx, const ffca_dims* d, int precision, c
   return FFCA_OK;
 }
 
-int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,
-                  const double* W, const double* L, const double* H, double* out) {
+static int nll_bins_entry(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,
+                          const double* W, const double* L, const double* H, double* out,
+                          bool blk) {
   if (!ctx || !d || !x || !W || !L || !H || !out)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_nll_bins: null argument");
   int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
@@ -415,11 +462,85 @@ int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
   DeviceGuard g(ctx->device);
   rc = (precision == FFCA_PREC_FP64)
            ? fit_host<double>(ctx, &one, &o, x, nullptr, w.data(), l.data(), h.data(), nullptr,
-                              slots.data(), nullptr)
+                              slots.data(), nullptr, false, blk)
            : fit_host<float>(ctx, &one, &o, x, nullptr, w.data(), l.data(), h.data(), nullptr,
-                             slots.data(), nullptr);
+                             slots.data(), nullptr, false, blk);
   if (rc) return rc;
   std::memcpy(out, slots.data(), sizeof(double) * P);
+  return FFCA_OK;
+}
+
+int ffca_nll_bins(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* x,
+                  const double* W, const double* L, const double* H, double* out) {
+  return nll_bins_entry(ctx, d, precision, x, W, L, H, out, false);
+}
+
+int ffca_nll_bins_covs(ffca_ctx* ctx, const ffca_dims* d, int precision, const double* mats,
+                       const double* W, const double* L, const double* H, double* out) {
+  return nll_bins_entry(ctx, d, precision, mats, W, L, H, out, true);
+}
+
+int ffca_decorrelated_powers_covs(ffca_ctx* ctx, const ffca_dims* d, int precision,
+                                  const double* mats, const double* W, double floor_rel,
+                                  double* out) {
+  if (!ctx || !d || !mats || !W || !out)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_decorrelated_powers: null argument");
+  if (d->batch < 1 || d->bins < 1)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_decorrelated_powers: empty shape");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->dim, d->frames);
+  if (rc) return rc;
+  ctx->launches = 0;
+  DeviceGuard g(ctx->device);
+  const int P = d->batch * d->bins, M = d->dim, J = d->frames;
+  cudaStream_t st = ctx->stream;
+  cudaError_t err;
+  double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
+  double* dout = static_cast<double*>(ctx->get(kH, size_t(P) * J * M * 8, &err));
+  if (!dW || !dout) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dW, W, size_t(P) * M * M * 16, cudaMemcpyHostToDevice, st));
+  void* rec = nullptr;
+  if (precision == FFCA_PREC_FP64) {
+    rc = stage_covs<double>(ctx, P, M, J, mats, &rec, nullptr, st);
+    if (rc) return rc;
+    decorrelated_powers_blk_kernel<double><<<P, 256, 0, st>>>(
+        static_cast<const double*>(rec), reinterpret_cast<const double2*>(dW), M, J, floor_rel, dout);
+  } else {
+    rc = stage_covs<float>(ctx, P, M, J, mats, &rec, nullptr, st);
+    if (rc) return rc;
+    decorrelated_powers_blk_kernel<float><<<P, 256, 0, st>>>(
+        static_cast<const float*>(rec), reinterpret_cast<const double2*>(dW), M, J, floor_rel, dout);
+  }
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  FFCA_CUDA(cudaMemcpyAsync(out, dout, size_t(P) * J * M * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  return FFCA_OK;
+}
+
+int ffca_block_covs(ffca_ctx* ctx, const ffca_dims* d, int block_size, const double* x,
+                    double* mats, double* power) {
+  if (!ctx || !d || !x) return set_err(FFCA_INVALID_ARGUMENT, "ffca_block_covs: null argument");
+  const long long P = (long long)d->batch * d->bins;
+  const int M = d->dim, T = d->frames;
+  if (P < 1 || M < 1 || T < 1) return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: empty spectrogram");
+  if (block_size < 1) return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: block size must be >= 1");
+  if (M > 8) return set_err(FFCA_INVALID_ARGUMENT, "ffca: dim > 8 is not supported");
+  const int J = (T + block_size - 1) / block_size;
+  DeviceGuard g(ctx->device);
+  ctx->launches = 0;
+  cudaStream_t st = ctx->stream;
+  cudaError_t err;
+  double2* dx = static_cast<double2*>(ctx->get(kX, size_t(P) * T * M * 16, &err));
+  double2* dm = mats ? static_cast<double2*>(ctx->get(kImg, size_t(P) * J * M * M * 16, &err)) : nullptr;
+  double* dp = power ? static_cast<double*>(ctx->get(kPow, size_t(P) * 8, &err)) : nullptr;
+  if (!dx || (mats && !dm) || (power && !dp)) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dx, x, size_t(P) * T * M * 16, cudaMemcpyHostToDevice, st));
+  block_covs_kernel<double2, double><<<int(P), 256, 0, st>>>(dx, M, T, block_size, J, nullptr, dm, dp);
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  if (mats) FFCA_CUDA(cudaMemcpyAsync(mats, dm, size_t(P) * J * M * M * 16, cudaMemcpyDeviceToHost, st));
+  if (power) FFCA_CUDA(cudaMemcpyAsync(power, dp, size_t(P) * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
   return FFCA_OK;
 }
 
@@ -476,10 +597,11 @@ int ffca_separate(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
   return FFCA_OK;
 }
 
-int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset, int dim,
-                    int sources, int frames, const ffca_fit_opts* o, const void* x_dev,
-                    const double* power, double* W, double* L, void* H_dev, double* nll_slots,
-                    int32_t* status, void* stream) {
+static int fit_device_entry(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset,
+                            int dim, int sources, int frames, const ffca_fit_opts* o,
+                            const void* x_dev, const double* power, double* W, double* L,
+                            void* H_dev, double* nll_slots, int32_t* status, void* stream,
+                            bool blk) {
   if (!ctx || !o || !x_dev || !power || !W || !L || !H_dev || !status)
     return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_device: null argument");
   int rc = check_dims(problems, dim, sources, frames);
@@ -512,9 +634,51 @@ int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_
   fp.fix_loadings = o->fix_loadings;
   fp.seed = o->seed;
   fp.timing = ctx->timing;
+  fp.blk = blk ? 1 : 0;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   return o->precision == FFCA_PREC_FP64 ? launch_fit<double>(ctx, dim, fp, st)
                                         : launch_fit<float>(ctx, dim, fp, st);
+}
+
+int ffca_fit_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset, int dim,
+                    int sources, int frames, const ffca_fit_opts* o, const void* x_dev,
+                    const double* power, double* W, double* L, void* H_dev, double* nll_slots,
+                    int32_t* status, void* stream) {
+  return fit_device_entry(ctx, problems, bins_per_mixture, prob_offset, dim, sources, frames, o,
+                          x_dev, power, W, L, H_dev, nll_slots, status, stream, false);
+}
+
+int ffca_fit_covs_device(ffca_ctx* ctx, int problems, int bins_per_mixture, int prob_offset,
+                         int dim, int sources, int blocks, const ffca_fit_opts* o,
+                         const void* rec_dev, const double* power, double* W, double* L,
+                         void* H_dev, double* nll_slots, int32_t* status, void* stream) {
+  return fit_device_entry(ctx, problems, bins_per_mixture, prob_offset, dim, sources, blocks, o,
+                          rec_dev, power, W, L, H_dev, nll_slots, status, stream, true);
+}
+
+int ffca_block_covs_device(ffca_ctx* ctx, int problems, int dim, int frames, int block_size,
+                           int precision, const void* x_dev, void* rec_dev, double* power,
+                           void* stream) {
+  if (!ctx || !x_dev || !rec_dev) return set_err(FFCA_INVALID_ARGUMENT, "ffca_block_covs_device: null");
+  if (problems < 1 || dim < 1 || frames < 1)
+    return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: empty spectrogram");
+  if (block_size < 1) return set_err(FFCA_INVALID_ARGUMENT, "sample_covs: block size must be >= 1");
+  if (dim > 8) return set_err(FFCA_INVALID_ARGUMENT, "ffca: dim > 8 is not supported");
+  DeviceGuard g(ctx->device);
+  ctx->launches = 0;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  const int J = (frames + block_size - 1) / block_size;
+  if (precision == FFCA_PREC_FP64)
+    block_covs_kernel<double2, double><<<problems, 256, 0, st>>>(
+        static_cast<const double2*>(x_dev), dim, frames, block_size, J,
+        static_cast<double*>(rec_dev), nullptr, power);
+  else
+    block_covs_kernel<float2, float><<<problems, 256, 0, st>>>(
+        static_cast<const float2*>(x_dev), dim, frames, block_size, J,
+        static_cast<float*>(rec_dev), nullptr, power);
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  return FFCA_OK;
 }
 
 int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int frames,

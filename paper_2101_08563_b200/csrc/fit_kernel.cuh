@@ -9,6 +9,13 @@
 //
 // Data layout (frame-major records, the reference's own per-bin order):
 //   x   [t][m]  complex   (Spectrogram::f[i] column-major, stft.hpp:21-29)
+//       or, block-stationary input (BLK, block_size > 1, sigmodel.cpp:34-41):
+//   X   [j][M*M] real     packed Hermitian block covariance of block j:
+//                         [a*M+a] = X_aa, [a*M+c] = Re X_ac, [c*M+a] = Im X_ac
+//                         (a < c) -- exactly the outer-product layout pass A
+//                         forms from a snapshot, so Q accumulates it directly
+//                         (fastfca.cpp:29-32) and U = max(0, w^H X w)
+//                         (sigmodel.cpp:98-105).
 //   H   [t][n]  real      (FastFcaParams::act[i] column-major, sigmodel.hpp:76)
 //   wk  [t][2M] real      U(m) = |w_m^H x_t|^2, then Phi(m) of the current source
 // so one thread reads a frame's record with a few vector loads.
@@ -63,6 +70,7 @@ struct FitParams {
   int iters, flavor, record, normalize, fix_loadings, resident;
   int nc;           // MM: sources per L-reduction chunk
   int tloc;         // frames held per CTA (= T, or ceil(T/C) for a C-CTA cluster)
+  int blk;          // x holds packed block covariances [nprob][T][M*M] (T = blocks)
   unsigned long long* timing;  // optional per-problem phase cycle counters [nprob][16]
   unsigned long long seed;
 };
@@ -104,8 +112,9 @@ struct MmChunk {
 };
 
 // Shared-memory carve-up, identical on host and device.
-template <int M, int NT, typename R>
+template <int M, int NT, typename R, bool BLK = false>
 struct FitSmem {
+  static constexpr int XR = BLK ? M * M : 2 * M;  // reals per x record
   int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
       off_us, off_hsum,
       off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_wsm, off_scal, off_big,
@@ -159,7 +168,7 @@ struct FitSmem {
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
     if (resident)
-      o = al(al(al(o + T * 2 * M * (int)sizeof(R)) + T * N * (int)sizeof(R)) +
+      o = al(al(al(o + T * XR * (int)sizeof(R)) + T * N * (int)sizeof(R)) +
              T * 2 * M * (int)sizeof(R));
     total = o;
   }
@@ -238,11 +247,13 @@ struct Uniform {
 // RES: the bin's records live in shared memory (compile-time, so the record
 // accesses are LDS/STS rather than generic loads); !RES streams them from
 // global memory (bins beyond a 16-CTA cluster).
-template <int M, int NT, bool EXACT, typename R, bool CL, bool RES>
+// BLK: the records are packed block covariances (block-stationary input).
+template <int M, int NT, bool EXACT, typename R, bool CL, bool RES, bool BLK = false>
 __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kernel(FitParams p) {
   using C = cplx_t<R>;
   using S = Split<M>;
-  constexpr int XR = 2 * M;  // reals per x record
+  using Lay = FitSmem<M, NT, R, BLK>;
+  constexpr int XR = Lay::XR;  // reals per x record
   constexpr int WR = 2 * M;  // reals per work record: U[M], Phi[M]
   constexpr bool HOIST = (M * NT <= 32);
   constexpr int FU = FFCA_FRAMES_IN_FLIGHT;  // frames per loop trip (ILP vs registers)
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const int t0g = int((long long)T * crank / csize);  // this CTA's frames [t0g, t0g + Tl)
   const int Tl = int((long long)T * (crank + 1) / csize) - t0g;
   const bool lead = crank == 0;  // writes the per-bin outputs
-  const FitSmem<M, NT, R> lay(nwarps, N, p.tloc, p.nc, RES);
+  const Lay lay(nwarps, N, p.tloc, p.nc, RES);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
   // Per-bin scalar algebra (L master, balance scales, sweep updates) runs in
@@ -333,15 +344,17 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   R* wk;
   if constexpr (RES) {
     const int ox = lay.off_big;
-    const int oh = FitSmem<M, NT, R>::al(ox + p.tloc * XR * (int)sizeof(R));
-    const int ow = FitSmem<M, NT, R>::al(oh + p.tloc * N * (int)sizeof(R));
+    const int oh = Lay::al(ox + p.tloc * XR * (int)sizeof(R));
+    const int ow = Lay::al(oh + p.tloc * N * (int)sizeof(R));
     R* xsm = reinterpret_cast<R*>(smem + ox);
     Hs = reinterpret_cast<R*>(smem + oh);
     wk = reinterpret_cast<R*>(smem + ow);
-    {
+    if constexpr (XR % 2 == 0) {
       const C* src = reinterpret_cast<const C*>(xg);
       C* dst = reinterpret_cast<C*>(xsm);
-      for (int k = tid; k < M * Tl; k += nthreads) dst[k] = src[k];
+      for (int k = tid; k < (XR / 2) * Tl; k += nthreads) dst[k] = src[k];
+    } else {  // odd M under BLK: records are not 8-byte aligned
+      for (int k = tid; k < XR * Tl; k += nthreads) xsm[k] = xg[k];
     }
     for (int k = tid; k < N * Tl; k += nthreads) Hs[k] = Hg[k];
     xs = xsm;
@@ -407,19 +420,39 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     }
   };
 
-  // y = W^H x and U = |y|^2 of one frame.
+  // y = W^H x and U = |y|^2 of one frame; BLK: U = max(0, w_m^H X w_m) of
+  // one block from the packed Hermitian record (sigmodel.cpp:98-105).
   auto decorrelate = [&](const WU& w, const R (&xv)[XR], R (&u)[M]) {
+    if constexpr (BLK) {
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      R yr = w[2 * m * M] * xv[0] + w[2 * m * M + 1] * xv[1];
-      R yi = w[2 * m * M] * xv[1] - w[2 * m * M + 1] * xv[0];
+      for (int m = 0; m < M; ++m) {
+        R acc = R(0);
 #pragma unroll
-      for (int c = 1; c < M; ++c) {
-        const R wx = w[2 * (c + m * M)], wy = w[2 * (c + m * M) + 1];
-        yr += wx * xv[2 * c] + wy * xv[2 * c + 1];
-        yi += wx * xv[2 * c + 1] - wy * xv[2 * c];
+        for (int a = 0; a < M; ++a) {
+          const R ar = w[2 * (a + m * M)], ai = w[2 * (a + m * M) + 1];
+          acc += (ar * ar + ai * ai) * xv[a * M + a];
+#pragma unroll
+          for (int c = a + 1; c < M; ++c) {
+            const R cr = w[2 * (c + m * M)], ci = w[2 * (c + m * M) + 1];
+            // 2 Re(conj(w_a) X_ac w_c), conj(w_a) w_c = (ar cr + ai ci) + i (ar ci - ai cr)
+            acc += R(2) * ((ar * cr + ai * ci) * xv[a * M + c] - (ar * ci - ai * cr) * xv[c * M + a]);
+          }
+        }
+        u[m] = acc > R(0) ? acc : R(0);
       }
-      u[m] = yr * yr + yi * yi;
+    } else {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        R yr = w[2 * m * M] * xv[0] + w[2 * m * M + 1] * xv[1];
+        R yi = w[2 * m * M] * xv[1] - w[2 * m * M + 1] * xv[0];
+#pragma unroll
+        for (int c = 1; c < M; ++c) {
+          const R wx = w[2 * (c + m * M)], wy = w[2 * (c + m * M) + 1];
+          yr += wx * xv[2 * c] + wy * xv[2 * c + 1];
+          yi += wx * xv[2 * c + 1] - wy * xv[2 * c];
+        }
+        u[m] = yr * yr + yi * yi;
+      }
     }
   };
 
@@ -496,7 +529,12 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       for (int f = 0; f < FU; ++f) {
         if (!ok[f]) continue;
         R P[M * M];
-        if (want_q) {
+        if constexpr (BLK) {
+          if (want_q) {
+#pragma unroll
+            for (int k = 0; k < M * M; ++k) P[k] = xv[f][k];
+          }
+        } else if (want_q) {
 #pragma unroll
           for (int a = 0; a < M; ++a) {
             P[a * M + a] = xv[f][2 * a] * xv[f][2 * a] + xv[f][2 * a + 1] * xv[f][2 * a + 1];

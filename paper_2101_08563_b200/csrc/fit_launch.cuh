@@ -17,7 +17,7 @@
 
 namespace ffca {
 
-template <int M, int NT, bool EXACT, typename R, bool CL, bool RES>
+template <int M, int NT, bool EXACT, typename R, bool CL, bool RES, bool BLK = false>
 int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev_max) {
   int threads = fit_threads(M, fp.tloc, Launch<M>::threads);
   if (const char* e = getenv("FFCA_FIT_THREADS")) {  // tuning experiments only
@@ -26,10 +26,10 @@ int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev
     if (v >= per && v <= Launch<M>::threads && v % per == 0) threads = v;
   }
   const int nwarps = threads / 32;
-  const FitSmem<M, NT, R> lay(nwarps, fp.N, fp.tloc, fp.nc, RES);
+  const FitSmem<M, NT, R, BLK> lay(nwarps, fp.N, fp.tloc, fp.nc, RES);
   if (lay.total > dev_max)
     return ffca_set_err(FFCA_CUDA_ERROR, "ffca: fit kernel shared memory exceeds the device limit");
-  auto kern = fit_kernel<M, NT, EXACT, R, CL, RES>;
+  auto kern = fit_kernel<M, NT, EXACT, R, CL, RES, BLK>;
   FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
   if constexpr (CL) {
     if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -56,24 +56,26 @@ int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev
 
 // Cluster size for a bin: the smallest C in {1, 2, 4, 8, 16} whose per-CTA
 // frame range fits the shared-memory budget; 0 when even 16 does not.
-template <int M, int NT, typename R>
+template <int M, int NT, typename R, bool BLK = false>
 int pick_cluster(const FitParams& fp, int budget) {
   for (int C = 1; C <= 16; C *= 2) {
     const int tloc = (fp.T + C - 1) / C;
     const int nwarps = fit_threads(M, tloc, Launch<M>::threads) / 32;
-    if (FitSmem<M, NT, R>(nwarps, fp.N, tloc, fp.nc, true).total <= budget) return C;
+    if (FitSmem<M, NT, R, BLK>(nwarps, fp.N, tloc, fp.nc, true).total <= budget) return C;
   }
   return 0;
 }
 
-template <int M, int NT, bool EXACT, typename R>
+// BLK (block-covariance records): one CTA per bin when the bin fits, else
+// streaming (no cluster variants).
+template <int M, int NT, bool EXACT, typename R, bool BLK = false>
 int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   fp.nc = MmChunk<M, NT>::value;
   int dev_max = 0;
   cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   if (dev_max <= 0) dev_max = 227 * 1024;
   const int budget = dev_max - 2048;
-  int C = pick_cluster<M, NT, R>(fp, budget);
+  int C = pick_cluster<M, NT, R, BLK>(fp, budget);
   if (const char* e = getenv("FFCA_FORCE_CLUSTER")) {  // tuning experiments only
     const int f = atoi(e);
     if (!EXACT && f > C && f <= 16) C = f;
@@ -82,10 +84,10 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   if (C == 1) {
     fp.resident = 1;
     fp.tloc = fp.T;
-    return launch_fit_cfg<M, NT, EXACT, R, false, true>(ctx, fp, st, 1, dev_max);
+    return launch_fit_cfg<M, NT, EXACT, R, false, true, BLK>(ctx, fp, st, 1, dev_max);
   }
   if (C > 1) {
-    if constexpr (!EXACT) {
+    if constexpr (!EXACT && !BLK) {
       fp.resident = 1;
       fp.tloc = (fp.T + C - 1) / C;
       return launch_fit_cfg<M, NT, EXACT, R, true, true>(ctx, fp, st, C, dev_max);
@@ -99,7 +101,7 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
     fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
     if (!fp.work)
       return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
-    return launch_fit_cfg<M, NT, EXACT, R, false, false>(ctx, fp, st, 1, dev_max);
+    return launch_fit_cfg<M, NT, EXACT, R, false, false, BLK>(ctx, fp, st, 1, dev_max);
   } else {
     (void)err;
     return ffca_set_err(FFCA_CUDA_ERROR, "ffca: internal: exact-N variant selected for a large bin");
@@ -115,6 +117,10 @@ bool needs_cluster(const FitParams& fp) {
 
 template <int M>
 int launch_fit_f32(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
+  if (fp.blk) {
+    if (fp.N <= 4) return launch_fit_t<M, 4, false, float, true>(ctx, fp, st);
+    return launch_fit_t<M, 16, false, float, true>(ctx, fp, st);
+  }
   if constexpr (M <= 4) {
     if (!needs_cluster<M, float>(fp) && !getenv("FFCA_FORCE_CLUSTER")) {
       // Exact source-count specializations for the common shapes.
@@ -135,6 +141,10 @@ int launch_fit_f32(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
 
 template <int M>
 int launch_fit_f64(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
+  if (fp.blk) {
+    if (fp.N <= 4) return launch_fit_t<M, 4, false, double, true>(ctx, fp, st);
+    return launch_fit_t<M, 16, false, double, true>(ctx, fp, st);
+  }
   if (fp.N <= 4) return launch_fit_t<M, 4, false, double>(ctx, fp, st);
   return launch_fit_t<M, 16, false, double>(ctx, fp, st);
 }

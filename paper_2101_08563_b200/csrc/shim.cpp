@@ -50,21 +50,35 @@ int prec(const GpuOptions& g) {
 }
 
 // Contiguous host copies of bins [lo, hi) in the ABI's (reference) layout.
+// x: the snapshots [bin][frame][dim], or for a block set (no snapshots) the
+// block covariances [bin][block][dim*dim] (ffca.h *_covs entry points).
+// power: power_scale, or empty for a block set without one (the library
+// then takes SampleCovSet::power()'s trace fallback, sigmodel.cpp:50-55).
 struct Packed {
   std::vector<double> x, power, W, L, H;
+  bool snap = true;
+  const double* pw() const { return power.empty() ? nullptr : power.data(); }
 };
 
 void pack_bins(const SampleCovSet& covs, const FastFcaParams& p, int lo, int hi, Packed& out) {
   const int M = covs.dim, N = p.sources, T = covs.blocks, n = hi - lo;
-  out.x.resize(size_t(n) * T * M * 2);
-  out.power.resize(n);
+  out.snap = covs.has_snapshots();
+  const size_t rec = out.snap ? size_t(M) * 2 : size_t(M) * M * 2;  // doubles per frame / block
+  const bool has_pw = long(covs.power_scale.size()) == covs.bins;
+  out.x.resize(size_t(n) * T * rec);
+  out.power.resize(has_pw ? n : 0);
   out.W.resize(size_t(n) * M * M * 2);
   out.L.resize(size_t(n) * M * N);
   out.H.resize(size_t(n) * N * T);
   for (int i = lo; i < hi; ++i) {
     const size_t k = size_t(i - lo);
-    std::memcpy(out.x.data() + k * T * M * 2, covs.snapshots[i].data(), sizeof(double) * T * M * 2);
-    out.power[k] = covs.power(i);
+    if (out.snap) {
+      std::memcpy(out.x.data() + k * T * rec, covs.snapshots[i].data(), sizeof(double) * T * rec);
+    } else {
+      for (int j = 0; j < T; ++j)
+        std::memcpy(out.x.data() + (k * T + j) * rec, covs.mats[i][j].data(), sizeof(double) * rec);
+    }
+    if (has_pw) out.power[k] = covs.power_scale(i);
     std::memcpy(out.W.data() + k * M * M * 2, p.decorr[i].data(), sizeof(double) * M * M * 2);
     std::memcpy(out.L.data() + k * M * N, p.loading[i].data(), sizeof(double) * M * N);
     std::memcpy(out.H.data() + k * N * T, p.act[i].data(), sizeof(double) * N * T);
@@ -81,21 +95,39 @@ void unpack_bins(const Packed& in, int lo, int hi, FastFcaParams& p) {
   }
 }
 
+// A set the kernels can read: snapshots (dim x blocks each) with power_scale,
+// or block covariances mats[i][jb] (dim x dim) with power_scale or none.
+void check_covs(const SampleCovSet& covs, const char* what) {
+  const std::string bad = std::string(what) + ": malformed covariance set";
+  if (covs.has_snapshots()) {
+    if (int(covs.snapshots.size()) != covs.bins || long(covs.power_scale.size()) != covs.bins)
+      throw std::invalid_argument(bad);
+    for (const CMat& x : covs.snapshots)
+      if (x.rows() != covs.dim || x.cols() != covs.blocks) throw std::invalid_argument(bad);
+    return;
+  }
+  if (int(covs.mats.size()) != covs.bins ||
+      (covs.power_scale.size() != 0 && long(covs.power_scale.size()) != covs.bins))
+    throw std::invalid_argument(bad);
+  for (const auto& mi : covs.mats) {
+    if (int(mi.size()) != covs.blocks) throw std::invalid_argument(bad);
+    for (const CMat& m : mi)
+      if (m.rows() != covs.dim || m.cols() != covs.dim) throw std::invalid_argument(bad);
+  }
+}
+
 void check_fit_shapes(const SampleCovSet& covs, const FastFcaParams& init) {
   // fastfca.cpp:150-152
   if (init.dim != covs.dim || init.bins != covs.bins || init.frames != covs.blocks)
     throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
-  if (!covs.has_snapshots() || int(covs.snapshots.size()) != covs.bins ||
-      covs.power_scale.size() != covs.bins)
-    throw std::invalid_argument("fastfca_fit: covariance set has no snapshots (block_size > 1)");
+  check_covs(covs, "fastfca_fit");
   if (int(init.decorr.size()) != init.bins || int(init.loading.size()) != init.bins ||
       int(init.act.size()) != init.bins)
     throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
   for (int i = 0; i < init.bins; ++i)
     if (init.decorr[i].rows() != init.dim || init.decorr[i].cols() != init.dim ||
         init.loading[i].rows() != init.dim || init.loading[i].cols() != init.sources ||
-        init.act[i].rows() != init.sources || init.act[i].cols() != init.frames ||
-        covs.snapshots[i].rows() != covs.dim || covs.snapshots[i].cols() != covs.blocks)
+        init.act[i].rows() != init.sources || init.act[i].cols() != init.frames)
       throw std::invalid_argument("fastfca_fit: init/covariance shape mismatch");
 }
 
@@ -201,37 +233,67 @@ SampleCovSet sample_covs(const Spectrogram& spec, int block_size) {
   if (spec.bins == 0 || spec.frames == 0 || spec.channels == 0)
     throw std::invalid_argument("sample_covs: empty spectrogram");
   if (block_size < 1) throw std::invalid_argument("sample_covs: block size must be >= 1");
-  if (block_size != 1)
-    throw std::invalid_argument(
-        "sample_covs: block-stationary statistics (block_size > 1) are outside the GPU path");
+  const int M = spec.channels, F = spec.bins, T = spec.frames;
   SampleCovSet covs;
-  covs.dim = spec.channels;
-  covs.bins = spec.bins;
-  covs.frames = spec.frames;
-  covs.blocks = spec.frames;
-  covs.block_size = 1;
-  covs.snapshots = spec.f;
-  std::vector<double> x(size_t(spec.bins) * spec.frames * spec.channels * 2);
-  for (int i = 0; i < spec.bins; ++i)
-    std::memcpy(x.data() + size_t(i) * spec.frames * spec.channels * 2, spec.f[i].data(),
-                sizeof(double) * spec.frames * spec.channels * 2);
-  std::vector<double> pw(spec.bins);
-  ffca_dims d{1, spec.bins, spec.channels, 1, spec.frames, 0, 0};
-  raise(ffca_power_scale(context(0), &d, x.data(), pw.data()));
-  covs.power_scale = RVec::Zero(spec.bins);
-  for (int i = 0; i < spec.bins; ++i) covs.power_scale(i) = pw[i];
+  covs.dim = M;
+  covs.bins = F;
+  covs.frames = T;
+  covs.block_size = block_size;
+  covs.blocks = (T + block_size - 1) / block_size;
+  std::vector<double> x(size_t(F) * T * M * 2);
+  for (int i = 0; i < F; ++i)
+    std::memcpy(x.data() + size_t(i) * T * M * 2, spec.f[i].data(), sizeof(double) * T * M * 2);
+  std::vector<double> pw(F);
+  ffca_dims d{1, F, M, 1, T, 0, 0};
+  if (block_size == 1) {
+    covs.snapshots = spec.f;
+    raise(ffca_power_scale(context(0), &d, x.data(), pw.data()));
+  } else {
+    const int J = covs.blocks;
+    std::vector<double> mats(size_t(F) * J * M * M * 2);
+    raise(ffca_block_covs(context(0), &d, block_size, x.data(), mats.data(), pw.data()));
+    covs.mats.assign(F, std::vector<CMat>(J, CMat::Zero(M, M)));
+    for (int i = 0; i < F; ++i)
+      for (int j = 0; j < J; ++j)
+        std::memcpy(static_cast<void*>(covs.mats[i][j].data()),
+                    mats.data() + (size_t(i) * J + j) * M * M * 2, sizeof(double) * M * M * 2);
+  }
+  covs.power_scale = RVec::Zero(F);
+  for (int i = 0; i < F; ++i) covs.power_scale(i) = pw[i];
   return covs;
+}
+
+SampleCovSet piecewise_prepare(const Spectrogram& spec, int block_size) {
+  return sample_covs(spec, block_size);  // fastfca.cpp:266-268
+}
+
+FastFcaParams expand_block_params(const FastFcaParams& params, int block_size, int frames) {
+  if (block_size == 1 && frames == params.frames) return params;  // sigmodel.cpp:190
+  FastFcaParams out = params;
+  out.frames = frames;
+  for (int i = 0; i < params.bins; ++i) {
+    const RMat& h = params.act[i];
+    RMat e = RMat::Zero(h.rows(), frames);
+    for (int j = 0; j < frames; ++j) {
+      const long jb = std::min<long>(j / block_size, h.cols() - 1);
+      for (long n = 0; n < h.rows(); ++n) e(n, j) = h(n, jb);
+    }
+    out.act[i] = e;
+  }
+  return out;
 }
 
 double fastfca_nll(const SampleCovSet& covs, const FastFcaParams& p) {
   if (covs.dim != p.dim || covs.bins != p.bins || covs.blocks != p.frames)
     throw std::invalid_argument("nll: covariance/parameter shape mismatch");  // sigmodel.cpp:226-229
+  check_covs(covs, "nll");
   Packed pk;
   pack_bins(covs, p, 0, covs.bins, pk);
   std::vector<double> out(covs.bins);
   ffca_dims d{1, covs.bins, covs.dim, p.sources, covs.blocks, 0, 0};
-  raise(ffca_nll_bins(context(0), &d, FFCA_PREC_FP64, pk.x.data(), pk.W.data(), pk.L.data(),
-                      pk.H.data(), out.data()));
+  raise((pk.snap ? ffca_nll_bins : ffca_nll_bins_covs)(context(0), &d, FFCA_PREC_FP64,
+                                                         pk.x.data(), pk.W.data(), pk.L.data(),
+                                                         pk.H.data(), out.data()));
   double acc = 0.0;
   for (double v : out) acc += v;  // bin order
   return acc;
@@ -246,23 +308,38 @@ double fastfca_nll_freq(const SampleCovSet& covs, int i, const CMat& w, const RM
   one.act = {act};
   SampleCovSet c1;
   c1.dim = covs.dim, c1.bins = 1, c1.frames = covs.frames, c1.blocks = covs.blocks;
-  c1.snapshots = {covs.snapshots.at(i)};
+  c1.block_size = covs.block_size;
+  if (covs.has_snapshots())
+    c1.snapshots = {covs.snapshots.at(i)};
+  else
+    c1.mats = {covs.mats.at(i)};
   c1.power_scale = RVec::Zero(1);
   c1.power_scale(0) = covs.power(i);
   return fastfca_nll(c1, one);
 }
 
 RMat decorrelated_powers(const SampleCovSet& covs, int i, const CMat& w) {
-  if (i < 0 || i >= covs.bins || int(covs.snapshots.size()) != covs.bins)
-    throw std::invalid_argument("decorrelated_powers: bin out of range or no snapshots");
+  if (i < 0 || i >= covs.bins)
+    throw std::invalid_argument("decorrelated_powers: bin out of range");
+  check_covs(covs, "decorrelated_powers");
   if (w.rows() != covs.dim || w.cols() != covs.dim)
     throw std::invalid_argument("decorrelated_powers: W shape mismatch");
   const int M = covs.dim, T = covs.blocks;
   ffca_dims d{1, 1, M, M, T, 0, 0};
   RMat u(M, T);
-  raise(ffca_decorrelated_powers(context(0), &d, FFCA_PREC_FP64,
-                                 reinterpret_cast<const double*>(covs.snapshots[i].data()),
-                                 reinterpret_cast<const double*>(w.data()), -1.0, u.data()));
+  if (covs.has_snapshots()) {
+    raise(ffca_decorrelated_powers(context(0), &d, FFCA_PREC_FP64,
+                                   reinterpret_cast<const double*>(covs.snapshots[i].data()),
+                                   reinterpret_cast<const double*>(w.data()), -1.0, u.data()));
+  } else {  // sigmodel.cpp:97-105
+    std::vector<double> m(size_t(T) * M * M * 2);
+    for (int j = 0; j < T; ++j)
+      std::memcpy(m.data() + size_t(j) * M * M * 2, covs.mats[i][j].data(),
+                  sizeof(double) * M * M * 2);
+    raise(ffca_decorrelated_powers_covs(context(0), &d, FFCA_PREC_FP64, m.data(),
+                                        reinterpret_cast<const double*>(w.data()), -1.0,
+                                        u.data()));
+  }
   return u;
 }
 
@@ -281,9 +358,7 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
     throw std::invalid_argument("ica_mode_fit: requires as many sources as channels");
   if (static_cast<int>(w_init.size()) != covs.bins)
     throw std::invalid_argument("ica_mode_fit: one W per frequency required");
-  if (!covs.has_snapshots() || int(covs.snapshots.size()) != covs.bins ||
-      covs.power_scale.size() != covs.bins)
-    throw std::invalid_argument("ica_mode_fit: covariance set has no snapshots (block_size > 1)");
+  check_covs(covs, "ica_mode_fit");
   if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
   const int F = covs.bins, M = covs.dim, T = covs.blocks;
   for (const CMat& w : w_init)
@@ -305,9 +380,9 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
     const int n = hi - lo;
     std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
     ffca_dims d{1, n, M, sources, T, lo, F};
-    raise(ffca_ica_fit(context(dev), &d, &o, pk.x.data(), pk.power.data(), pk.W.data(),
-                       pk.L.data(), pk.H.data(), nullptr, fit.record_trace ? sl.data() : nullptr,
-                       nullptr));
+    raise((pk.snap ? ffca_ica_fit : ffca_ica_fit_covs)(
+        context(dev), &d, &o, pk.x.data(), pk.pw(), pk.W.data(), pk.L.data(), pk.H.data(),
+        nullptr, fit.record_trace ? sl.data() : nullptr, nullptr));
     unpack_bins(pk, lo, hi, p);
     for (int t = 0; fit.record_trace && t <= iters; ++t)
       for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
@@ -344,8 +419,9 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
     const int n = hi - lo;
     std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
     ffca_dims d{1, n, covs.dim, init.sources, covs.blocks, lo, F};
-    raise(ffca_fit(context(dev), &d, &o, pk.x.data(), pk.power.data(), pk.W.data(), pk.L.data(),
-                   pk.H.data(), nullptr, fit.record_trace ? sl.data() : nullptr, nullptr));
+    raise((pk.snap ? ffca_fit : ffca_fit_covs)(context(dev), &d, &o, pk.x.data(), pk.pw(),
+                                               pk.W.data(), pk.L.data(), pk.H.data(), nullptr,
+                                               fit.record_trace ? sl.data() : nullptr, nullptr));
     if (iters > 0) unpack_bins(pk, lo, hi, result.params);
     for (int t = 0; fit.record_trace && t <= iters; ++t)
       for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
@@ -375,7 +451,9 @@ std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>&
   for (int b = 0; b < B; ++b) {
     check_fit_shapes(covs[b], init[b]);
     if (covs[b].dim != covs[0].dim || covs[b].bins != covs[0].bins ||
-        covs[b].blocks != covs[0].blocks || init[b].sources != init[0].sources)
+        covs[b].blocks != covs[0].blocks || init[b].sources != init[0].sources ||
+        covs[b].has_snapshots() != covs[0].has_snapshots() ||
+        covs[b].power_scale.size() != covs[0].power_scale.size())
       throw std::invalid_argument("fastfca_fit_batch: mixtures must share one shape");
   }
   if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
@@ -394,9 +472,9 @@ std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>&
     }
     std::vector<double> nll(fit.record_trace ? size_t(nb) * (iters + 1) : 0);
     ffca_dims d{nb, F, covs[0].dim, init[0].sources, covs[0].blocks, 0, 0};
-    raise(ffca_fit(context(dev), &d, &o, all.x.data(), all.power.data(), all.W.data(),
-                   all.L.data(), all.H.data(), fit.record_trace ? nll.data() : nullptr, nullptr,
-                   nullptr));
+    raise((covs[0].has_snapshots() ? ffca_fit : ffca_fit_covs)(
+        context(dev), &d, &o, all.x.data(), all.pw(), all.W.data(), all.L.data(), all.H.data(),
+        fit.record_trace ? nll.data() : nullptr, nullptr, nullptr));
     if (iters > 0) {
       const int M = covs[0].dim, N = init[0].sources, T = covs[0].blocks;
       for (int b = lo; b < hi; ++b) {

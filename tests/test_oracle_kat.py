@@ -15,7 +15,9 @@ EXACT_CASES = ["ip_scalar_case", "ip_column_normalization", "nll_scale_invarianc
                "fastfca_nll_equals_fca_nll_jd", "fastfca_nll_scale_invariance",
                "em_update_known_answers", "mm_update_known_answers", "fastfca_nll_scalar_unit",
                "fca_nll_scalar_unit", "decomposed_wiener_filter", "separate_partitions_mixture",
-               "floor_positive_cases", "sample_covs_traces"]
+               "floor_positive_cases", "sample_covs_traces", "fastfca_nll_block_decomposition",
+               "decomposition_identity_along_fit", "sample_covs_block_averaging",
+               "piecewise_prepare_block_conventions"]
 
 
 @pytest.fixture(scope="module")
