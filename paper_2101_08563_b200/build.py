@@ -63,6 +63,8 @@ def build_lib(verbose: bool = False, jobs: int | None = None, variant: str = "",
     for src in cu:
         obj = bdir / (src.stem + ".o")
         if only and src.stem not in only and src.stem != "ffca_api":
+            if variant:  # diagnostics / experiment builds link the production objects
+                objs.append(BUILD / (src.stem + ".o"))
             continue
         objs.append(obj)
         if _stale(obj, src, deps):

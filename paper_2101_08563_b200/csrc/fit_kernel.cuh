@@ -77,11 +77,15 @@ struct FitParams {
 
 enum : int { kStatusOk = 0, kStatusSilent = 1, kStatusIpSingular = 2, kStatusSingularW = 3 };
 
+#ifndef FFCA_SPLIT_MIN
+#define FFCA_SPLIT_MIN 5
+#endif
 template <int M>
 struct Split {
-  // M <= 4: every thread accumulates all M weighted covariances (M^3 values).
-  // M  > 4: the CTA splits into M groups of warps, group g owns Q_g (M^2).
-  static constexpr int MSPLIT = (M <= 4) ? 1 : M;
+  // M <  FFCA_SPLIT_MIN: every thread accumulates all M weighted covariances
+  // (M^3 values).  Else the CTA splits into M groups of warps, group g owns
+  // Q_g (M^2).
+  static constexpr int MSPLIT = (M < FFCA_SPLIT_MIN) ? 1 : M;
   static constexpr int MG = M / MSPLIT;
   static constexpr int KQ = MG * M * M;          // Q values per thread
   static constexpr int KA = KQ + MG + 1;         // + sum U r per channel + sum log2 s2
@@ -92,13 +96,24 @@ struct Split {
 // registers), so the 513 bins of a 1024-point STFT fit on 148 SMs in one
 // wave; 4 warps per bin keep the per-warp share of the reductions and of the
 // all-warp updates small (c1: 128 threads beat 192 by ~6%).
+// M = 4 runs one CTA per SM (its pass A needs the full register file: the
+// bound of 2 CTAs forced 128 registers and spilled; c2 1.84 -> 1.42 ms).
+#ifndef FFCA_MINB_M3
+#define FFCA_MINB_M3 4
+#endif
+#ifndef FFCA_MINB_M4
+#define FFCA_MINB_M4 1
+#endif
+#ifndef FFCA_THREADS_BIG
+#define FFCA_THREADS_BIG 256
+#endif
 template <int M>
 struct Launch {
-  static constexpr int threads = (M <= 3) ? 128 : 256;
-  static constexpr int minb = (M <= 3) ? 4 : (M == 4 ? 2 : 1);
+  static constexpr int threads = (M <= 3) ? 128 : FFCA_THREADS_BIG;
+  static constexpr int minb = (M <= 2) ? 4 : (M == 3 ? FFCA_MINB_M3 : (M == 4 ? FFCA_MINB_M4 : 1));
 };
 
-constexpr int kMaxWarps = 8;
+constexpr int kMaxWarps = FFCA_THREADS_BIG / 32;
 
 #ifndef FFCA_FRAMES_IN_FLIGHT
 #define FFCA_FRAMES_IN_FLIGHT 1
