@@ -191,12 +191,12 @@ struct Pow2Ceil {
 };
 
 // Reduce K per-lane values over the warp and store the K totals to dst[0..K)
-// (as double).  Recursive halving: at each step the lanes split the remaining
+// (converted to D).  Recursive halving: at each step the lanes split the remaining
 // values in two and exchange the half they give away, so the warp issues
 // Kp - 1 + (5 - log2 Kp) shuffles instead of 5K (Kp = K rounded up to a power
 // of two, <= 32).  The summation tree is fixed, so results are deterministic.
-template <int K, typename T>
-__device__ __forceinline__ void warp_reduce_store(const T (&in)[K], double* dst, int lane) {
+template <int K, typename T, typename D>
+__device__ __forceinline__ void warp_reduce_store(const T (&in)[K], D* dst, int lane) {
   static_assert(K <= 32, "warp_reduce_store: at most 32 values");
   constexpr int KP = Pow2Ceil<K>::value;
   T v[KP];
@@ -220,6 +220,6 @@ __device__ __forceinline__ void warp_reduce_store(const T (&in)[K], double* dst,
   for (int oo = o; oo > 0; oo >>= 1) s += __shfl_xor_sync(0xffffffffu, s, oo);
   // Lanes whose low (plain-reduction) bits are zero hold distinct totals.
   const int lowmask = o == 0 ? 0 : (o << 1) - 1;
-  if ((lane & lowmask) == 0 && idx < K) dst[idx] = double(s);
+  if ((lane & lowmask) == 0 && idx < K) dst[idx] = D(s);
 }
 }  // namespace ffca

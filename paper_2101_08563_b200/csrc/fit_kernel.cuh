@@ -52,6 +52,20 @@
 
 namespace ffca {
 
+// Shared-memory carve-up of one fit CTA (byte offsets).  Computed on the
+// host (FitSmem below) and passed in the kernel parameters, so the kernel
+// reads every offset from the constant bank instead of re-deriving the
+// layout (the compiler rematerialised that chain inside the frame loops of
+// register-capped variants: 15 % of the instructions of the M = 3 kernel).
+struct FitLayout {
+  int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
+      off_us, off_hsum,
+      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_wsm, off_scal, off_big,
+      off_x, off_h, off_w,  // resident records: x, H, work
+      kred, kres,
+      total;
+};
+
 struct FitParams {
   int nprob;        // problems in this launch (= gridDim.x)
   int N, T;         // sources, frames
@@ -73,6 +87,7 @@ struct FitParams {
   int blk;          // x holds packed block covariances [nprob][T][M*M] (T = blocks)
   unsigned long long* timing;  // optional per-problem phase cycle counters [nprob][16]
   unsigned long long seed;
+  FitLayout lay;
 };
 
 enum : int { kStatusOk = 0, kStatusSilent = 1, kStatusIpSingular = 2, kStatusSingularW = 3 };
@@ -115,6 +130,21 @@ struct Launch {
 
 constexpr int kMaxWarps = FFCA_THREADS_BIG / 32;
 
+// Fixed-order pairwise sum of K per-warp partials red[w*K + k], w < nwarps
+// <= NW (issued as independent loads; slots beyond nwarps masked to zero):
+// depth log2(NW) instead of a serial chain.
+template <int NW, typename T>
+__device__ __forceinline__ T tree_sum_warps(const T* red, int K, int k, int nwarps) {
+  T v[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) v[w] = (w < nwarps) ? red[w * K + k] : T(0);
+#pragma unroll
+  for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+    for (int w = 0; w < h; ++w) v[w] += v[w + h];
+  return v[0];
+}
+
 #ifndef FFCA_FRAMES_IN_FLIGHT
 #define FFCA_FRAMES_IN_FLIGHT 1
 #endif
@@ -128,13 +158,8 @@ struct MmChunk {
 
 // Shared-memory carve-up, identical on host and device.
 template <int M, int NT, typename R, bool BLK = false>
-struct FitSmem {
+struct FitSmem : FitLayout {
   static constexpr int XR = BLK ? M * M : 2 * M;  // reals per x record
-  int off_wd, off_wlg, off_wsc, off_wr, off_ld, off_le, off_linv, off_hsc, off_hinv, off_hscr,
-      off_us, off_hsum,
-      off_num, off_den, off_reda, off_redb, off_res, off_rng, off_cx, off_wsm, off_scal, off_big,
-      kred, kres,
-      total;
   __host__ __device__ static int al(int v) { return (v + 15) & ~15; }
   __host__ __device__ FitSmem(int nwarps, int N, int T, int nc, bool resident) {
     using S = Split<M>;
@@ -182,12 +207,24 @@ struct FitSmem {
     off_scal = o; o = al(o + 64);
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
-    if (resident)
-      o = al(al(al(o + T * XR * (int)sizeof(R)) + T * N * (int)sizeof(R)) +
-             T * 2 * M * (int)sizeof(R));
+    off_x = o;
+    off_h = al(off_x + T * XR * (int)sizeof(R));
+    off_w = al(off_h + T * N * (int)sizeof(R));
+    if (resident) o = al(off_w + T * 2 * M * (int)sizeof(R));
     total = o;
   }
 };
+
+// The kernel's view of its layout: M <= 2 derives it in registers (measured
+// faster for c1: 0.655 vs 0.677 ms), larger M reads the host-computed copy in
+// the kernel parameters (c4: 46.9 -> 40.5 ms per 10 iterations).
+template <bool LOCAL, int M, int NT, typename R, bool BLK, typename P>
+__device__ __forceinline__ decltype(auto) fit_layout(const P& p, int nwarps, int N, bool res) {
+  if constexpr (LOCAL)
+    return FitSmem<M, NT, R, BLK>(nwarps, N, p.tloc, p.nc, res);
+  else
+    return (p.lay);
+}
 
 struct Scalars {
   double eps, nll0, logdet0, logs;
@@ -289,7 +326,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   const int t0g = int((long long)T * crank / csize);  // this CTA's frames [t0g, t0g + Tl)
   const int Tl = int((long long)T * (crank + 1) / csize) - t0g;
   const bool lead = crank == 0;  // writes the per-bin outputs
-  const Lay lay(nwarps, N, p.tloc, p.nc, RES);
+  const auto& lay = fit_layout<(M <= 2), M, NT, R, BLK>(p, nwarps, N, RES);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   double2* Wlg = reinterpret_cast<double2*>(smem + lay.off_wlg);
   // Per-bin scalar algebra (L master, balance scales, sweep updates) runs in
@@ -358,9 +395,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   R* Hs;
   R* wk;
   if constexpr (RES) {
-    const int ox = lay.off_big;
-    const int oh = Lay::al(ox + p.tloc * XR * (int)sizeof(R));
-    const int ow = Lay::al(oh + p.tloc * N * (int)sizeof(R));
+    const int ox = lay.off_x, oh = lay.off_h, ow = lay.off_w;
     R* xsm = reinterpret_cast<R*>(smem + ox);
     Hs = reinterpret_cast<R*>(smem + oh);
     wk = reinterpret_cast<R*>(smem + ow);
@@ -473,16 +508,9 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 
   // Fixed-order sum of the per-warp partials red[w*K + k] (issued as
   // independent loads, then added in warp order).
+  constexpr int NWMAX = Launch<M>::threads / 32;
   auto sum_warps = [&](const double* red, int K, int k) {
-    // Branch-free: every load hits a valid slot (index clamped), then the
-    // slots beyond nwarps are masked to zero.
-    double v[kMaxWarps];
-#pragma unroll
-    for (int w = 0; w < kMaxWarps; ++w) v[w] = red[(w < nwarps ? w : 0) * K + k];
-    double s = v[0];
-#pragma unroll
-    for (int w = 1; w < kMaxWarps; ++w) s += (w < nwarps) ? v[w] : 0.0;
-    return s;
+    return tree_sum_warps<NWMAX>(red, K, k, nwarps);
   };
 
   // ---------------------------------------------------------------- pass A --
@@ -694,12 +722,39 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
           for (int k = 0; k < NT; ++k)
             if (k == n) hn = h[f][k];
           const R ihn = rcp_fast(hn);
+          // Mixture variances L H + eps of all channels.  With the loadings
+          // in shared memory (M * NT > 32) and M % 4 == 0 they are read one
+          // column per vector load (the scalar form issued M * N loads).
+          R lhs[M];
+          if constexpr (!HOIST && M % 4 == 0 && sizeof(R) == 4) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) lhs[m] = eps;
+#pragma unroll
+            for (int k = 0; k < NT; ++k) {
+              if (FFCA_NK(k)) {
+#pragma unroll
+                for (int q = 0; q < M; q += 4) {
+                  const float4 c = *reinterpret_cast<const float4*>(Le + k * M + q);
+                  lhs[q] += c.x * h[f][k];
+                  lhs[q + 1] += c.y * h[f][k];
+                  lhs[q + 2] += c.z * h[f][k];
+                  lhs[q + 3] += c.w * h[f][k];
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              R v = eps;
+#pragma unroll
+              for (int k = 0; k < NT; ++k)
+                if (FFCA_NK(k)) v += le[m + k * M] * h[f][k];
+              lhs[m] = v;
+            }
+          }
 #pragma unroll
           for (int m = 0; m < M; ++m) {
-            R lh = eps;
-#pragma unroll
-            for (int k = 0; k < NT; ++k)
-              if (FFCA_NK(k)) lh += le[m + k * M] * h[f][k];
+            const R lh = lhs[m];
             const R lnhn = le[m + n * M] * hn;
             const R gg = lnhn * rcp_fast(lh);
             const R phi = gg * (gg * w[f][m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
@@ -724,13 +779,16 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       }
     }
     FFCA_TIC(4);
+    // Per-warp partials in the compute type (the cross-warp sum of NWMAX
+    // fp32 partials adds nothing to the per-thread fp32 accumulation error).
+    R* redr = reinterpret_cast<R*>(red);
     if (phis) {
-      warp_reduce_store<2 * M + 1>(acc, red + warp * (2 * M + 1), lane);
+      warp_reduce_store<2 * M + 1>(acc, redr + warp * (2 * M + 1), lane);
     } else {
       R a1[M + 1];
 #pragma unroll
       for (int k = 0; k <= M; ++k) a1[k] = acc[k];
-      warp_reduce_store<M + 1>(a1, red + warp * (M + 1), lane);
+      warp_reduce_store<M + 1>(a1, redr + warp * (M + 1), lane);
     }
     __syncthreads();
   };
@@ -1056,26 +1114,28 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
           // the identical update; each shared value below is written with the
           // same bits by every warp and is not read in its old state after
           // the barrier.
-          double tot = (lane < K) ? sum_warps(red, K, lane) : 0.0;
+          R tot = (lane < K) ? tree_sum_warps<NWMAX>(reinterpret_cast<const R*>(red), K, lane,
+                                                     nwarps)
+                             : R(0);
           if constexpr (CL) {
             // CTA totals -> cluster totals (rank order); every warp reads them.
-            if (warp == 0 && lane < K) res[lane] = tot;
+            if (warp == 0 && lane < K) res[lane] = double(tot);
             __syncwarp();
             cluster_sum(res, K, res, true);
-            tot = (lane < K) ? res[lane] : 0.0;
+            tot = (lane < K) ? R(res[lane]) : R(0);
             __syncwarp();
           }
           // Shuffles while the warp is converged: the H row n-1 sum and (last
           // sweep) sum_t Phi(m) on lane m.
-          const double hs = __shfl_sync(0xffffffffu, tot, M);
-          const double ps = __shfl_down_sync(0xffffffffu, tot, M + 1);
+          const R hs = __shfl_sync(0xffffffffu, tot, M);
+          const R ps = __shfl_down_sync(0xffffffffu, tot, M + 1);
           FFCA_TIC(8);
           if (lane < M) {
             // L(:, n) = max(sum_t Phi / H_true / T, tiny) with H_true = H * hsc
             // (fastfca.cpp:92-94).  The next sweep (or pass A) stores the true
             // H row n, so Le(:, n) becomes the new L column (no hsc).
             const int m = lane;
-            const B l = update_loading ? fmax(B(tot * invT) * hinv[n], tinyB) : Ld[m + n * M];
+            const B l = update_loading ? fmax(B(tot) * B(invT) * hinv[n], tinyB) : Ld[m + n * M];
             const R lr = R(l);
             Ld[m + n * M] = l;
             if (!phis) Le[m + n * M] = lr;  // with phis the balance rewrites all of Le

@@ -27,6 +27,7 @@ int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev
   }
   const int nwarps = threads / 32;
   const FitSmem<M, NT, R, BLK> lay(nwarps, fp.N, fp.tloc, fp.nc, RES);
+  fp.lay = lay;  // the kernel reads its carve-up from the parameters
   if (lay.total > dev_max)
     return ffca_set_err(FFCA_CUDA_ERROR, "ffca: fit kernel shared memory exceeds the device limit");
   auto kern = fit_kernel<M, NT, EXACT, R, CL, RES, BLK>;
@@ -87,14 +88,15 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
     return launch_fit_cfg<M, NT, EXACT, R, false, true, BLK>(ctx, fp, st, 1, dev_max);
   }
   if (C > 1) {
-    if constexpr (!EXACT && !BLK) {
+    if constexpr (!BLK) {
       fp.resident = 1;
       fp.tloc = (fp.T + C - 1) / C;
       return launch_fit_cfg<M, NT, EXACT, R, true, true>(ctx, fp, st, C, dev_max);
     }
   }
   // Streaming: the bin's records stay in global memory (L2/HBM).  Only the
-  // guarded variants get here (needs_cluster routes large bins to them).
+  // guarded variants get here (needs_cluster routes large bins to them, the
+  // exact M = 8, N = 12 variant included when a 16-CTA cluster holds them).
   if constexpr (!EXACT) {
     fp.resident = 0;
     fp.tloc = fp.T;
@@ -133,6 +135,12 @@ int launch_fit_f32(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
         default: break;
       }
     }
+  }
+  if constexpr (M == 8) {
+    // BASELINE config 3 (M = 8, N = 12): exact source count (vector H loads,
+    // no source guards), single CTA or cluster.
+    if (fp.N == 12 && pick_cluster<M, 12, float>(fp, 227 * 1024 - 2048) > 0)
+      return launch_fit_t<M, 12, true, float>(ctx, fp, st);
   }
   if (fp.N <= 4) return launch_fit_t<M, 4, false, float>(ctx, fp, st);
   if (fp.N <= 8) return launch_fit_t<M, 8, false, float>(ctx, fp, st);
