@@ -154,11 +154,18 @@ def oracle_sample(cfg, args, budget_s: float = 10.0):
     return oracle, cores, S, (x, W[:S], L[:S], H[:S]), sample
 
 
-def cpu_baseline(cfg, args) -> dict:
-    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args)
-    _, _, _, _, _, secs = oracle.fit(x, W, L, H, cfg.iters, record_trace=True, workers=cores)
-    return {"value": S * cfg.T * cfg.iters / secs, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": sample + f" ({secs:.2f} s)"}
+def cpu_baseline(cfg, args, budget_s: float = 10.0) -> dict:
+    """The oracle port on all host threads over the bounded sample, repeated
+    until about budget_s of CPU time has been measured (the whole c1 fit is
+    well under a second on the box's cores)."""
+    oracle, cores, S, (x, W, L, H), sample = oracle_sample(cfg, args, budget_s=budget_s)
+    total, reps = 0.0, 0
+    while reps == 0 or total < budget_s:
+        _, _, _, _, _, secs = oracle.fit(x, W, L, H, cfg.iters, record_trace=True, workers=cores)
+        total += secs
+        reps += 1
+    return {"value": reps * S * cfg.T * cfg.iters / total, "unit": UNIT, "cores": cores,
+            "kind": "port", "sample": sample + f" x {reps} repetitions ({total:.1f} s)"}
 
 
 def run_reference(cfg, args, rank: int, world: int) -> None:

@@ -267,6 +267,44 @@ int main() {
       for (int k = 0; k < 3; ++k) m = std::max(m, std::abs(u(k, t) - uo(k, t)) / (uo(k, t) + 1e-300));
     CHECK(m <= 1e-12);
   }
+  // ---- block-stationary input: piecewise_prepare (sample_covs with B = 3,
+  // sigmodel.cpp:17-48), fastfca_fit / fastfca_nll on the block covariances
+  // (fastfca.cpp:29-32, sigmodel.cpp:97-105) and expand_block_params.
+  {
+    const int B = 3;
+    const auto bc = fastfca::piecewise_prepare(spec, B);
+    CHECK(!bc.has_snapshots() && bc.blocks == (spec.frames + B - 1) / B && bc.block_size == B);
+    std::vector<Complex> x(size_t(spec.bins) * spec.frames * spec.channels);
+    for (int i = 0; i < spec.bins; ++i)
+      for (int j = 0; j < spec.frames; ++j)
+        for (int k = 0; k < spec.channels; ++k)
+          x[(size_t(i) * spec.frames + j) * spec.channels + k] = spec.f[i](k, j);
+    const auto obc = oracle::sample_covs(spec.channels, spec.bins, spec.frames, x.data(), B);
+    double m = 0.0;
+    for (int i = 0; i < bc.bins; ++i) {
+      CHECK(std::abs(bc.power(i) - obc.power(i)) <= 1e-13 * obc.power(i));
+      for (int j = 0; j < bc.blocks; ++j)
+        for (int c = 0; c < 3; ++c)
+          for (int r = 0; r < 3; ++r)
+            m = std::max(m, std::abs(bc.mats[i][j](r, c) - obc.mats[i][j](r, c)));
+    }
+    CHECK(m <= 1e-12);
+    auto init = random_params(3, 4, bc.blocks, 2, rng);
+    fastfca::GpuOptions g64;
+    g64.precision = fastfca::Precision::fp64;
+    const auto fit = fastfca::fastfca_fit(bc, init, fastfca::LhFlavor::em, 15, {}, {}, g64);
+    const auto ofit = oracle::fastfca_fit(obc, oracle_params(init), oracle::LhFlavor::em, 15);
+    std::printf("block fit (B = %d) nll max rel vs oracle: %.3g\n", B, max_rel(fit.nll, ofit.nll));
+    CHECK(max_rel(fit.nll, ofit.nll) <= 1e-10);
+    CHECK(std::abs(fastfca::fastfca_nll(bc, fit.params) - fit.nll.back()) <=
+          1e-10 * std::abs(fit.nll.back()));
+    const auto full = fastfca::expand_block_params(fit.params, B, spec.frames);
+    CHECK(full.frames == spec.frames);
+    CHECK(full.act[0](1, 4) == fit.params.act[0](1, 1));
+    CHECK(full.act[2](0, spec.frames - 1) == fit.params.act[2](0, bc.blocks - 1));
+    const auto img = fastfca::fastfca_separate(spec, full);
+    CHECK(img.size() == 2);
+  }
   // ---- stft / istft (stft.cpp:51-128) round trip through the C++ API.
   {
     fastfca::MultichannelWave w;
