@@ -122,9 +122,12 @@ struct Split {
 #ifndef FFCA_THREADS_BIG
 #define FFCA_THREADS_BIG 256
 #endif
+#ifndef FFCA_THREADS_SMALL
+#define FFCA_THREADS_SMALL 128
+#endif
 template <int M>
 struct Launch {
-  static constexpr int threads = (M <= 3) ? 128 : FFCA_THREADS_BIG;
+  static constexpr int threads = (M <= 3) ? FFCA_THREADS_SMALL : FFCA_THREADS_BIG;
   static constexpr int minb = (M <= 2) ? 4 : (M == 3 ? FFCA_MINB_M3 : (M == 4 ? FFCA_MINB_M4 : 1));
 };
 
@@ -1003,6 +1006,66 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
     B* hscn = hsc0 + nx * NT;
     B* hinvn = hinv0 + nx * NT;
     B* Ldn = Ld0 + nx * (M * NT);
+    if constexpr (M * NT <= 32) {
+      // Small models: lane k owns L(m, n), k = m + n M, and derives every
+      // row mean and channel scale it needs itself, in registers -- the same
+      // operations in the same order as the general path below (so the same
+      // bits), without its shared-memory round trips and warp syncs.
+      const int k = lane < M * N ? lane : 0;
+      const int m = k % M, n = k / M;
+      B hv[NT];  // hinv of every source
+      unsigned vmask = 0u;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        B mu = B(1);
+        if (FFCA_NK(j)) {
+          if (phi_mean && j == N - 1) {
+            B c = B(0);
+#pragma unroll
+            for (int mm = 0; mm < M; ++mm) c += psum[mm] * BM::rcp(Ld[mm + j * M]);
+            mu = c * B(invT / double(M));
+          } else {
+            mu = hsumv[j] * B(invT);
+          }
+        }
+        const bool v = on && mu > B(0) && isfinite(mu);
+        hv[j] = v ? mu : B(1);
+        vmask |= v ? (1u << j) : 0u;
+      }
+      B hn = hv[0];
+#pragma unroll
+      for (int j = 1; j < NT; ++j)
+        if (j == n) hn = hv[j];
+      const B hs = ((vmask >> n) & 1u) ? BM::rcp(hn) : B(1);
+      B s = B(0);
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        if (FFCA_NK(j)) s += Ld[m + j * M] * hv[j];
+      s *= B(1.0 / double(N));
+      const bool vs = on && s > B(0) && isfinite(s);
+      const B usm = vs ? BM::rcp(s) : B(1);
+      double ls = (vs && n == 0 && lane < M * N) ? double(BM::log_d(s)) : 0.0;
+      const B l0 = Ld[k];
+      B l = l0 * hn * usm;
+      l = (l0 > B(0) && !(l > B(0))) ? tinyB : l;
+      const B le = l * hs;
+      if (lane < M * N) {
+        Ldn[k] = l;
+        Le[k] = R((l > B(0) && !(le > B(0))) ? tinyB : le);
+        if (m == 0) hscn[n] = hs, hinvn[n] = hn;
+        if (n == 0) us[m] = usm, wsc[m] = vs ? BM::rsq(s) : B(1);
+      }
+      // sum_m log s_m over lanes 0..M-1 (n == 0), fixed order.
+#pragma unroll
+      for (int o = Pow2Ceil<M>::value / 2; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+      if (lane == 0) sc->logs = ls;
+      par = nx;
+      Ld = Ldn;
+      hsc = hscn;
+      hinv = hinvn;
+      __syncwarp();
+      return;
+    }
     for (int n = lane; n < N; n += 32) {
       B mu;
       if (phi_mean && n == N - 1) {
