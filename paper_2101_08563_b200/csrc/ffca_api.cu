@@ -4,7 +4,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -288,6 +290,159 @@ int fit_host(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
   return FFCA_OK;
 }
 
+// The host-buffer fit pipelined over K bin chunks on K streams: chunk c's
+// H2D + conversion overlaps the fit of chunk c-1, and its results go back
+// while later chunks still compute.  Each bin's fit is latency-bound (its
+// per-iteration dependency chain, not the SM count, sets the time), so the
+// chunks' kernels co-reside and the call costs about the transfers plus one
+// fit instead of their sum.  Snapshot input, non-ICA, enough bins only.
+// On FFCA_NUMERICAL the W/L/H buffers hold the partially updated values.
+template <typename R>
+int fit_host_chunked(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
+                     const double* power, double* W, double* L, double* H, double* nll,
+                     double* nll_slots, int32_t* bin_status, int K) {
+  const int P = d->batch * d->bins, M = d->dim, N = d->sources, T = d->frames;
+  const int iters = o->iters;
+  const bool record = o->record_trace != 0;
+  cudaError_t err;
+  const size_t nx = size_t(P) * T * M * 2, nh = size_t(P) * T * N;
+  double* dx = static_cast<double*>(ctx->get(kX, nx * 8, &err));
+  R* xs = sizeof(R) == 8 ? reinterpret_cast<R*>(dx) : static_cast<R*>(ctx->get(kXs, nx * sizeof(R), &err));
+  double* dh = static_cast<double*>(ctx->get(kH, nh * 8, &err));
+  R* hs = static_cast<R*>(ctx->get(kHs, nh * sizeof(R), &err));
+  double* dW = static_cast<double*>(ctx->get(kW, size_t(P) * M * M * 16, &err));
+  double* dL = static_cast<double*>(ctx->get(kL, size_t(P) * M * N * 8, &err));
+  double* dpow = static_cast<double*>(ctx->get(kPow, size_t(P) * 8, &err));
+  double* dnll = static_cast<double*>(ctx->get(kNll, size_t(iters + 1) * P * 8, &err));
+  int* dstat = static_cast<int*>(ctx->get(kStat, size_t(P) * 4, &err));
+  if (!dx || !xs || !dh || !hs || !dW || !dL || !dpow || !dnll || !dstat)
+    return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  for (int c = 0; c < K; ++c)
+    if (!ctx->cstream[c]) FFCA_CUDA(cudaStreamCreateWithFlags(&ctx->cstream[c], cudaStreamNonBlocking));
+  // Breadth-first issue (all uploads, then all kernels, then all downloads):
+  // a chunk's download queued before the next chunk's upload would hold the
+  // upload behind the first chunk's fit in the copy engine's queue.
+  auto range = [&](int c, int& lo, int& n) {
+    lo = int((long long)P * c / K);
+    n = int((long long)P * (c + 1) / K) - lo;
+  };
+  for (int c = 0; c < K; ++c) {
+    int lo, n;
+    range(c, lo, n);
+    if (n == 0) continue;
+    cudaStream_t s = ctx->cstream[c];
+    const size_t xo = size_t(lo) * T * M * 2, xn = size_t(n) * T * M * 2;
+    const size_t ho = size_t(lo) * T * N, hn = size_t(n) * T * N;
+    FFCA_CUDA(cudaMemcpyAsync(dx + xo, x + xo, xn * 8, cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dh + ho, H + ho, hn * 8, cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dW + size_t(lo) * M * M * 2, W + size_t(lo) * M * M * 2,
+                              size_t(n) * M * M * 16, cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dL + size_t(lo) * M * N, L + size_t(lo) * M * N,
+                              size_t(n) * M * N * 8, cudaMemcpyHostToDevice, s));
+    if (power)
+      FFCA_CUDA(cudaMemcpyAsync(dpow + lo, power + lo, size_t(n) * 8, cudaMemcpyHostToDevice, s));
+  }
+  for (int c = 0; c < K; ++c) {
+    int lo, n;
+    range(c, lo, n);
+    if (n == 0) continue;
+    cudaStream_t s = ctx->cstream[c];
+    const size_t xo = size_t(lo) * T * M * 2, xn = size_t(n) * T * M * 2;
+    const size_t ho = size_t(lo) * T * N, hn = size_t(n) * T * N;
+    if (sizeof(R) != 8) {
+      convert_kernel<double, R><<<grid_for(xn, 256), 256, 0, s>>>(dx + xo, xs + xo, xn);
+      ctx->launches++;
+      FFCA_CUDA(cudaGetLastError());
+    }
+    convert_kernel<double, R><<<grid_for(hn, 256), 256, 0, s>>>(dh + ho, hs + ho, hn);
+    ctx->launches++;
+    FFCA_CUDA(cudaGetLastError());
+    if (!power) {
+      power_kernel<double2><<<n, 256, 0, s>>>(reinterpret_cast<const double2*>(dx + xo), dpow + lo,
+                                              M, T);
+      ctx->launches++;
+      FFCA_CUDA(cudaGetLastError());
+    }
+    FitParams fp{};
+    fp.nprob = n;
+    fp.N = N;
+    fp.T = T;
+    fp.F = d->mixture_bins > 0 ? d->mixture_bins : d->bins;
+    fp.seed_bin0 = d->first_bin + lo;  // restart seed index (first_bin + p) % F
+    fp.prob_offset = lo;
+    fp.x = xs + xo;
+    fp.H = hs + ho;
+    fp.W = reinterpret_cast<double2*>(dW) + size_t(lo) * M * M;
+    fp.L = dL + size_t(lo) * M * N;
+    fp.power = dpow + lo;
+    fp.nll = dnll;
+    fp.nll_stride = P;
+    fp.status = dstat + lo;
+    fp.iters = iters;
+    fp.flavor = o->flavor;
+    fp.record = record ? 1 : 0;
+    fp.normalize = o->normalize_scales;
+    fp.fix_loadings = o->fix_loadings;
+    fp.seed = o->seed;
+    int rc = launch_fit<R>(ctx, M, fp, s);
+    if (rc) return rc;
+    if (iters > 0) {
+      unpack_h_kernel<R><<<grid_for(hn, 256), 256, 0, s>>>(hs + ho, dh + ho, dstat + lo,
+                                                            size_t(T) * N, hn);
+      ctx->launches++;
+      FFCA_CUDA(cudaGetLastError());
+    }
+  }
+  for (int c = 0; c < K && iters > 0; ++c) {
+    int lo, n;
+    range(c, lo, n);
+    if (n == 0) continue;
+    cudaStream_t s = ctx->cstream[c];
+    const size_t ho = size_t(lo) * T * N, hn = size_t(n) * T * N;
+    FFCA_CUDA(cudaMemcpyAsync(H + ho, dh + ho, hn * 8, cudaMemcpyDeviceToHost, s));
+    FFCA_CUDA(cudaMemcpyAsync(W + size_t(lo) * M * M * 2, dW + size_t(lo) * M * M * 2,
+                              size_t(n) * M * M * 16, cudaMemcpyDeviceToHost, s));
+    FFCA_CUDA(cudaMemcpyAsync(L + size_t(lo) * M * N, dL + size_t(lo) * M * N,
+                              size_t(n) * M * N * 8, cudaMemcpyDeviceToHost, s));
+  }
+  for (int c = 0; c < K; ++c) FFCA_CUDA(cudaStreamSynchronize(ctx->cstream[c]));
+  std::vector<int> stat(P);
+  FFCA_CUDA(cudaMemcpy(stat.data(), dstat, size_t(P) * 4, cudaMemcpyDeviceToHost));
+  std::vector<double> slots;
+  if (record) {
+    slots.resize(size_t(iters + 1) * P);
+    FFCA_CUDA(cudaMemcpy(slots.data(), dnll, slots.size() * 8, cudaMemcpyDeviceToHost));
+  }
+  for (int p = 0; p < P; ++p) {
+    const int st = stat[p] & 0xff;
+    if (st == kStatusIpSingular)
+      return set_err(FFCA_NUMERICAL, "ip_update_w: singular system for column " +
+                                         std::to_string(stat[p] >> 8));
+    if (st == kStatusSingularW) return set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
+  }
+  if (bin_status) std::memcpy(bin_status, stat.data(), size_t(P) * 4);
+  if (record) {
+    const int F = d->bins;
+    for (int b = 0; b < d->batch; ++b)
+      for (int t = 0; t <= iters; ++t) {
+        double sum = 0.0;  // bin order, fastfca.cpp:188
+        for (int i = 0; i < F; ++i) sum += slots[size_t(t) * P + size_t(b) * F + i];
+        if (nll) nll[size_t(b) * (iters + 1) + t] = sum;
+        if (nll_slots)
+          for (int i = 0; i < F; ++i)
+            nll_slots[(size_t(b) * (iters + 1) + t) * F + i] = slots[size_t(t) * P + size_t(b) * F + i];
+      }
+  }
+  return FFCA_OK;
+}
+
+// Chunks for the pipelined host fit: one per ~128 bins, at most kMaxChunks;
+// 1 (the plain path) below 256 bins.
+inline int fit_chunks(int P) {
+  if (const char* e = getenv("FFCA_FIT_CHUNKS")) return std::max(1, std::min(kMaxChunks, atoi(e)));
+  return P < 256 ? 1 : std::min(kMaxChunks, P / 128);
+}
+
 // ffca_fit / ffca_ica_fit and their block-covariance variants.
 int fit_entry(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* x,
               const double* power, double* W, double* L, double* H, double* nll,
@@ -313,6 +468,11 @@ int fit_entry(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const d
       if (bin_status) std::memset(bin_status, 0, sizeof(int32_t) * d->batch * d->bins);
       return FFCA_OK;
     }
+    const int K = blk ? 1 : fit_chunks(d->batch * d->bins);
+    if (K > 1)
+      return o->precision == FFCA_PREC_FP64
+                 ? fit_host_chunked<double>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, K)
+                 : fit_host_chunked<float>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, K);
     if (o->precision == FFCA_PREC_FP64)
       return fit_host<double>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, blk);
     return fit_host<float>(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, blk);
@@ -373,6 +533,8 @@ void ffca_ctx_destroy(ffca_ctx* ctx) {
   for (auto& b : ctx->bufs)
     if (b.p) cudaFree(b.p);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (auto& s : ctx->cstream)
+    if (s) cudaStreamDestroy(s);
   delete ctx;
 }
 

@@ -312,6 +312,11 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   constexpr int WR = 2 * M;  // reals per work record: U[M], Phi[M]
   constexpr bool HOIST = (M * NT <= 32);
   constexpr int FU = FFCA_FRAMES_IN_FLIGHT;  // frames per loop trip (ILP vs registers)
+#ifdef FFCA_FRAMES_IN_FLIGHT_EM
+  constexpr int FUE = FFCA_FRAMES_IN_FLIGHT_EM;  // EM sweeps (tuning experiments)
+#else
+  constexpr int FUE = FU;
+#endif
   using WU = Uniform<2 * M * M, (2 * M * M <= 32), R>;  // W in the compute type
   extern __shared__ __align__(16) unsigned char smem[];
   const int nthreads = blockDim.x, tid = threadIdx.x, nwarps = nthreads >> 5;
@@ -685,12 +690,12 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
 #pragma unroll
     for (int k = 0; k <= 2 * M; ++k) acc[k] = R(0);
     const int j = n - 1;
-    // FU frames per trip: loads, independent arithmetic chains, then stores.
-    for (int tb = tid; tb < Tl; tb += FU * nthreads) {
-      R h[FU][NT], w[FU][WR];
-      bool ok[FU];
+    // FUE frames per trip: loads, independent arithmetic chains, then stores.
+    for (int tb = tid; tb < Tl; tb += FUE * nthreads) {
+      R h[FUE][NT], w[FUE][WR];
+      bool ok[FUE];
 #pragma unroll
-      for (int f = 0; f < FU; ++f) {
+      for (int f = 0; f < FUE; ++f) {
         const int t = tb + f * nthreads;
         ok[f] = t < Tl;
         const int tt = ok[f] ? t : tb;  // always a valid record
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
       }
 #pragma unroll
-      for (int f = 0; f < FU; ++f) {
+      for (int f = 0; f < FUE; ++f) {
         if (!ok[f]) continue;
         if (j >= 0) {
           R s = linv[0] * w[f][M];
@@ -768,7 +773,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
       }
 #pragma unroll
-      for (int f = 0; f < FU; ++f) {
+      for (int f = 0; f < FUE; ++f) {
         if (!ok[f]) continue;
         const int t = tb + f * nthreads;
         if (j >= 0) {

@@ -209,3 +209,20 @@ def test_cluster_split_bins_match_oracle(gpu, precision, M, N, T, iters):
     img_o = oracle.separate(x, Wo, Lo, Ho)
     for n in range(N):
         assert rel_l2(img_g[n].f, img_o[n]) <= SEP_TOL[precision]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_pipelined_host_fit_matches_single_launch(gpu, precision, monkeypatch):
+    # ffca_fit splits >= 256 bins into chunks on separate streams (transfers
+    # overlap the fit); every bin's result must be bit-identical to one launch.
+    x, W, L, H = make_case(2, 3, 300, 200, seed=5)
+    monkeypatch.setenv("FFCA_FIT_CHUNKS", "1")
+    a = gpu_fit(x, W, L, H, 8, precision)
+    monkeypatch.setenv("FFCA_FIT_CHUNKS", "3")
+    b = gpu_fit(x, W, L, H, 8, precision)
+    assert np.array_equal(np.asarray(a.nll), np.asarray(b.nll))
+    assert np.array_equal(a.params.act, b.params.act)
+    assert np.array_equal(a.params.loading, b.params.loading)
+    assert np.array_equal(a.params.decorr, b.params.decorr)
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, 8)
+    assert (np.abs(np.asarray(b.nll) - nll_o) / np.abs(nll_o)).max() <= NLL_TOL[precision]
