@@ -195,3 +195,17 @@ def test_device_block_path_matches_host_path(gpu):
     nll_dev = slots.cpu().numpy().sum(axis=1)
     assert rel(nll_dev, np.asarray(host.nll)) <= 1e-12
     np.testing.assert_array_equal(np.swapaxes(Ld.cpu().numpy(), -1, -2), host.params.loading)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_block_fit_streaming_bin_matches_oracle(gpu, precision):
+    # 2000 blocks of M = 4 records (240 KB per bin) exceed one CTA's shared
+    # memory: the block path streams its records from global memory.
+    M, N, F, T, B, iters = 4, 6, 2, 4000, 2, 5
+    x, W, L, H = make_case(M, N, F, T, B, seed=31, kind="fullrank")
+    covs = api.sample_covs(api.Spectrogram(x), B)
+    assert covs.blocks == 2000
+    r = api.fastfca_fit(covs, api.FastFcaParams(W, L, H), api.LhFlavor.em, iters,
+                        precision=precision)
+    Wo, Lo, Ho, nll_o, _ = oracle.fit_covs(covs.mats, W, L, H, iters, power=covs.power_scale)
+    assert rel(r.nll, nll_o) <= NLL_TOL[precision]

@@ -226,3 +226,14 @@ def test_pipelined_host_fit_matches_single_launch(gpu, precision, monkeypatch):
     assert np.array_equal(a.params.decorr, b.params.decorr)
     Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, 8)
     assert (np.abs(np.asarray(b.nll) - nll_o) / np.abs(nll_o)).max() <= NLL_TOL[precision]
+
+
+# A bin beyond a 16-CTA cluster's shared memory streams its records from
+# global memory (the !RES variant); config 3's M, N with T = 20000 frames.
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_streaming_bin_matches_oracle(gpu, precision):
+    x, W, L, H = make_case(8, 12, 1, 20000, seed=23)
+    r = gpu_fit(x, W, L, H, 2, precision)
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, 2)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision], rel.max()
