@@ -92,6 +92,10 @@ struct FitParams {
 
 enum : int { kStatusOk = 0, kStatusSilent = 1, kStatusIpSingular = 2, kStatusSingularW = 3 };
 
+// M > 4 IP: registers (ip_update_warp_reg) or shared-memory Gauss-Jordan.
+#ifndef FFCA_IP_WARP_REG
+#define FFCA_IP_WARP_REG 1
+#endif
 #ifndef FFCA_SPLIT_MIN
 #define FFCA_SPLIT_MIN 5
 #endif
@@ -960,7 +964,11 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
         __syncwarp();
       }
+#if FFCA_IP_WARP_REG
+      ok = ip_update_warp_reg<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
+#else
       ok = ip_update_warp<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
+#endif
     } else {
       if (lane == 0) {
         IpExtras<R> ex;

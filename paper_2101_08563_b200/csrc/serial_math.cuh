@@ -682,4 +682,144 @@ __device__ bool ip_update_warp(double2* w, const double* qraw, double invT,
   return true;
 }
 
+// ip_update_w (fastfca.cpp:36-72) by one warp with the system in registers:
+// lane r (< M) holds row r of A = W^H Q_col (and of the right-hand side e_col)
+// and column r of W.  Gauss-Jordan with partial pivoting runs on virtual row
+// positions: the pivot is the largest |A(., k)|^2 among the rows not yet used
+// (ties -> lowest current position, exactly the order the physical row swaps
+// of ip_update_warp / Eigen::PartialPivLU produce), its row is broadcast by
+// shuffles and every other row eliminates against it -- no shared-memory
+// round trips or warp syncs inside the elimination.  Q_col is read from
+// `scratch` (M x M).  Same arithmetic, acceptance tests and seeded restart as
+// ip_update_warp.
+template <int M, typename SR>
+__device__ bool ip_update_warp_reg(double2* w, const double* qraw, double invT,
+                                   unsigned long long seed, int bin, RestartRng* rng,
+                                   cplx_t<SR>* scratch, int lane, int& bad_col) {
+  using SC = cplx_t<SR>;
+  SC* Q = scratch;  // M x M, column-major
+  const bool act = lane < M;
+  const int r = act ? lane : 0;
+  bool restarted = false;
+  SC wcol[M];  // column r of W, compute type
+#pragma unroll
+  for (int k = 0; k < M; ++k) wcol[k] = mkc<SR>(SR(w[k + r * M].x), SR(w[k + r * M].y));
+  for (int col = 0; col < M; ++col) {
+    const double* p = qraw + col * M * M;
+    for (int e = lane; e < M * M; e += 32) {
+      const int a = e % M, b = e / M;
+      if (a == b) Q[e] = mkc<SR>(SR(p[a * M + a] * invT), SR(0));
+      else if (a < b) Q[e] = mkc<SR>(SR(p[a * M + b] * invT), SR(p[b * M + a] * invT));
+      else Q[e] = mkc<SR>(SR(p[b * M + a] * invT), SR(-p[a * M + b] * invT));
+    }
+    __syncwarp();
+    for (int attempt = 0;; ++attempt) {
+      // Row r of A = W^H Q (column r of W against every column of Q).
+      SC row[M + 1], a0[M];
+      SR an = SR(0);
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        SC s = cmulc(wcol[0], Q[c * M]);
+#pragma unroll
+        for (int k = 1; k < M; ++k) s = cadd(s, cmulc(wcol[k], Q[k + c * M]));
+        row[c] = s;
+        a0[c] = s;
+        an += act ? cabs2(s) : SR(0);
+      }
+      row[M] = mkc<SR>(r == col ? SR(1) : SR(0), SR(0));
+      const SR anorm = warp_allsum(an);
+      // Gauss-Jordan on virtual positions.
+      bool used = !act;
+      int pos = lane;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        SR best = used ? SR(-1) : cabs2(row[k]);
+        int bpos = used ? 1 << 20 : pos, blane = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const SR ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, blane, o);
+          if (ob > best || (ob == best && op < bpos)) best = ob, bpos = op, blane = ol;
+        }
+        const int pl = blane;  // pivot lane
+        SC prow[M + 1];
+#pragma unroll
+        for (int c = k; c <= M; ++c)
+          prow[c] = mkc<SR>(__shfl_sync(0xffffffffu, row[c].x, pl),
+                            __shfl_sync(0xffffffffu, row[c].y, pl));
+        const SR pm = cabs2(prow[k]);
+        const SR sc = SMath<SR>::rcp(pm);
+        const SC ipiv = mkc<SR>(prow[k].x * sc, -prow[k].y * sc);
+        // Scaled pivot row (columns > k): A(k,c) / A(k,k).
+#pragma unroll
+        for (int c = k + 1; c <= M; ++c) prow[c] = cmul(prow[c], ipiv);
+        if (lane == pl) {
+#pragma unroll
+          for (int c = k + 1; c <= M; ++c) row[c] = prow[c];
+        } else if (act) {
+          const SC f = row[k];
+#pragma unroll
+          for (int c = k + 1; c <= M; ++c) row[c] = csub(row[c], cmul(f, prow[c]));
+        }
+        // Position bookkeeping of the emulated swap of rows k and bpos.
+        const int ppos = bpos;
+        if (pos == k) pos = ppos;
+        if (lane == pl) pos = k, used = true;
+      }
+      // The row now at position i holds w_i in its right-hand side; lane r
+      // collects w_r.
+      SC wm = mkc<SR>(SR(0), SR(0));
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const unsigned bal = __ballot_sync(0xffffffffu, act && pos == i);
+        const int src = __ffs(bal) - 1;
+        const SR vx = __shfl_sync(0xffffffffu, row[M].x, src < 0 ? 0 : src);
+        const SR vy = __shfl_sync(0xffffffffu, row[M].y, src < 0 ? 0 : src);
+        if (lane == i) wm = mkc<SR>(vx, vy);
+      }
+      const bool fin = __all_sync(0xffffffffu, !act || (isfinite(wm.x) && isfinite(wm.y)));
+      const SR wn = warp_allsum(act ? cabs2(wm) : SR(0));
+      SC rr = mkc<SR>(r == col ? SR(-1) : SR(0), SR(0));
+      SC qw = mkc<SR>(SR(0), SR(0));
+      SC wall[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        wall[c] = mkc<SR>(__shfl_sync(0xffffffffu, wm.x, c), __shfl_sync(0xffffffffu, wm.y, c));
+        rr = cadd(rr, cmul(a0[c], wall[c]));
+        qw = cadd(qw, cmul(Q[r + c * M], wall[c]));
+      }
+      const SR rn = warp_allsum(act ? cabs2(rr) : SR(0));
+      const SR en = warp_allsum(act ? cmulc(wm, qw).x : SR(0));
+      const SR scale = SR(sqrt_approx(float(anorm * wn))) + SR(1);
+      if (fin && rn <= SMath<SR>::kResidTol2 * scale * scale && en > SR(0) && isfinite(en)) {
+        const SR s = SMath<SR>::rsq(en);
+        if (act) {
+          const SC nw = mkc<SR>(wm.x * s, wm.y * s);
+          w[lane + col * M] = make_double2(double(nw.x), double(nw.y));
+        }
+        if (lane == col) {
+#pragma unroll
+          for (int k = 0; k < M; ++k) wcol[k] = mkc<SR>(wall[k].x * s, wall[k].y * s);
+        }
+        __syncwarp();
+        break;
+      }
+      if (attempt >= 1) {
+        bad_col = col;
+        return false;
+      }
+      if (lane == 0) ip_perturb(w + col * M, M, rng, !restarted, seed, bin);
+      restarted = true;
+      __syncwarp();
+      if (lane == col) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) wcol[k] = mkc<SR>(SR(w[k + col * M].x), SR(w[k + col * M].y));
+      }
+      __syncwarp();
+    }
+  }
+  return true;
+}
+
 }  // namespace ffca
