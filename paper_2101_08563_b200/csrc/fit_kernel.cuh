@@ -96,6 +96,10 @@ enum : int { kStatusOk = 0, kStatusSilent = 1, kStatusIpSingular = 2, kStatusSin
 #ifndef FFCA_IP_WARP_REG
 #define FFCA_IP_WARP_REG 1
 #endif
+// Smallest M whose IP runs warp-cooperatively (below: one lane in registers).
+#ifndef FFCA_IP_WARP_MIN
+#define FFCA_IP_WARP_MIN 3
+#endif
 #ifndef FFCA_SPLIT_MIN
 #define FFCA_SPLIT_MIN 5
 #endif
@@ -210,7 +214,8 @@ struct FitSmem : FitLayout {
     off_res = o; o = al(o + kres * 8);
     off_cx = o; o = al(o + 2 * kres * 8);               // cluster exchange, double-buffered
     off_wsm = o;  // warp-cooperative algebra scratch (M > 4): warp 0 then warp 1
-    o = al(o + (M > 4 ? (4 * M * M + M + M * (M + 1)) * 2 * (int)sizeof(R) : 0));
+    o = al(o + ((M > 4 || M >= FFCA_IP_WARP_MIN) ? (4 * M * M + M + M * (M + 1)) * 2 * (int)sizeof(R)
+                                                  : 0));
     off_scal = o; o = al(o + 64);
     off_big = o;
     // x, H and work records, each region 16-byte aligned.
@@ -955,7 +960,8 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
   auto run_ip = [&](unsigned long long seed, bool with_logdet, bool scaled) {
     int bad = -1;
     bool ok = true;
-    if constexpr (M > 4) {
+    constexpr bool WIP = (M > 4) || (M >= FFCA_IP_WARP_MIN);  // warp-cooperative IP
+    if constexpr (WIP) {
       if (scaled) {
         for (int k = lane; k < M * M; k += 32) {
           const double c = double(wsc[k / M]);
@@ -964,11 +970,10 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
         }
         __syncwarp();
       }
-#if FFCA_IP_WARP_REG
-      ok = ip_update_warp_reg<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
-#else
-      ok = ip_update_warp<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
-#endif
+      if constexpr (FFCA_IP_WARP_REG || M <= 4)
+        ok = ip_update_warp_reg<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
+      else
+        ok = ip_update_warp<M, R>(Wd, res, invT, seed, bin_index, rng, wsm0, lane, bad);
     } else {
       if (lane == 0) {
         IpExtras<R> ex;
@@ -987,7 +992,7 @@ __global__ void __launch_bounds__(Launch<M>::threads, Launch<M>::minb) fit_kerne
       sc->stop = 1;
     }
     __syncwarp();
-    if constexpr (M > 4)
+    if constexpr (WIP)
       for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
     if constexpr (M > 2)
       for (int k = lane; k < M * M; k += 32) Wlg[k] = Wd[k];  // log-det input (ldwarp)
