@@ -49,6 +49,40 @@ __global__ void power_kernel(const C* __restrict__ x, double* __restrict__ out, 
   }
 }
 
+// The host fit's per-chunk staging in one launch: x (fp64 -> compute type,
+// skipped when R is double), H (fp64 -> compute type) and, when power is
+// non-null, power_scale exactly as power_kernel computes it (same loop and
+// reduction order, so the same bits).  One CTA of 256 threads per problem.
+template <typename R>
+__global__ void __launch_bounds__(256) stage_kernel(const double2* __restrict__ x,
+                                                    cplx_t<R>* __restrict__ xs,
+                                                    const double* __restrict__ h,
+                                                    R* __restrict__ hs, double* __restrict__ power,
+                                                    int M, int N, int T) {
+  __shared__ double red[32];
+  const int p = blockIdx.x;
+  const double2* xp = x + size_t(p) * T * M;
+  cplx_t<R>* xo = xs + size_t(p) * T * M;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < T * M; k += blockDim.x) {
+    const double2 v = xp[k];
+    if (sizeof(R) != 8) xo[k] = mkc<R>(R(v.x), R(v.y));
+    s += cabs2(v);
+  }
+  const double* hp = h + size_t(p) * T * N;
+  R* ho = hs + size_t(p) * T * N;
+  for (int k = threadIdx.x; k < T * N; k += blockDim.x) ho[k] = R(hp[k]);
+  if (!power) return;
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) tot += red[w];
+    power[p] = tot / (double(T) * M);
+  }
+}
+
 // decorrelated_powers (sigmodel.cpp:93-107, snapshot branch :96) followed by
 // floor_positive (sigmodel.cpp:10-15) when floor_rel >= 0: U(m, t) =
 // |w_m^H x_t|^2, then U = max(U, rel * mean(U)) (1e-300 if the mean is not

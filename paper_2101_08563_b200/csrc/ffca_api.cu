@@ -349,20 +349,12 @@ int fit_host_chunked(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, 
     cudaStream_t s = ctx->cstream[c];
     const size_t xo = size_t(lo) * T * M * 2, xn = size_t(n) * T * M * 2;
     const size_t ho = size_t(lo) * T * N, hn = size_t(n) * T * N;
-    if (sizeof(R) != 8) {
-      convert_kernel<double, R><<<grid_for(xn, 256), 256, 0, s>>>(dx + xo, xs + xo, xn);
-      ctx->launches++;
-      FFCA_CUDA(cudaGetLastError());
-    }
-    convert_kernel<double, R><<<grid_for(hn, 256), 256, 0, s>>>(dh + ho, hs + ho, hn);
+    (void)xn;
+    stage_kernel<R><<<n, 256, 0, s>>>(reinterpret_cast<const double2*>(dx + xo),
+                                      reinterpret_cast<cplx_t<R>*>(xs + xo), dh + ho, hs + ho,
+                                      power ? nullptr : dpow + lo, M, N, T);
     ctx->launches++;
     FFCA_CUDA(cudaGetLastError());
-    if (!power) {
-      power_kernel<double2><<<n, 256, 0, s>>>(reinterpret_cast<const double2*>(dx + xo), dpow + lo,
-                                              M, T);
-      ctx->launches++;
-      FFCA_CUDA(cudaGetLastError());
-    }
     FitParams fp{};
     fp.nprob = n;
     fp.N = N;

@@ -29,7 +29,7 @@ def main():
     opts = _lib.FitOpts(_lib.FLAVOR_EM, iters, 1, 0, 1, 0, _lib.PREC_FP32)
     ctx = _lib.Context(0)
     L_ = _lib.lib()
-    for k in (1, 4, 6, 8):
+    for k in (1, 4):
         os.environ["FFCA_FIT_CHUNKS"] = str(k)
         ts = []
         for i in range(8):
