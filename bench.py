@@ -309,6 +309,26 @@ def main() -> None:
     trace = bin_order_trace(all_slots, cfg.batch, cfg.F)  # [iters+1, batch]
     monotone = bool((trace[1:] <= trace[:-1] + 1e-5 * np.abs(trace[:-1])).all())
 
+    # The same fit with record_trace off (timed with the trace
+    # on -- the headline, as the parity runs -- and off).
+    opts_nt = _lib.FitOpts(_lib.FLAVOR_EM, iters, 0, 0, 1, 0, prec)
+    nt_ms = []
+    for i in range(3 + 10):
+        reset()
+        flush.fill_(i & 0xff)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(L_.ffca_fit_device(ctx.handle, Pl, cfg.F, lo, M, N, T, opts_nt, _lib.ptr(x_d),
+                                      _lib.ptr(power), _lib.ptr(W_d), _lib.ptr(L_d),
+                                      _lib.ptr(H_d), None, _lib.ptr(status), sp))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            nt_ms.append(e0.elapsed_time(e1))
+    trace_off = {"ms_per_step": statistics.median(nt_ms),
+                 "value": P * T * iters / (statistics.median(nt_ms) / 1e3),
+                 "note": "record_trace=false (no per-iteration NLL), median of 10, this rank"}
+
     # Separation (fastfca_separate) of the fitted parameters, device path.
     img = torch.empty((N, Pl, T, M), dtype=cdt, device=dev)
     sep_ms = []
@@ -400,6 +420,7 @@ def main() -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "trace_off": trace_off,
             "separate": separate,
             "clocks": clocks,
             "trace": {"nll_first": float(trace[0].sum()), "nll_last": float(trace[-1].sum()),
