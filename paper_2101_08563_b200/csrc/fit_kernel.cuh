@@ -133,9 +133,13 @@ struct Split {
 #ifndef FFCA_THREADS_SMALL
 #define FFCA_THREADS_SMALL 128
 #endif
+#ifndef FFCA_THREADS_M4
+#define FFCA_THREADS_M4 FFCA_THREADS_BIG
+#endif
 template <int M>
 struct Launch {
-  static constexpr int threads = (M <= 3) ? FFCA_THREADS_SMALL : FFCA_THREADS_BIG;
+  static constexpr int threads =
+      (M <= 3) ? FFCA_THREADS_SMALL : (M == 4 ? FFCA_THREADS_M4 : FFCA_THREADS_BIG);
   static constexpr int minb = (M <= 2) ? 4 : (M == 3 ? FFCA_MINB_M3 : (M == 4 ? FFCA_MINB_M4 : 1));
 };
 

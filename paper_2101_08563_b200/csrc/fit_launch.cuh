@@ -19,7 +19,7 @@ namespace ffca {
 
 template <int M, int NT, bool EXACT, typename R, bool CL, bool RES, bool BLK = false>
 int launch_fit_cfg(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int C, int dev_max) {
-  int threads = fit_threads(M, fp.tloc, Launch<M>::threads);
+  int threads = fit_threads(M, fp.tloc, Launch<M>::threads, Split<M>::MSPLIT);
   if (const char* e = getenv("FFCA_FIT_THREADS")) {  // tuning experiments only
     const int v = atoi(e);
     const int per = (M <= 4) ? 32 : 32 * M;
@@ -61,7 +61,7 @@ template <int M, int NT, typename R, bool BLK = false>
 int pick_cluster(const FitParams& fp, int budget) {
   for (int C = 1; C <= 16; C *= 2) {
     const int tloc = (fp.T + C - 1) / C;
-    const int nwarps = fit_threads(M, tloc, Launch<M>::threads) / 32;
+    const int nwarps = fit_threads(M, tloc, Launch<M>::threads, Split<M>::MSPLIT) / 32;
     if (FitSmem<M, NT, R, BLK>(nwarps, fp.N, tloc, fp.nc, true).total <= budget) return C;
   }
   return 0;

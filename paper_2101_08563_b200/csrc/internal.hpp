@@ -53,8 +53,8 @@ enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kWave, kS
 // Threads per fit CTA: about 4 frames per thread, capped at the kernel's
 // launch bound; a multiple of 32*M when the weighted-covariance pass is split
 // by channel (M > 4).
-inline int fit_threads(int M, int T, int maxt) {
-  const int per = (M <= 4) ? 32 : 32 * M;
+inline int fit_threads(int M, int T, int maxt, int msplit = 0) {
+  const int per = (msplit > 1) ? 32 * msplit : ((M <= 4) ? 32 : 32 * M);
   const int want = (T + 3) / 4;
   int th = ((want + per - 1) / per) * per;
   const int cap = (maxt / per) * per;
