@@ -143,8 +143,6 @@ struct Launch {
   static constexpr int minb = (M <= 2) ? 4 : (M == 3 ? FFCA_MINB_M3 : (M == 4 ? FFCA_MINB_M4 : 1));
 };
 
-constexpr int kMaxWarps = FFCA_THREADS_BIG / 32;
-
 // Fixed-order pairwise sum of K per-warp partials red[w*K + k], w < nwarps
 // <= NW (issued as independent loads; slots beyond nwarps masked to zero):
 // depth log2(NW) instead of a serial chain.
