@@ -44,6 +44,12 @@ FIT_CASES = {
     "fit_m3n4_mm_fixL": (3, 4, 2, 300, 10, 1, "jd", 18, {"fix_loadings": True}),
 }
 ICA_CASE = ("ica_m2", 2, 3, 300, 15, 19)
+# block-stationary input (sample_covs(spec, B), sigmodel.cpp:17-48):
+# name: (M, N, F, T, B, iters, flavor, seed); T % B != 0 leaves a ragged tail block
+BLOCK_CASES = {
+    "block_m2n2_b10_em": (2, 2, 4, 505, 10, 20, 0, 21),
+    "block_m3n4_b4_mm": (3, 4, 3, 313, 4, 10, 1, 22),
+}
 
 
 def inputs(M, N, F, T, kind, seed):
@@ -64,6 +70,16 @@ def main() -> None:
         if name == "fit_m2n3_em":
             out["images"] = oracle.separate(x, Wo, Lo, Ho).astype(np.complex128)
         np.savez_compressed(HERE / f"{name}.npz", **out)
+        print(name, "nll", nll[0], "->", nll[-1])
+    for name, (M, N, F, T, B, iters, flavor, seed) in BLOCK_CASES.items():
+        x, W, L, _ = inputs(M, N, F, T, "jd", seed)
+        J = -(-T // B)
+        H = np.random.default_rng(seed + 1).lognormal(0.0, 1.0, (F, N, J))
+        mats, power = oracle.block_covs(x, B)
+        Wo, Lo, Ho, nll, _ = oracle.fit_covs(mats, W, L, H, iters, flavor=flavor, power=power)
+        np.savez_compressed(HERE / f"{name}.npz", x=x.astype(np.complex64), block_size=B,
+                            W0=W, L0=L, H0=H, iters=iters, flavor=flavor, mats=mats,
+                            power=power, W=Wo, L=Lo, H=Ho, nll=nll)
         print(name, "nll", nll[0], "->", nll[-1])
     name, M, F, T, iters, seed = ICA_CASE
     x, W, _, _ = inputs(M, M, F, T, "jd", seed)

@@ -16,6 +16,7 @@ import pytest
 
 GOLD = Path(__file__).resolve().parent / "golden"
 FIT_FILES = sorted(p.name for p in GOLD.glob("fit_*.npz"))
+BLOCK_FILES = sorted(p.name for p in GOLD.glob("block_*.npz"))
 NLL_TOL = {"fp32": 1e-5, "fp64": 1e-10}
 SEP_TOL = {"fp32": 1e-3, "fp64": 1e-10}
 
@@ -34,7 +35,7 @@ def max_rel(a, b):
 
 
 def test_fixture_set_complete():
-    assert len(FIT_FILES) >= 8 and (GOLD / "ica_m2.npz").exists()
+    assert len(FIT_FILES) >= 8 and len(BLOCK_FILES) >= 2 and (GOLD / "ica_m2.npz").exists()
     g = load("fit_m2n3_em.npz")
     assert g["nll"].shape == (int(g["iters"]) + 1,) and "images" in g
 
@@ -103,4 +104,36 @@ def test_gpu_ica_matches_golden(gpu, precision):
     assert max_rel(np.asarray(r.nll), g["nll"]) <= NLL_TOL[precision]
     assert np.array_equal(r.params.loading, np.tile(np.eye(M), (g["x"].shape[0], 1, 1)))
     if precision == "fp64":
+        assert rel_l2(r.params.decorr, g["W"]) <= 1e-7
+
+
+# --------------------------------------------- block-stationary fixtures --
+@pytest.mark.parametrize("name", BLOCK_FILES)
+def test_oracle_reproduces_golden_block_fit(built, name):
+    import oracle
+    g = load(name)
+    mats, power = oracle.block_covs(g["x"].astype(np.complex128), int(g["block_size"]))
+    assert rel_l2(mats, g["mats"]) <= 1e-14 and max_rel(power, g["power"]) <= 1e-14
+    Wo, Lo, Ho, nll, _ = oracle.fit_covs(mats, g["W0"], g["L0"], g["H0"], int(g["iters"]),
+                                         flavor=int(g["flavor"]), power=power)
+    assert max_rel(nll, g["nll"]) <= 1e-12
+    for got, want in ((Wo, g["W"]), (Lo, g["L"]), (Ho, g["H"])):
+        assert rel_l2(got, want) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", BLOCK_FILES)
+def test_gpu_block_fit_matches_golden(gpu, name, precision):
+    from paper_2101_08563_b200 import api
+    g = load(name)
+    covs = api.sample_covs(api.Spectrogram(g["x"].astype(np.complex128)), int(g["block_size"]))
+    assert rel_l2(covs.mats, g["mats"]) <= 1e-12  # block covariances are fp64 on the GPU
+    assert max_rel(covs.power_scale, g["power"]) <= 1e-12
+    r = api.fastfca_fit(covs, api.FastFcaParams(g["W0"], g["L0"], g["H0"]), int(g["flavor"]),
+                        int(g["iters"]), precision=precision)
+    assert max_rel(np.asarray(r.nll), g["nll"]) <= NLL_TOL[precision]
+    assert (r.bin_status == 0).all()
+    if precision == "fp64":
+        assert rel_l2(r.params.loading, g["L"]) <= 1e-7
         assert rel_l2(r.params.decorr, g["W"]) <= 1e-7
