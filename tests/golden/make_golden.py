@@ -30,6 +30,7 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "oracle"))
 
 import oracle  # noqa: E402
+import stft_oracle  # noqa: E402
 from paper_2101_08563_b200 import synth  # noqa: E402
 
 # name: (M, N, F, T, iters, flavor 0=em/1=mm, kind, seed, extra)
@@ -49,6 +50,14 @@ ICA_CASE = ("ica_m2", 2, 3, 300, 15, 19)
 BLOCK_CASES = {
     "block_m2n2_b10_em": (2, 2, 4, 505, 10, 20, 0, 21),
     "block_m3n4_b4_mm": (3, 4, 3, 313, 4, 10, 1, 22),
+}
+
+
+# STFT front end / iSTFT back end (stft.cpp:33-128): name: (channels, length,
+# frame_len, shift, padding 0=centered/1=full_frames, seed)
+STFT_CASES = {
+    "stft_c2_n5000_f256_centered": (2, 5000, 256, 128, 0, 23),
+    "stft_c3_n3001_f512_full": (3, 3001, 512, 256, 1, 24),
 }
 
 
@@ -81,6 +90,13 @@ def main() -> None:
                             W0=W, L0=L, H0=H, iters=iters, flavor=flavor, mats=mats,
                             power=power, W=Wo, L=Lo, H=Ho, nll=nll)
         print(name, "nll", nll[0], "->", nll[-1])
+    for name, (C, n, fl, sh, pad, seed) in STFT_CASES.items():
+        wave = np.random.default_rng(seed).standard_normal((C, n))
+        spec = stft_oracle.stft(wave, fl, sh, pad)
+        back = stft_oracle.istft(spec, fl, sh, n, pad)
+        np.savez_compressed(HERE / f"{name}.npz", wave=wave, frame_len=fl, shift=sh, pad=pad,
+                            spec=spec, back=back)
+        print(name, "spec", spec.shape, "round trip", float(np.abs(back - wave).max()))
     name, M, F, T, iters, seed = ICA_CASE
     x, W, _, _ = inputs(M, M, F, T, "jd", seed)
     Wo, Lo, Ho, nll = oracle.ica_fit(x, W, iters)

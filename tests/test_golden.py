@@ -17,6 +17,7 @@ import pytest
 GOLD = Path(__file__).resolve().parent / "golden"
 FIT_FILES = sorted(p.name for p in GOLD.glob("fit_*.npz"))
 BLOCK_FILES = sorted(p.name for p in GOLD.glob("block_*.npz"))
+STFT_FILES = sorted(p.name for p in GOLD.glob("stft_*.npz"))
 NLL_TOL = {"fp32": 1e-5, "fp64": 1e-10}
 SEP_TOL = {"fp32": 1e-3, "fp64": 1e-10}
 
@@ -35,7 +36,7 @@ def max_rel(a, b):
 
 
 def test_fixture_set_complete():
-    assert len(FIT_FILES) >= 8 and len(BLOCK_FILES) >= 2 and (GOLD / "ica_m2.npz").exists()
+    assert len(FIT_FILES) >= 8 and len(BLOCK_FILES) >= 2 and len(STFT_FILES) >= 2 and (GOLD / "ica_m2.npz").exists()
     g = load("fit_m2n3_em.npz")
     assert g["nll"].shape == (int(g["iters"]) + 1,) and "images" in g
 
@@ -137,3 +138,30 @@ def test_gpu_block_fit_matches_golden(gpu, name, precision):
     if precision == "fp64":
         assert rel_l2(r.params.loading, g["L"]) <= 1e-7
         assert rel_l2(r.params.decorr, g["W"]) <= 1e-7
+
+
+# ------------------------------------------------- STFT / iSTFT fixtures --
+@pytest.mark.parametrize("name", STFT_FILES)
+def test_oracle_reproduces_golden_stft(name):
+    import stft_oracle
+    g = load(name)
+    fl, sh, pad = int(g["frame_len"]), int(g["shift"]), int(g["pad"])
+    spec = stft_oracle.stft(g["wave"], fl, sh, pad)
+    assert np.abs(spec - g["spec"]).max() <= 1e-12 * np.abs(g["spec"]).max()
+    back = stft_oracle.istft(g["spec"], fl, sh, g["wave"].shape[1], pad)
+    assert np.abs(back - g["back"]).max() <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", STFT_FILES)
+def test_gpu_stft_istft_match_golden(gpu, name):
+    from paper_2101_08563_b200 import api
+    g = load(name)
+    fl, sh, pad = int(g["frame_len"]), int(g["shift"]), int(g["pad"])
+    n = g["wave"].shape[1]
+    spec = api.stft(api.MultichannelWave(g["wave"], 16000.0), fl, sh, pad)
+    assert spec.f.shape == g["spec"].shape
+    # fp64 FFTs on both sides: error grows like eps * log2(frame_len) * scale
+    assert np.abs(spec.f - g["spec"]).max() <= 1e-13 * np.abs(g["spec"]).max() * np.log2(fl)
+    back = api.istft(api.Spectrogram(g["spec"]), fl, sh, n, 16000.0, pad)
+    np.testing.assert_allclose(back.samples, g["back"], atol=1e-12)
