@@ -270,6 +270,48 @@ def fastfca_fit(covs: SampleCovSet, init: FastFcaParams, flavor: int, iters: int
                             status)
 
 
+def fastfca_fit_batch(covs: list[SampleCovSet], init: list[FastFcaParams], flavor: int,
+                      iters: int, fit: FitOptions | None = None,
+                      opts: FastFcaOptions | None = None, *, precision: str = "fp32",
+                      device: int | None = None) -> list[FastFcaFitResult]:
+    """Batch entry (config 4): equal to the loop of fastfca_fit
+    over the mixtures, run as ONE C-ABI call with dims.batch = len(covs) (the
+    C++ shim's fastfca_fit_batch on one device).  All mixtures share one shape."""
+    fit = fit or FitOptions()
+    opts = opts or FastFcaOptions()
+    if len(covs) != len(init):
+        raise InvalidArgument("fastfca_fit_batch: covariance/init count mismatch")
+    if not covs:
+        return []
+    c0, i0 = covs[0], init[0]
+    for c, p in zip(covs, init):
+        _check_shape(c, p, "fastfca_fit")
+        if (c.dim, c.bins, c.blocks, p.sources, c.has_snapshots(), c.power_scale is None) != \
+                (c0.dim, c0.bins, c0.blocks, i0.sources, c0.has_snapshots(), c0.power_scale is None):
+            raise InvalidArgument("fastfca_fit_batch: mixtures must share one shape")
+    if iters < 0:
+        raise InvalidArgument("fastfca_fit: negative iteration count")
+    B, F = len(covs), c0.bins
+    ins = [_covs_input(c) for c in covs]
+    x = np.ascontiguousarray(np.stack([t[0] for t in ins]))
+    power = None if ins[0][1] is None else np.ascontiguousarray(np.stack([t[1] for t in ins]))
+    refs = [_params_ref(p) for p in init]
+    W, L, H = (np.ascontiguousarray(np.stack([r[k] for r in refs])) for k in range(3))
+    d = _lib.Dims(B, F, c0.dim, i0.sources, c0.blocks)
+    o = _lib.FitOpts(int(flavor), int(iters), int(bool(fit.record_trace)), int(fit.seed),
+                     int(bool(opts.normalize_scales)), int(bool(opts.fix_loadings)),
+                     _prec(precision))
+    nll = np.zeros((B, iters + 1)) if fit.record_trace else None
+    status = np.zeros(B * F, np.int32)
+    ctx = _lib.context(device)
+    fn = _lib.lib().ffca_fit if ins[0][2] else _lib.lib().ffca_fit_covs
+    _lib.check(fn(ctx.handle, d, o, _lib.ptr(x), _lib.ptr(power), _lib.ptr(W), _lib.ptr(L),
+                  _lib.ptr(H), _lib.ptr(nll), None, _lib.ptr(status)))
+    return [FastFcaFitResult(_params_from_ref(W[b], L[b], H[b]),
+                             list(nll[b]) if nll is not None else [], status[b * F:(b + 1) * F])
+            for b in range(B)]
+
+
 def ica_mode_fit(covs: SampleCovSet, sources: int, iters: int, w_init: np.ndarray,
                  fit: FitOptions | None = None, *, precision: str = "fp32",
                  device: int | None = None) -> FastFcaFitResult:

@@ -61,6 +61,11 @@ STFT_CASES = {
 }
 
 
+# batch of independent mixtures (config 4's shape family, fastfca_fit_batch):
+# (batch, M, N, F, T, iters, seed)
+BATCH_CASE = ("batch3_m3n4_em", 3, 3, 4, 3, 313, 12, 25)
+
+
 def inputs(M, N, F, T, kind, seed):
     cfg = synth.small(M, N, F, T, seed=seed, kind=kind)
     x = synth.mixture(cfg).astype(np.complex64).astype(np.complex128)
@@ -97,6 +102,13 @@ def main() -> None:
         np.savez_compressed(HERE / f"{name}.npz", wave=wave, frame_len=fl, shift=sh, pad=pad,
                             spec=spec, back=back)
         print(name, "spec", spec.shape, "round trip", float(np.abs(back - wave).max()))
+    name, Bn, M, N, F, T, iters, seed = BATCH_CASE
+    cases = [inputs(M, N, F, T, "jd", seed + b) for b in range(Bn)]
+    x, W, L, H = (np.stack([c[k] for c in cases]) for k in range(4))
+    Wo, Lo, Ho, nll, _, _ = oracle.fit(x, W, L, H, iters)  # batched: the loop of fastfca_fit
+    np.savez_compressed(HERE / f"{name}.npz", x=x.astype(np.complex64), W0=W, L0=L, H0=H,
+                        iters=iters, W=Wo, L=Lo, H=Ho, nll=nll)
+    print(name, "nll", nll[:, 0], "->", nll[:, -1])
     name, M, F, T, iters, seed = ICA_CASE
     x, W, _, _ = inputs(M, M, F, T, "jd", seed)
     Wo, Lo, Ho, nll = oracle.ica_fit(x, W, iters)

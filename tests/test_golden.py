@@ -165,3 +165,36 @@ def test_gpu_stft_istft_match_golden(gpu, name):
     assert np.abs(spec.f - g["spec"]).max() <= 1e-13 * np.abs(g["spec"]).max() * np.log2(fl)
     back = api.istft(api.Spectrogram(g["spec"]), fl, sh, n, 16000.0, pad)
     np.testing.assert_allclose(back.samples, g["back"], atol=1e-12)
+
+
+# ------------------------------------------------ batch (config-4 family) --
+def test_oracle_reproduces_golden_batch(built):
+    import oracle
+    g = load("batch3_m3n4_em.npz")
+    Wo, Lo, Ho, nll, _, _ = oracle.fit(g["x"].astype(np.complex128), g["W0"], g["L0"], g["H0"],
+                                       int(g["iters"]))
+    assert max_rel(nll, g["nll"]) <= 1e-12
+    assert rel_l2(Ho, g["H"]) <= 1e-10 and rel_l2(Wo, g["W"]) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_gpu_fit_batch_matches_golden(gpu, precision):
+    """fastfca_fit_batch: one batched C-ABI call equals the per-mixture loop."""
+    from paper_2101_08563_b200 import api
+    g = load("batch3_m3n4_em.npz")
+    x = g["x"].astype(np.complex128)
+    covs = [api.sample_covs(api.Spectrogram(xb)) for xb in x]
+    init = [api.FastFcaParams(g["W0"][b], g["L0"][b], g["H0"][b]) for b in range(x.shape[0])]
+    rs = api.fastfca_fit_batch(covs, init, api.LhFlavor.em, int(g["iters"]), precision=precision)
+    assert len(rs) == x.shape[0]
+    for b, r in enumerate(rs):
+        assert max_rel(np.asarray(r.nll), g["nll"][b]) <= NLL_TOL[precision]
+        assert (r.bin_status == 0).all()
+        if precision == "fp64":
+            assert rel_l2(r.params.act, g["H"][b]) <= 1e-7
+    # the batch equals the loop of single fits
+    one = api.fastfca_fit(covs[1], init[1], api.LhFlavor.em, int(g["iters"]), precision=precision)
+    assert np.array_equal(np.asarray(one.nll), np.asarray(rs[1].nll))
+    with pytest.raises(api.InvalidArgument):
+        api.fastfca_fit_batch(covs, init[:2], api.LhFlavor.em, 3)
