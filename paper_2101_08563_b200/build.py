@@ -30,6 +30,20 @@ def _headers() -> list[Path]:
         sorted((ROOT / "include").rglob("*.h*"))
 
 
+def _includes(src: Path, seen: set | None = None) -> set:
+    """Local headers src includes, transitively (quoted includes only)."""
+    import re
+    seen = set() if seen is None else seen
+    for m in re.finditer(r'#include\s+"([^"]+)"', src.read_text()):
+        h = (src.parent / m.group(1)).resolve()
+        if not h.exists():
+            h = (ROOT / "include" / m.group(1)).resolve()
+        if h.exists() and h not in seen:
+            seen.add(h)
+            _includes(h, seen)
+    return seen
+
+
 def _stale(obj: Path, src: Path, deps: list[Path]) -> bool:
     if not obj.exists():
         return True
@@ -55,7 +69,6 @@ def build_lib(verbose: bool = False, jobs: int | None = None, variant: str = "",
     if variant.startswith("x_"):  # tuning experiments: FFCA_NVCC_EXTRA="-DFOO=1 ..."
         extra = os.environ.get("FFCA_NVCC_EXTRA", "").split()
     bdir.mkdir(exist_ok=True)
-    deps = _headers()
     cu = sorted(CSRC.glob("*.cu"))
     cpp = sorted(CSRC.glob("*.cpp"))
     jobs_list = []
@@ -67,12 +80,12 @@ def build_lib(verbose: bool = False, jobs: int | None = None, variant: str = "",
                 objs.append(BUILD / (src.stem + ".o"))
             continue
         objs.append(obj)
-        if _stale(obj, src, deps):
+        if _stale(obj, src, sorted(_includes(src))):
             jobs_list.append([NVCC, *ARCH, *NVFLAGS, *extra, "-c", str(src), "-o", str(obj)])
     for src in cpp:
         obj = bdir / (src.stem + ".cpp.o")
         objs.append(obj)
-        if _stale(obj, src, deps):
+        if _stale(obj, src, sorted(_includes(src))):
             jobs_list.append(["g++", *CXXFLAGS, "-c", str(src), "-o", str(obj)])
     saved, LIB = LIB, lib
     if jobs_list:

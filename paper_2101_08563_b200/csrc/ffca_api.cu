@@ -59,6 +59,9 @@ int grid_for(size_t n, int threads) {
 template <typename R>
 int launch_fit(ffca_ctx* ctx, int M, FitParams& fp, cudaStream_t st) {
   const bool fp64 = sizeof(R) == 8;
+  bool handled = false;
+  const int rc = launch_fit_big(ctx, fp, st, M, fp64, &handled);
+  if (rc != FFCA_OK || handled) return rc;
   switch (M) {
     case 1: return launch_fit_m1(ctx, fp, st, fp64);
     case 2: return launch_fit_m2(ctx, fp, st, fp64);

@@ -1,0 +1,68 @@
+// fit_big.cu -- instantiations and launcher of the large-bin fit kernel
+// (fit_big.cuh): M = 8, N = 12 (BASELINE config 3) in fp32 and the fp64
+// check mode.
+#include <cstdlib>
+
+#include "fit_big.cuh"
+#include "internal.hpp"
+
+namespace ffca {
+
+namespace {
+
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS>
+int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
+  using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
+  *handled = false;
+  int dev_max = 0;
+  cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (dev_max <= 0) dev_max = 227 * 1024;
+  const int C = (fp.T + Cfg::TCAP - 1) / Cfg::TCAP;
+  if (C < 1 || C > 16) return FFCA_OK;  // not handled: the streaming kernel takes it
+  const BigLayout lay = Cfg::layout(C);
+  if (lay.total > dev_max || !Cfg::fits_u(lay)) return FFCA_OK;
+  *handled = true;
+  if (fp.nprob == 0) return FFCA_OK;
+  if (C == 1) {
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false>;
+    FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+    kern<<<fp.nprob, NTHR, lay.total, st>>>(fp, lay);
+  } else {
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true>;
+    FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
+    if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(fp.nprob) * unsigned(C));
+    cfg.blockDim = dim3(NTHR);
+    cfg.dynamicSmemBytes = lay.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FFCA_CUDA(cudaLaunchKernelEx(&cfg, kern, fp, lay));
+  }
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  return FFCA_OK;
+}
+
+}  // namespace
+
+// The large-bin kernel takes IP+EM fits of snapshot records with the
+// shapes instantiated here; *handled = false leaves the fit to fit_kernel.
+int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp64, bool* handled) {
+  *handled = false;
+  if (getenv("FFCA_NO_BIG")) return FFCA_OK;  // A/B experiments against fit_kernel
+  if (fp.blk || fp.flavor != 0 || fp.fix_loadings) return FFCA_OK;
+  if (M == 8 && fp.N == 12) {
+    if (fp64) return launch_big_t<8, 12, double, 3, 384, 2>(ctx, fp, st, handled);
+    return launch_big_t<8, 12, float, 7, 384, 1>(ctx, fp, st, handled);
+  }
+  return FFCA_OK;
+}
+
+}  // namespace ffca

@@ -76,4 +76,7 @@ FFCA_DECLARE_FIT_LAUNCHER(6)
 FFCA_DECLARE_FIT_LAUNCHER(7)
 FFCA_DECLARE_FIT_LAUNCHER(8)
 
+// Large-bin kernel (fit_big.cu): sets *handled when it took the fit.
+int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp64, bool* handled);
+
 }  // namespace ffca

@@ -1,0 +1,97 @@
+"""GPU parity of the large-bin fit kernel (csrc/fit_big.cuh: M = 8, N = 12,
+BASELINE config 3's channel/source counts) against the fp64 oracle, through
+the C-ABI.  Frame counts are chosen so the bin runs on one CTA and on 2-7 CTA
+clusters (fp32: 2688 frames per CTA, fp64: 1152).
+
+Tolerances (BASELINE.json north_star): fp32 NLL 1e-5 relative per iteration
+and separated STFTs 1e-3 relative L2; fp64 check mode 1e-10 for both.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2101_08563_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+
+NLL_TOL = {"fp32": 1e-5, "fp64": 1e-10}
+SEP_TOL = {"fp32": 1e-3, "fp64": 1e-10}
+
+
+def make_case(F, T, seed, sigma_v=2.0):
+    cfg = synth.small(8, 12, F, T, seed=seed, sigma_v=sigma_v)
+    x = synth.mixture(cfg).astype(np.complex128)
+    W, L, H = synth.init_params(cfg)
+    return x, W, L, H
+
+
+def fit(x, W, L, H, iters, precision, **kw):
+    covs = api.sample_covs(api.Spectrogram(x))
+    fo = api.FitOptions(record_trace=kw.pop("record_trace", True), seed=kw.pop("seed", 0))
+    oo = api.FastFcaOptions(**kw)
+    return api.fastfca_fit(covs, api.FastFcaParams(W, L, H), api.LhFlavor.em, iters, fo, oo,
+                           precision=precision)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("T", [700, 3000, 8000])
+def test_big_fit_trace_and_separation(gpu, precision, T):
+    iters = 5 if T == 8000 else 8
+    x, W, L, H = make_case(2, T, seed=T)
+    r = fit(x, W, L, H, iters, precision)
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, iters)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision], (rel.max(), int(rel.argmax()))
+    assert (r.bin_status == 0).all()
+    img_g = api.fastfca_separate(api.Spectrogram(x), r.params, precision=precision)
+    img_o = oracle.separate(x, Wo, Lo, Ho)
+    for n in range(12):
+        assert rel_l2(img_g[n].f, img_o[n]) <= SEP_TOL[precision], n
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_big_fit_options(gpu, precision):
+    """normalize_scales off, record_trace off, iters = 0 (fastfca.cpp:146-191)."""
+    x, W, L, H = make_case(2, 3000, seed=5)
+    r = fit(x, W, L, H, 4, precision, normalize_scales=False)
+    _, _, _, nll_o, _, _ = oracle.fit(x, W, L, H, 4, normalize_scales=False)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision]
+    r2 = fit(x, W, L, H, 4, precision, record_trace=False)
+    assert len(r2.nll) == 0
+    r1 = fit(x, W, L, H, 4, precision)
+    for a, b in zip(r2.params.act, r1.params.act):
+        assert np.array_equal(a, b)  # the trace does not change the fit
+    r0 = fit(x, W, L, H, 0, precision)
+    assert len(r0.nll) == 1
+    for a, b in zip(r0.params.act, [h for h in H]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_big_silent_bin_untouched(gpu, precision):
+    x, W, L, H = make_case(3, 3000, seed=9)
+    x[1] = 0.0
+    r = fit(x, W, L, H, 3, precision)
+    _, _, _, nll_o, _, _ = oracle.fit(x, W, L, H, 3)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision]
+    assert np.array_equal(r.params.act[1], H[1])
+    assert np.array_equal(r.params.decorr[1], W[1])
+
+
+def test_big_matches_cluster_kernel(gpu, monkeypatch):
+    """The large-bin kernel and the round-1 cluster kernel (FFCA_NO_BIG) run the
+    same algorithm: their fp32 traces agree to the parity tolerance."""
+    x, W, L, H = make_case(3, 6000, seed=13)
+    r_big = fit(x, W, L, H, 6, "fp32")
+    monkeypatch.setenv("FFCA_NO_BIG", "1")
+    r_old = fit(x, W, L, H, 6, "fp32")
+    a, b = np.asarray(r_big.nll), np.asarray(r_old.nll)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5

@@ -19,6 +19,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 PHASES = ["A frames", "A reduce", "IP serial", "iter sync", "EM frames", "EM barrier",
           "EM update", "balance", "EM sum", "init"]
+# fit_big.cuh (M = 8, N = 12 large-bin kernel) phase order
+PHASES_BIG = ["U pass", "EM frames", "EM reduce", "balance", "A1", "A2 frames", "A2 reduce",
+              "IP", "iter sync", "init"]
 
 
 def main() -> None:
@@ -30,6 +33,7 @@ def main() -> None:
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--phases", action="store_true")
+    ap.add_argument("--big", action="store_true", help="phase names of the large-bin kernel")
     a = ap.parse_args()
     import torch
     from paper_2101_08563_b200 import _lib, synth
@@ -89,7 +93,7 @@ def main() -> None:
         tot = c.sum(axis=1)
         print("phase cycles per bin (mean over bins, per iteration):")
         for k in range(10):
-            print(f"  {PHASES[k]:<11} {c[:, k].mean() / iters:10.0f}  ({100 * c[:, k].sum() / tot.sum():5.1f} %)")
+            print(f"  {(PHASES_BIG if a.big else PHASES)[k]:<11} {c[:, k].mean() / iters:10.0f}  ({100 * c[:, k].sum() / tot.sum():5.1f} %)")
 
 
 if __name__ == "__main__":
