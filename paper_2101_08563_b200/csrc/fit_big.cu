@@ -20,7 +20,7 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
   const int C = (fp.T + Cfg::TCAP - 1) / Cfg::TCAP;
   if (C < 1 || C > 16) return FFCA_OK;  // not handled: the streaming kernel takes it
   const BigLayout lay = Cfg::layout(C);
-  if (lay.total > dev_max || !Cfg::fits_u(lay)) return FFCA_OK;
+  if (lay.total > dev_max) return FFCA_OK;
   *handled = true;
   if (fp.nprob == 0) return FFCA_OK;
   if (C == 1) {
@@ -59,8 +59,8 @@ int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp
   if (getenv("FFCA_NO_BIG")) return FFCA_OK;  // A/B experiments against fit_kernel
   if (fp.blk || fp.flavor != 0 || fp.fix_loadings) return FFCA_OK;
   if (M == 8 && fp.N == 12) {
-    if (fp64) return launch_big_t<8, 12, double, 3, 384, 2>(ctx, fp, st, handled);
-    return launch_big_t<8, 12, float, 7, 384, 1>(ctx, fp, st, handled);
+    if (fp64) return launch_big_t<8, 12, double, 4, 448, 2>(ctx, fp, st, handled);
+    return launch_big_t<8, 12, float, 8, 512, 1>(ctx, fp, st, handled);
   }
   return FFCA_OK;
 }

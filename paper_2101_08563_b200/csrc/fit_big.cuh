@@ -3,38 +3,45 @@
 //
 // Same per-bin algorithm as fit_kernel.cuh (one CTA group owns one frequency
 // problem for every iteration of fastfca_fit, reference src/fastfca.cpp:
-// 158-184), re-laid-out for bins whose records do not fit one SM:
+// 158-184), laid out for bins whose per-frame state does not fit one SM's
+// shared memory.  The per-iteration serial chain (N + 1 reductions and the IP
+// sweep) is paid once per SM group, so the design goal is the fewest SMs per
+// bin: every per-frame array lives on chip, split over the SM's three stores:
 //
-//  * Per-frame state is split between shared memory and registers so a bin
-//    needs as few SMs as possible (the per-iteration serial chain -- 13
-//    reductions and the IP sweep -- is paid once per SM group, so fewer SMs
-//    per bin means more bins in flight and less idle time):
-//      H   [NHP planes][t] 16-byte vectors   shared   (persistent, in/out)
-//      U   [NUP planes][t] 16-byte vectors   shared   (|W^H x|^2, then 1/sigma^2)
-//      Phi [SLOTS][M]                        registers (posterior of the
+//      H    [NHP planes][t] 16-byte vectors  shared memory (persistent, in/out)
+//      U    [slot] M values                  tensor memory (|W^H x|^2, then 1/sigma^2)
+//      Phi  [slot] M values                  tensor memory (posterior of the
 //                                            current source, sweep to sweep)
-//      x   [t][M] complex                    global (L2-resident: ~0.5 MB per
+//      x    [t][M] complex                   global (L2-resident: ~0.5 MB per
 //                                            bin, read twice per iteration)
-//    For c3 in fp32 that is 215 KB of shared memory per CTA and a 3-CTA
-//    cluster per bin (448 threads x 6 frame slots = 2688 frames per CTA).
-//  * Two thread-to-frame mappings.  The EM sweeps and the variance pass use
-//    one thread per frame (SLOTS frames per thread, fixed across sweeps so the
-//    posterior stays in registers).  The two passes that read x use M lanes
-//    per frame: the decorrelation pass (lane j owns channel j: y_j = w_j^H x
-//    with w_j in registers) and the weighted-covariance pass, where lane a
-//    forms the products x_a conj(x_{a+d mod M}), d = 0..M/2 -- every entry of
-//    the Hermitian outer product exactly once (the d = M/2 products of lanes
-//    a >= M/2 are the only duplicates) -- and accumulates them against all M
-//    weights 1/sigma^2_m (a [M x T] . [T x M^2] product with no recomputed
-//    outer products).
+//
+// Tensor memory (256 KB per SM, unused by this non-GEMM path otherwise) is the
+// lever: thread (warp w, lane l) owns TMEM lane 32 (w % 4) + l and a 128-column
+// strip per warp group, and moves a frame's U and Phi with one 32x32b
+// tcgen05.ld / tcgen05.st.  For c3 in fp32 a CTA holds 4096 frames (512
+// threads x 8 slots): a bin needs a 2-CTA cluster and all 148 SMs are used
+// (74 bins in flight).
+//
+// Two thread-to-frame mappings, both warp-local (a warp only ever touches the
+// frames its lanes own, so no barrier separates the passes):
+//  * one thread per frame (slots s: frame 32 w + lane + s NTHR) for the EM
+//    sweeps and the variance pass;
+//  * M lanes per frame for the two passes that read x -- the decorrelation
+//    pass (lane j owns channel j: y_j = w_j^H x with w_j in registers; the
+//    owner lane gathers U with shuffles) and the weighted-covariance pass,
+//    where lane a forms x_a conj(x_{a+d mod M}), d = 0..M/2 -- every entry of
+//    the Hermitian outer product once (the d = M/2 products of lanes a >= M/2
+//    are the only duplicates) -- and accumulates them against the M weights
+//    1/sigma^2_m shuffled from the owner lane (a [M x T] . [T x M^2] product
+//    with no recomputed outer products).
 //
 // Per iteration (fastfca.cpp:172-183):
-//   IP       warp 0: ip_update_warp_reg (serial_math.cuh), the reference's
-//            column sweep with the seeded restart (fastfca.cpp:36-72), on the
-//            cluster-reduced weighted covariances.
+//   IP       ip_fast.cuh (Q^{-1} and W^{-H} in parallel, Sherman-Morrison
+//            column chain; the reference's column solves with the seeded
+//            restart as the fallback, fastfca.cpp:36-72).
 //   U        decorrelated powers U = |W^H x|^2 (sigmodel.cpp:93-107).
 //   EM       N sweeps (em_update_lh, fastfca.cpp:80-99): sweep n finishes H
-//            row n-1 from the registered posterior and the freshly reduced L
+//            row n-1 from the stored posterior and the freshly reduced L
 //            column, forms the posterior of source n and reduces its L column.
 //   balance  every warp, lane-parallel (fastfca.cpp:127-142); H row scales
 //            are folded into the effective loadings (lazy), W column scales
@@ -51,16 +58,18 @@
 
 #include "common.cuh"
 #include "fit_kernel.cuh"
+#include "ip_fast.cuh"
 #include "serial_math.cuh"
 
 namespace ffca {
 
 // Shared-memory carve-up of a big-bin CTA (byte offsets), computed on the host.
 struct BigLayout {
-  int off_h, off_u, ps;  // planes: ps 16-byte vectors per plane
+  int off_h, ps;  // H planes: ps 16-byte vectors per plane
   int off_le, off_ld, off_hsc, off_hinv, off_linv, off_us, off_wsc, off_hsum, off_psum;
-  int off_wd, off_wr, off_q, off_ipscr, off_ldscr, off_red, off_cx, off_scal;
-  int off_gscr, off_ex, off_rng;  // inside the U region (dead while used)
+  int off_wd, off_wr, off_ipscr, off_ldscr, off_red, off_cx, off_scal;
+  int off_scr;                                    // reused scratch region:
+  int off_gscr, off_ex, off_q, off_ipf, off_rng;  //   covariance tree, then the rest
   int total;
   int csize, tcap;
 };
@@ -69,11 +78,16 @@ template <typename R> struct Vec16;
 template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
 
+constexpr int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
 template <int M, int N, typename R, int SLOTS, int NTHR, int MS>
 struct BigCfg {
   static constexpr int VE = Vec16<R>::n;           // reals per 16-byte vector
   static constexpr int NHP = (N + VE - 1) / VE;    // H planes
-  static constexpr int NUP = M / VE;               // U planes
   static constexpr int NW = NTHR / 32;
   static constexpr int TCAP = NTHR * SLOTS;        // frames per CTA
   static constexpr int D = M / 2;                  // cyclic product distances
@@ -82,23 +96,30 @@ struct BigCfg {
   static constexpr int KA = NP * MW;               // accumulators per covariance lane
   static constexpr int GS = M * MS;                // covariance lanes per frame
   static constexpr int KRED = 2 * M + 1;           // EM sweep partials
-  static constexpr int KQ = M * M * M + M + 1;     // covariance + NLL totals
-  static_assert(M % VE == 0, "channel planes");
+  static constexpr int KQ = M * M * M;             // covariance totals
+  static constexpr int WPR = M * int(sizeof(R)) / 4;  // TMEM columns per record
+  static constexpr int SCOL = 2 * WPR;             // columns per slot (U, Phi)
+  static constexpr int WGROUPS = (NW + 3) / 4;     // warps sharing a TMEM lane quarter
+  static constexpr int PW = pow2_at_least(NW);
+  static constexpr int HW = PW / 2 > 0 ? PW / 2 : 1;  // warps publishing in the first tree step
+  static constexpr int CNT = [] {
+    int c = KA;
+    for (int o = 16; o >= GS; o >>= 1) c /= 2;
+    return c;
+  }();  // covariance partials per lane after the in-warp reduce-scatter
   static_assert(32 % GS == 0 && 32 % M == 0, "lanes per frame must divide a warp");
   static_assert(NTHR % 32 == 0, "whole warps");
+  static_assert(SLOTS * SCOL * WGROUPS <= 512, "tensor memory columns");
+  static_assert(WPR == 8 || WPR == 16, "record width");
 
   static int al(int v) { return (v + 15) & ~15; }
   static BigLayout layout(int csize) {
     BigLayout L{};
     L.csize = csize;
     L.tcap = TCAP;
-    // plane stride = TCAP + 4 vectors: consecutive planes start 16 banks apart,
-    // so the decorrelation pass's scalar stores (4 frames x 2 planes per warp)
-    // are conflict-free.
-    L.ps = TCAP + ((TCAP % 8 == 0) ? 4 : (12 - TCAP % 8) % 8);
+    L.ps = TCAP + 4;  // planes start 16 banks apart
     int o = 0;
     L.off_h = o; o = al(o + NHP * L.ps * 16);
-    L.off_u = o; o = al(o + NUP * L.ps * 16);
     const int rs = int(sizeof(R));
     L.off_le = o; o = al(o + N * M * rs);
     L.off_ld = o; o = al(o + 2 * M * N * rs);
@@ -111,28 +132,32 @@ struct BigCfg {
     L.off_psum = o; o = al(o + M * rs);
     L.off_wd = o; o = al(o + M * M * 16);
     L.off_wr = o; o = al(o + M * M * 2 * rs);
-    L.off_q = o; o = al(o + M * M * M * 8);
     L.off_ipscr = o; o = al(o + M * M * 2 * rs);
     L.off_ldscr = o; o = al(o + M * (M + 1) * 2 * rs);
     L.off_red = o; o = al(o + 2 * NW * KRED * rs);
     L.off_cx = o; o = al(o + 2 * csize * KRED * 8);
     L.off_scal = o; o = al(o + 128);
+    // Scratch, reused: the covariance tree (HW warps' partials), then the
+    // CTA totals ex[] (read by the other CTAs of the cluster), the cluster
+    // totals qraw[], the fast-IP scratch and the restart generator.
+    L.off_scr = o;
+    const int gscr = HW * 32 * CNT * rs;
+    L.off_gscr = o;
+    L.off_ex = o;
+    int e = al(o + (KQ + 2 * (M + 1)) * 8);
+    L.off_q = e; e = al(e + KQ * 8);
+    L.off_ipf = e; e = al(e + int(sizeof(IpFastScratch<M, R>)));
+    L.off_rng = e; e = al(e + int(sizeof(RestartRng)));
+    o = al(o + gscr) > e ? al(o + gscr) : e;
     L.total = o;
-    // Inside the U region: covariance scratch, the CTA totals (read by the
-    // other CTAs of the cluster) and the IP restart generator.
-    L.off_gscr = L.off_u;
-    L.off_ex = al(L.off_gscr + NW * GS * KA * int(sizeof(R)));
-    L.off_rng = al(L.off_ex + (KQ + M + 1) * 8);
     return L;
-  }
-  static bool fits_u(const BigLayout& L) {
-    return L.off_rng + int(sizeof(RestartRng)) <= L.off_u + NUP * L.ps * 16;
   }
 };
 
 struct BigScalars {
   double eps, nll0, logdet0, logs;
   int stop, status, ldok;
+  unsigned tmem;
 };
 
 // Fixed-order pairwise sum of the per-warp partials red[w*K + k], w < NW
@@ -152,8 +177,95 @@ __device__ __forceinline__ T tree_sum_any(const T* red, int K, int k) {
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------- TMEM --
+// 32x32b register transfers: thread l of the warp reads / writes TMEM lane
+// (quarter base + l), columns [col, col + n).  Raw 32-bit words; a double is
+// two columns (low word first).
+__device__ __forceinline__ void tm_ld8(unsigned a, unsigned (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(a));
+}
+__device__ __forceinline__ void tm_ld16(unsigned a, unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(a));
+}
+__device__ __forceinline__ void tm_st8(unsigned a, const unsigned (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(a),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st16(unsigned a, const unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(a),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// One record of M values in the compute type.
+template <int M, typename R>
+__device__ __forceinline__ void tm_load_rec(unsigned a, R (&v)[M]) {
+  static_assert(M == 8, "records are 8 values");
+  if constexpr (sizeof(R) == 4) {
+    unsigned w[8];
+    tm_ld8(a, w);
+    tm_wait_ld();
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = __uint_as_float(w[m]);
+  } else {
+    unsigned w[16];
+    tm_ld16(a, w);
+    tm_wait_ld();
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = __hiloint2double(int(w[2 * m + 1]), int(w[2 * m]));
+  }
+}
+// Two adjacent records (U then Phi) in one transfer.
+template <int M, typename R>
+__device__ __forceinline__ void tm_load_rec2(unsigned a, R (&u)[M], R (&ph)[M]) {
+  if constexpr (sizeof(R) == 4) {
+    unsigned w[16];
+    tm_ld16(a, w);
+    tm_wait_ld();
+#pragma unroll
+    for (int m = 0; m < M; ++m) u[m] = __uint_as_float(w[m]), ph[m] = __uint_as_float(w[M + m]);
+  } else {
+    tm_load_rec<M, R>(a, u);
+    tm_load_rec<M, R>(a + 16, ph);
+  }
+}
+template <int M, typename R>
+__device__ __forceinline__ void tm_store_rec(unsigned a, const R (&v)[M]) {
+  if constexpr (sizeof(R) == 4) {
+    unsigned w[8];
+#pragma unroll
+    for (int m = 0; m < M; ++m) w[m] = __float_as_uint(v[m]);
+    tm_st8(a, w);
+  } else {
+    unsigned w[16];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      w[2 * m] = unsigned(__double2loint(v[m]));
+      w[2 * m + 1] = unsigned(__double2hiint(v[m]));
+    }
+    tm_st16(a, w);
+  }
 }
 
 template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL>
@@ -161,14 +273,18 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
   using C = cplx_t<R>;
   using V = typename Vec16<R>::type;
-  constexpr int VE = Cfg::VE, NHP = Cfg::NHP, NUP = Cfg::NUP, NW = Cfg::NW;
+  constexpr int VE = Cfg::VE, NHP = Cfg::NHP, NW = Cfg::NW, PW = Cfg::PW, HW = Cfg::HW;
   constexpr int D = Cfg::D, NP = Cfg::NP, MW = Cfg::MW, KA = Cfg::KA, GS = Cfg::GS;
-  constexpr int KRED = Cfg::KRED;
+  constexpr int KRED = Cfg::KRED, KQ = Cfg::KQ, WPR = Cfg::WPR, SCOL = Cfg::SCOL, CNT = Cfg::CNT;
   using B = R;
   using BM = SMath<B>;
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // Provably warp-uniform (a shuffle from lane 0), so branches on the warp
+  // index stay convergent and shuffles inside them need no collective
+  // fallback code.
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   int crank = 0, csize = 1;
   if constexpr (CL) {
     const cg::cluster_group cl = cg::this_cluster();
@@ -203,9 +319,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
 #endif
 
   V* Hp = reinterpret_cast<V*>(smem + lay.off_h);
-  V* Up = reinterpret_cast<V*>(smem + lay.off_u);
   R* Hs = reinterpret_cast<R*>(Hp);
-  R* Us = reinterpret_cast<R*>(Up);
   R* Le = reinterpret_cast<R*>(smem + lay.off_le);  // [N][M]: column n at Le + n M
   B* const Ld0 = reinterpret_cast<B*>(smem + lay.off_ld);
   B* const hsc0 = reinterpret_cast<B*>(smem + lay.off_hsc);
@@ -217,7 +331,6 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   B* psum = reinterpret_cast<B*>(smem + lay.off_psum);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
-  double* qraw = reinterpret_cast<double*>(smem + lay.off_q);
   C* ipscr = reinterpret_cast<C*>(smem + lay.off_ipscr);
   C* ldscr = reinterpret_cast<C*>(smem + lay.off_ldscr);
   R* red = reinterpret_cast<R*>(smem + lay.off_red);
@@ -225,6 +338,8 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   BigScalars* sc = reinterpret_cast<BigScalars*>(smem + lay.off_scal);
   R* gscr = reinterpret_cast<R*>(smem + lay.off_gscr);
   double* ex = reinterpret_cast<double*>(smem + lay.off_ex);
+  double* qraw = reinterpret_cast<double*>(smem + lay.off_q);
+  IpFastScratch<M, R>* ipf = reinterpret_cast<IpFastScratch<M, R>*>(smem + lay.off_ipf);
   RestartRng* rng = reinterpret_cast<RestartRng*>(smem + lay.off_rng);
   B* Ld = Ld0;
   B* hsc = hsc0;
@@ -234,6 +349,12 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   const C* xg = reinterpret_cast<const C*>(p.x) + (size_t(b) * T + t0g) * M;
   R* Hg = reinterpret_cast<R*>(p.H) + (size_t(b) * T + t0g) * N;
 
+  // ---- tensor memory: all 512 columns (one CTA per SM).
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        unsigned(__cvta_generic_to_shared(&sc->tmem))));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
   // ---- load the bin: H into planes (pad entries 0), W, L, scalars.
   for (int k = tid; k < NHP * VE * Tl; k += NTHR) {
     const int t = k / (NHP * VE), e = k - t * (NHP * VE);
@@ -259,7 +380,14 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     sc->ldok = 1;
     sc->logs = 0.0;
   }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  // This thread's TMEM strip: lane quarter (warp % 4), columns of its warp group.
+  const unsigned tmrow =
+      sc->tmem + (unsigned(32 * (warp & 3)) << 16) + unsigned((warp >> 2) * SLOTS * SCOL);
+  auto tm_u = [&](int s) { return tmrow + unsigned(s * SCOL); };          // U (then 1/sigma^2)
+  auto tm_phi = [&](int s) { return tmrow + unsigned(s * SCOL + WPR); };  // posterior
   const R eps = R(sc->eps);
   const double invT = 1.0 / double(T);
   const int bin_index = (p.seed_bin0 + b) % p.F;  // mix_seed index (fastfca.cpp:40)
@@ -267,15 +395,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   const bool silent = !(power > 0.0);
   const bool bal = p.normalize != 0;
 
-  // ---- cluster helpers
-  auto cl_sync = [&]() {
-    if constexpr (CL) {
-      cluster_arrive();
-      cluster_wait();
-    }
-  };
-
-  // ---- frame records, thread-per-frame mapping
+  // ---- frame records
   auto load_h = [&](int t, R (&h)[NHP * VE]) {
 #pragma unroll
     for (int q = 0; q < NHP; ++q) {
@@ -287,33 +407,10 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       }
     }
   };
-  auto load_u = [&](int t, R (&u)[M]) {
-#pragma unroll
-    for (int q = 0; q < NUP; ++q) {
-      const V v = Up[q * ps + t];
-      if constexpr (VE == 4) {
-        u[q * 4] = v.x, u[q * 4 + 1] = v.y, u[q * 4 + 2] = v.z, u[q * 4 + 3] = v.w;
-      } else {
-        u[q * 2] = v.x, u[q * 2 + 1] = v.y;
-      }
-    }
-  };
-  auto store_u = [&](int t, const R (&u)[M]) {
-#pragma unroll
-    for (int q = 0; q < NUP; ++q) {
-      V v;
-      if constexpr (VE == 4) {
-        v.x = u[q * 4], v.y = u[q * 4 + 1], v.z = u[q * 4 + 2], v.w = u[q * 4 + 3];
-      } else {
-        v.x = u[q * 2], v.y = u[q * 2 + 1];
-      }
-      Up[q * ps + t] = v;
-    }
-  };
   auto hidx = [&](int n, int t) { return ((n / VE) * ps + t) * VE + (n % VE); };
-  // Loading column k of the effective loadings as vectors.  Volatile shared
-  // loads: re-read per frame from the broadcast bank instead of being hoisted
-  // into 12 x M registers the frame loops cannot afford.
+  // Column k of the effective loadings as vectors.  Volatile shared loads:
+  // re-read per frame from the broadcast bank instead of being hoisted into
+  // 12 x M registers the frame loops cannot afford.
   auto load_le = [&](int k, R (&l)[M]) {
     const unsigned a = unsigned(__cvta_generic_to_shared(Le + k * M));
 #pragma unroll
@@ -341,51 +438,61 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       for (int m = 0; m < M; ++m) lh[m] += l[m] * h[k];
     }
   };
-
-  // Posterior of the current source, per frame slot (registers).
-  R phi[SLOTS][M];
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s)
-#pragma unroll
-    for (int m = 0; m < M; ++m) phi[s][m] = R(0);
+  auto frame_of = [&](int s, int owner) { return warp * 32 + owner + s * NTHR; };
 
   // ---------------------------------------------------- decorrelation pass --
-  // U(j, t) = |w_j^H x_t|^2: M lanes per frame, lane j owns column j of W.
+  // U(j, t) = |w_j^H x_t|^2: M lanes per frame, lane j owns column j of W;
+  // the frame's owner lane gathers its M values and stores them to TMEM.
   auto u_pass = [&]() {
-    const int j = lane % M;
-    const int g = (warp * 32 + lane) / M;
-    constexpr int NG = NTHR / M;
+    constexpr int FPB = 32 / M;  // frames per batch
+    const int j = lane % M, g = lane / M;
     C wc[M];
 #pragma unroll
     for (int c = 0; c < M; ++c) wc[c] = Wr[c + j * M];
-    R* ucol = Us + (j / VE) * ps * VE + (j % VE);
-#pragma unroll 2
-    for (int t = g; t < Tl; t += NG) {
-      const V* xv = reinterpret_cast<const V*>(xg + size_t(t) * M);
-      C xc[M];
+#pragma unroll 1
+    for (int s = 0; s < SLOTS; ++s) {
+      R uo[M];
 #pragma unroll
-      for (int q = 0; q < M * 2 / VE; ++q) {
-        const V v = __ldg(xv + q);
-        if constexpr (VE == 4) {
-          xc[2 * q] = mkc<R>(v.x, v.y);
-          xc[2 * q + 1] = mkc<R>(v.z, v.w);
-        } else {
-          xc[q] = mkc<R>(v.x, v.y);
+      for (int m = 0; m < M; ++m) uo[m] = R(0);
+#pragma unroll
+      for (int bb = 0; bb < 32 / FPB; ++bb) {
+        const int t0 = frame_of(s, bb * FPB + g);
+        const int t = t0 < Tl ? t0 : 0;
+        const V* xv = reinterpret_cast<const V*>(xg + size_t(t) * M);
+        C xc[M];
+#pragma unroll
+        for (int q = 0; q < M * 2 / VE; ++q) {
+          const V v = __ldg(xv + q);
+          if constexpr (VE == 4) {
+            xc[2 * q] = mkc<R>(v.x, v.y);
+            xc[2 * q + 1] = mkc<R>(v.z, v.w);
+          } else {
+            xc[q] = mkc<R>(v.x, v.y);
+          }
+        }
+        R yr = wc[0].x * xc[0].x + wc[0].y * xc[0].y;
+        R yi = wc[0].x * xc[0].y - wc[0].y * xc[0].x;
+#pragma unroll
+        for (int c = 1; c < M; ++c) {
+          yr += wc[c].x * xc[c].x + wc[c].y * xc[c].y;
+          yi += wc[c].x * xc[c].y - wc[c].y * xc[c].x;
+        }
+        const R uval = yr * yr + yi * yi;
+        // owner lane bb*FPB + g' takes channel m from lane g'*M + m
+        const bool mine = (lane / FPB) == bb;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const R v = __shfl_sync(0xffffffffu, uval, (lane % FPB) * M + m);
+          uo[m] = mine ? v : uo[m];
         }
       }
-      R yr = wc[0].x * xc[0].x + wc[0].y * xc[0].y;
-      R yi = wc[0].x * xc[0].y - wc[0].y * xc[0].x;
-#pragma unroll
-      for (int c = 1; c < M; ++c) {
-        yr += wc[c].x * xc[c].x + wc[c].y * xc[c].y;
-        yi += wc[c].x * xc[c].y - wc[c].y * xc[c].x;
-      }
-      ucol[t * VE] = yr * yr + yi * yi;
+      tm_store_rec<M, R>(tm_u(s), uo);
     }
+    tm_wait_st();
   };
 
   // ---------------------------------------------------- EM sweep n --------
-  // Ends with the per-warp partials in red[par] and ONE barrier.
+  // Ends with the per-warp partials in rd and ONE barrier.
   auto em_sweep = [&](int n, bool phis, R* rd) {
     R linv[M];
 #pragma unroll
@@ -395,40 +502,41 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     R acc[KRED];
 #pragma unroll
     for (int k = 0; k < KRED; ++k) acc[k] = R(0);
-    // Branch-free over the frame slots: a slot past the CTA's frame range
-    // computes on frame 0 with its posterior forced to 0 and its stores and
-    // sums masked (no divergent joins for the register allocator to merge).
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < SLOTS; ++s) {
-      const int t0 = tid + s * NTHR;
+      const int t0 = frame_of(s, lane);
       const bool ok = t0 < Tl;
       const int t = ok ? t0 : 0;
+      R u[M], php[M];
+      tm_load_rec2<M, R>(tm_u(s), u, php);
       if (n > 0) {  // H row n-1 (fastfca.cpp:95-97), stored before the row is read
-        R sum = phi[s][0] * linv[0];
+        R sum = php[0] * linv[0];
 #pragma unroll
-        for (int m = 1; m < M; ++m) sum += phi[s][m] * linv[m];
+        for (int m = 1; m < M; ++m) sum += php[m] * linv[m];
         R hn1 = sum * R(1.0 / M);
         hn1 = hn1 > tiny<R>() ? hn1 : tiny<R>();
         if (ok) Hs[hidx(n - 1, t)] = hn1;
         acc[M] += ok ? hn1 : R(0);
       }
-      R h[NHP * VE], u[M], lh[M];
+      R h[NHP * VE], lh[M];
       load_h(t, h);
-      load_u(t, u);
       mix_var(h, lh);
       const R hn = Hs[hidx(n, t)];
       const R ihn = rcp_fast(hn);
+      R ph[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const R lnhn = lc[m] * hn;
         const R gg = lnhn * rcp_fast(lh[m]);
-        R ph = gg * (gg * u[m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
-        ph = ok ? ph : R(0);
-        phi[s][m] = ph;
-        acc[m] += ph * ihn;
-        if (phis) acc[M + 1 + m] += ph;
+        R v = gg * (gg * u[m] - lnhn) + lnhn;  // G^2 U + (1 - G) L_n H_n
+        v = ok ? v : R(0);
+        ph[m] = v;
+        acc[m] += v * ihn;
+        if (phis) acc[M + 1 + m] += v;
       }
+      tm_store_rec<M, R>(tm_phi(s), ph);
     }
+    tm_wait_st();
     if (phis) {
       warp_reduce_store<KRED>(acc, rd + warp * KRED, lane);
     } else {
@@ -441,16 +549,22 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   };
 
   // CTA totals of K partials (lane k), then cluster totals in rank order.
-  // Every warp calls this; returns lane k's total (0 for k >= K).
+  // Every warp calls this; returns lane k's total (0 for k >= K).  Only warp
+  // 0 writes remote slots, so only it needs release semantics.
   auto reduce_tot = [&](const R* rd, int K, int cbuf) -> R {
     R tot = (lane < K) ? tree_sum_any<NW>(rd, KRED, lane) : R(0);
     if constexpr (CL) {
       namespace cg = cooperative_groups;
       cg::cluster_group cl = cg::this_cluster();
       double* slot = cx + cbuf * (csize * KRED) + crank * KRED;
-      if (warp == 0 && lane < K)
-        for (int r = 0; r < csize; ++r) cl.map_shared_rank(slot, r)[lane] = double(tot);
-      cl_sync();
+      if (warp == 0) {
+        if (lane < K)
+          for (int r = 0; r < csize; ++r) cl.map_shared_rank(slot, r)[lane] = double(tot);
+        cluster_arrive();
+      } else {
+        cluster_arrive_relaxed();
+      }
+      cluster_wait();
       double s = 0.0;
       if (lane < K)
         for (int r = 0; r < csize; ++r) s += cx[cbuf * (csize * KRED) + r * KRED + lane];
@@ -468,22 +582,23 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     for (int m = 0; m < M; ++m) linv[m] = finish ? Linv[m] : R(0);
 #pragma unroll
     for (int k = 0; k <= M; ++k) nacc[k] = R(0);
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < SLOTS; ++s) {
-      const int t0 = tid + s * NTHR;
+      const int t0 = frame_of(s, lane);
       const bool ok = t0 < Tl;
       const int t = ok ? t0 : 0;
+      R u[M], php[M];
+      tm_load_rec2<M, R>(tm_u(s), u, php);
       if (finish) {
-        R sum = phi[s][0] * linv[0];
+        R sum = php[0] * linv[0];
 #pragma unroll
-        for (int m = 1; m < M; ++m) sum += phi[s][m] * linv[m];
+        for (int m = 1; m < M; ++m) sum += php[m] * linv[m];
         R hn1 = sum * R(1.0 / M);
         hn1 = hn1 > tiny<R>() ? hn1 : tiny<R>();
         if (ok) Hs[hidx(N - 1, t)] = hn1;
       }
-      R h[NHP * VE], u[M], lh[M];
+      R h[NHP * VE], lh[M];
       load_h(t, h);
-      load_u(t, u);
       mix_var(h, lh);
       R r[M];
       R lsum = R(0);
@@ -494,19 +609,20 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
         lsum += flog2_ftz(lh[m]);
       }
       nacc[M] += ok ? lsum : R(0);
-      if (ok) store_u(t, r);
+      tm_store_rec<M, R>(tm_u(s), r);
     }
+    tm_wait_st();
   };
 
   // ------------------------------------------ A2: weighted covariances --
   // Lane a of a frame's GS lanes forms x_a conj(x_{a+d}), d = 0..M/2, and
-  // accumulates them against weights [mh*MW, (mh+1)*MW).  Then reduces the
-  // products (and the NLL partials) to CTA totals in ex[], cluster totals in
-  // qraw[] (packed Hermitian, the layout ip_update_warp_reg reads) and res.
+  // accumulates them against weights [mh*MW, (mh+1)*MW) shuffled from the
+  // frame's owner lane.  Then reduces the products (and the NLL partials) to
+  // CTA totals in ex[], cluster totals in qraw[] (packed Hermitian, the
+  // layout the IP reads) and nll_tot.
   auto a2_pass = [&](bool want_q, const R (&nacc)[M + 1], double (&nll_tot)[M + 1]) {
-    const int a = lane % M, mh = (lane / M) % MS;
-    const int g = (warp * 32 + lane) / GS;
-    constexpr int NG = NTHR / GS;
+    constexpr int FPB = 32 / GS;  // frames per batch
+    const int a = lane % M, mh = (lane / M) % MS, g = lane / GS;
     R acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) acc[k] = R(0);
@@ -514,43 +630,47 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
 #pragma unroll
     for (int d = 0; d <= D; ++d) coff[d] = (a + d) % M;
     if (want_q) {
+#pragma unroll 1
+      for (int s = 0; s < SLOTS; ++s) {
+        R ro[M];  // this lane's own frame weights 1/sigma^2
+        tm_load_rec<M, R>(tm_u(s), ro);
 #pragma unroll 2
-      for (int t = g; t < Tl; t += NG) {
-        const C* xf = xg + size_t(t) * M;
-        C xr[D + 1];
+        for (int bb = 0; bb < 32 / FPB; ++bb) {
+          const int owner = bb * FPB + g;
+          const int t0 = frame_of(s, owner);
+          const bool ok = t0 < Tl;
+          const C* xf = xg + size_t(ok ? t0 : 0) * M;
+          C xr[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) xr[d] = xf[coff[d]];
-        R rr[MW];
-        {
-          const V* rv = Up + t;
+          for (int d = 0; d <= D; ++d) xr[d] = xf[coff[d]];
+          R P[NP];
+          P[0] = xr[0].x * xr[0].x + xr[0].y * xr[0].y;
 #pragma unroll
-          for (int q = 0; q < MW / VE; ++q) {
-            const V v = rv[(mh * MW / VE + q) * ps];
-            if constexpr (VE == 4) {
-              rr[q * 4] = v.x, rr[q * 4 + 1] = v.y, rr[q * 4 + 2] = v.z, rr[q * 4 + 3] = v.w;
+          for (int d = 1; d <= D; ++d) {
+            // x_a conj(x_c): Re = ar cr + ai ci, Im = ai cr - ar ci
+            P[2 * d - 1] = xr[0].x * xr[d].x + xr[0].y * xr[d].y;
+            P[2 * d] = xr[0].y * xr[d].x - xr[0].x * xr[d].y;
+          }
+#pragma unroll
+          for (int mm = 0; mm < MW; ++mm) {
+            R rm;
+            if constexpr (MS == 1) {
+              rm = __shfl_sync(0xffffffffu, ro[mm], owner);
             } else {
-              rr[q * 2] = v.x, rr[q * 2 + 1] = v.y;
+              const R r0 = __shfl_sync(0xffffffffu, ro[mm], owner);
+              const R r1 = __shfl_sync(0xffffffffu, ro[MW + mm], owner);
+              rm = mh == 0 ? r0 : r1;
             }
+            rm = ok ? rm : R(0);
+#pragma unroll
+            for (int jj = 0; jj < NP; ++jj) acc[jj * MW + mm] += P[jj] * rm;
           }
         }
-        R P[NP];
-        P[0] = xr[0].x * xr[0].x + xr[0].y * xr[0].y;
-#pragma unroll
-        for (int d = 1; d <= D; ++d) {
-          // x_a conj(x_c): Re = ar cr + ai ci, Im = ai cr - ar ci
-          P[2 * d - 1] = xr[0].x * xr[d].x + xr[0].y * xr[d].y;
-          P[2 * d] = xr[0].y * xr[d].x - xr[0].x * xr[d].y;
-        }
-#pragma unroll
-        for (int j = 0; j < NP; ++j)
-#pragma unroll
-          for (int mm = 0; mm < MW; ++mm) acc[j * MW + mm] += P[j] * rr[mm];
       }
     }
     FFCA_BTIC(5);
     // Lanes of equal role (lane mod GS) hold partials of the same products:
-    // reduce-scatter over the groups of the warp.
-    constexpr int GPW = 32 / GS;  // groups per warp (power of two)
+    // reduce-scatter over the frame groups of the warp.
     int base = 0;
     int cnt = KA;
 #pragma unroll
@@ -568,67 +688,68 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       if (up) base += h2;
       cnt = h2;
     }
-    (void)GPW;
     // NLL partials of A1 (thread-per-frame accumulators).
     R* rd = red;  // EM partial buffers are idle here
     warp_reduce_store<M + 1>(nacc, rd + warp * KRED, lane);
-    __syncthreads();  // every warp is done reading 1/sigma^2 from U
-    if (want_q) {
-      // gscr[warp][role][KA] (role = lane % GS)
-      R* dst = gscr + (warp * GS + (lane % GS)) * KA + base;
-      for (int i = 0; i < cnt; ++i) dst[i] = acc[i];
-    }
-    __syncthreads();
-    // CTA totals in the packed layout: ex[m*M*M + (a*M + c)] (a < c: Re at
-    // a*M+c, Im at c*M+a; diagonal at a*M+a), then the NLL terms.
-    constexpr int KQ = M * M * M;
-    if (want_q) {
-      for (int o = tid; o < GS * KA; o += NTHR) {
-        const int role = o / KA, k = o - role * KA;
-        const int ra = role % M, rmh = role / M;
-        const int j = k / MW, mm = k - j * MW;
-        const int m = rmh * MW + mm;
-        double s = 0.0;
-        {
-          double v[NW];
+    // Cross-warp tree through the scratch (fixed order): at step h, warps
+    // [h, 2h) publish, warps [0, h) add.  Warp 0 ends with the CTA totals.
+#pragma unroll 1
+    for (int h = HW; h >= 1; h >>= 1) {
+      if (want_q && warp >= h && warp < 2 * h && warp < NW) {
+        R* dst = gscr + ((warp - h) * 32 + lane) * CNT;
 #pragma unroll
-          for (int w = 0; w < NW; ++w) v[w] = double(gscr[(w * GS + role) * KA + k]);
-          // fixed-order pairwise tree
-#pragma unroll
-          for (int hh = 1; hh < NW; hh <<= 1)
-#pragma unroll
-            for (int w = 0; w + hh < NW; w += 2 * hh) v[w] += v[w + hh];
-          s = v[0];
-        }
-        int idx = -1;
-        double val = s;
-        if (j == 0) {
-          idx = ra * M + ra;
-        } else {
-          const int d = (j + 1) / 2;
-          const bool im = (j % 2) == 0;
-          const int c = (ra + d) % M;
-          if (d * 2 == M && ra >= M / 2) {
-            idx = -1;  // duplicate of (c, ra)
-          } else if (ra < c) {
-            idx = im ? c * M + ra : ra * M + c;
-          } else {
-            // x_ra conj(x_c) = conj(x_c conj(x_ra)), c < ra
-            idx = im ? ra * M + c : c * M + ra;
-            if (im) val = -val;
-          }
-        }
-        if (idx >= 0) ex[m * M * M + idx] = val;
+        for (int i = 0; i < CNT; ++i) dst[i] = acc[i];
       }
+      __syncthreads();
+      if (want_q && warp < h && warp + h < NW) {
+        const R* src = gscr + (warp * 32 + lane) * CNT;
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) acc[i] += src[i];
+      }
+      __syncthreads();
     }
-    if (warp == 0 && lane <= M) ex[KQ + lane] = double(tree_sum_any<NW>(rd, KRED, lane));
+    (void)PW;
+    // CTA totals (warp 0) in the packed layout: ex[m*M*M + (a*M + c)]
+    // (a < c: Re at a*M+c, Im at c*M+a; diagonal at a*M+a), then the NLL.
+    if (warp == 0) {
+      if (want_q) {
+        const int ra = lane % M, rmh = (lane / M) % MS;
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) {
+          const int k = base + i;
+          const int j = k / MW, mm = k - j * MW;
+          const int m = rmh * MW + mm;
+          int idx = -1;
+          double val = double(acc[i]);
+          if (j == 0) {
+            idx = ra * M + ra;
+          } else {
+            const int d = (j + 1) / 2;
+            const bool im = (j % 2) == 0;
+            const int c = (ra + d) % M;
+            if (d * 2 == M && ra >= M / 2) {
+              idx = -1;  // duplicate of (c, ra)
+            } else if (ra < c) {
+              idx = im ? c * M + ra : ra * M + c;
+            } else {
+              // x_ra conj(x_c) = conj(x_c conj(x_ra)), c < ra
+              idx = im ? ra * M + c : c * M + ra;
+              if (im) val = -val;
+            }
+          }
+          if (idx >= 0) ex[m * M * M + idx] = val;
+        }
+      }
+      if (lane <= M) ex[KQ + lane] = double(tree_sum_any<NW>(rd, KRED, lane));
+    }
     __syncthreads();
     // Cluster totals, rank order (every CTA the same bits).
     const int nq = want_q ? KQ : 0;
     if constexpr (CL) {
       namespace cg = cooperative_groups;
       cg::cluster_group cl = cg::this_cluster();
-      cl_sync();
+      cluster_arrive();
+      cluster_wait();
       for (int o = tid; o < nq + M + 1; o += NTHR) {
         const int oo = o < nq ? o : KQ + (o - nq);
         double s = 0.0;
@@ -636,7 +757,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
         if (o < nq) qraw[o] = s;
         else ex[KQ + M + 1 + (o - nq)] = s;  // cluster NLL totals after the CTA ones
       }
-      cluster_arrive();  // this CTA is done reading the others' ex[]
+      cluster_arrive_relaxed();  // done reading the others' ex[] (its wait comes later)
     } else {
       for (int o = tid; o < nq; o += NTHR) qraw[o] = ex[o];
       for (int o = tid; o <= M; o += NTHR) ex[KQ + M + 1 + o] = ex[KQ + o];
@@ -708,38 +829,56 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     __syncwarp();
   };
 
-  // IP sweep (warp 0): pending balance W column scales first.
+  // IP sweep, called by EVERY thread: Q^{-1} and (W^H)^{-1} in parallel
+  // (ip_fast.cuh), then the sequential column updates on warp 0; on a failed
+  // acceptance test warp 0 reruns the sweep the reference's way
+  // (ip_update_warp_reg: LU-equivalent solves, residual test, seeded
+  // restart) from the saved W.  Leaves log|det W|^2 of the result in
+  // sc->logdet0 / sc->ldok for the next trace entry.
   auto run_ip = [&](unsigned long long seed) {
-    for (int k = lane; k < M * M; k += 32) {
-      const double c = double(wsc[k / M]);
-      Wd[k].x *= c;
-      Wd[k].y *= c;
+    ip_fast_prep<M, R, B>(warp, lane, Wd, wsc, qraw, invT, ipf);
+    __syncthreads();
+    if (warp == 0) {
+      double ldn = 0.0;
+      const bool fast_ok = ip_fast_sweep<M, R>(lane, Wd, ipf, ldn);
+      if (fast_ok) {
+        if (lane == 0) {
+          sc->logdet0 = ldn;
+          sc->ldok = 1;
+        }
+      } else {
+        for (int k = lane; k < M * M; k += 32) Wd[k] = ipf->wsave[k];
+        __syncwarp();
+        int bad = -1;
+        const bool ok = ip_update_warp_reg<M, R>(Wd, qraw, invT, seed, bin_index, rng, ipscr, lane, bad);
+        if (lane == 0 && !ok) {
+          sc->status = kStatusIpSingular | (bad << 8);
+          sc->stop = 1;
+        }
+        __syncwarp();
+        double ld = 0.0;
+        const bool lok = warp_log_abs_det2<M, R>(Wd, ldscr, lane, ld);
+        if (lane == 0) {
+          sc->logdet0 = ld;
+          sc->ldok = lok ? 1 : 0;
+        }
+      }
+      __syncwarp();
+      for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
     }
-    __syncwarp();
-    int bad = -1;
-    const bool ok = ip_update_warp_reg<M, R>(Wd, qraw, invT, seed, bin_index, rng, ipscr, lane, bad);
-    if (lane == 0 && !ok) {
-      sc->status = kStatusIpSingular | (bad << 8);
-      sc->stop = 1;
-    }
-    __syncwarp();
-    for (int k = lane; k < M * M; k += 32) Wr[k] = mkc<R>(R(Wd[k].x), R(Wd[k].y));
   };
-  auto logdet_warp = [&](double& ld) -> bool { return warp_log_abs_det2<M, R>(Wd, ldscr, lane, ld); };
 
   // -------------------------------------------------------------- driver --
   R nacc[M + 1];
   double ntot[M + 1];
   // Initial decorrelated powers, variances, NLL of the init and the first Q.
   u_pass();
-  __syncthreads();
   a1_pass(false, nacc);
-  __syncthreads();
   a2_pass(p.iters > 0 && !silent, nacc, ntot);
   if (warp == 0) {
     if (record) {
       double ld = 0.0;
-      const bool ok = logdet_warp(ld);
+      const bool ok = warp_log_abs_det2<M, R>(Wd, ldscr, lane, ld);
       if (lane == 0) {
         if (!ok) {
           sc->status = kStatusSingularW;
@@ -756,31 +895,19 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
         for (int t = 0; t < p.iters; ++t) p.nll[size_t(t + 1) * p.nll_stride + p.prob_offset + b] = sc->nll0;
     }
     __syncwarp();
-    if (!sc->stop && p.iters > 0) run_ip(p.seed);
   }
+  __syncthreads();
+  if (!sc->stop && p.iters > 0) run_ip(p.seed);
   if constexpr (CL) cluster_wait();  // pairs the arrive of a2_pass
   __syncthreads();
   FFCA_BTIC(9);
   bool touched = false;
   if (!sc->stop) {
     for (int it = 0; it < p.iters; ++it) {
-      // log|det W|^2 of the IP output (warp 1, off the other warps' path).
-      if (record && warp == (NW > 1 ? 1 : 0)) {
-        double ld = 0.0;
-        const bool ok = logdet_warp(ld);
-        if (lane == 0) {
-          sc->ldok = ok ? 1 : 0;
-          sc->logdet0 = ld;
-        }
-        __syncwarp();
-      }
       FFCA_BTIC(7);
       u_pass();
-      __syncthreads();
       FFCA_BTIC(0);
-      // EM sweeps (fastfca.cpp:80-99).  Sweep 0 is peeled so the posterior
-      // registers are provably written before they are read (no live range
-      // across the other passes).
+      // EM sweeps (fastfca.cpp:80-99).  The last sweep also sums Phi (balance).
       auto em_step = [&](int n) {
         const bool phis = bal && n == N - 1;
         R* rd = red + (n & 1) * NW * KRED;
@@ -803,35 +930,32 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
         __syncwarp();
         FFCA_BTIC(2);
       };
-      em_step(0);
-      for (int n = 1; n < N; ++n) em_step(n);
+#pragma unroll 1
+      for (int n = 0; n < N; ++n) em_step(n);
       balance_all(bal);
       FFCA_BTIC(3);
       touched = true;
       const bool more = it + 1 < p.iters;
       a1_pass(true, nacc);
-      __syncthreads();
       FFCA_BTIC(4);
       a2_pass(more, nacc, ntot);
       FFCA_BTIC(6);
-      if (warp == 0) {
-        if (lane == 0 && record) {
-          if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
-            sc->status = kStatusSingularW;
-            sc->stop = 1;
-          }
-          const double v = nll_value(ntot, sc->logdet0 - sc->logs);
-          if (lead) p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] = v;
+      if (warp == 0 && lane == 0 && record) {
+        if (!sc->ldok) {  // log_abs_det2 throws on a singular W (sigmodel.cpp:124-125)
+          sc->status = kStatusSingularW;
+          sc->stop = 1;
         }
-        __syncwarp();
-        if (more && !sc->stop) {
-          run_ip(p.seed + (unsigned long long)(it + 1));
-        } else {
-          for (int k = lane; k < M * M; k += 32) {  // the last balance's W scales
-            const double c = double(wsc[k / M]);
-            Wd[k].x *= c;
-            Wd[k].y *= c;
-          }
+        const double v = nll_value(ntot, sc->logdet0 - sc->logs);
+        if (lead) p.nll[size_t(it + 1) * p.nll_stride + p.prob_offset + b] = v;
+      }
+      __syncthreads();
+      if (more && !sc->stop) {
+        run_ip(p.seed + (unsigned long long)(it + 1));
+      } else if (warp == 0) {
+        for (int k = lane; k < M * M; k += 32) {  // the last balance's W scales
+          const double c = double(wsc[k / M]);
+          Wd[k].x *= c;
+          Wd[k].y *= c;
         }
       }
       FFCA_BTIC(7);
@@ -858,7 +982,13 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     for (int k = 0; k < 10; ++k) p.timing[size_t(b) * 16 + k] = tacc[k];
 #endif
 #undef FFCA_BTIC
-  if constexpr (CL) cl_sync();  // no CTA exits while others may read its shared memory
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(sc->tmem));
+  if constexpr (CL) {  // no CTA exits while others may read its shared memory
+    cluster_arrive();
+    cluster_wait();
+  }
 }
 
 }  // namespace ffca

@@ -95,3 +95,21 @@ def test_big_matches_cluster_kernel(gpu, monkeypatch):
     r_old = fit(x, W, L, H, 6, "fp32")
     a, b = np.asarray(r_big.nll), np.asarray(r_old.nll)
     assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_big_ip_restart_matches_oracle(gpu, precision):
+    """A zero first column of W makes W^H Q_0 singular: the reference's first
+    solve fails, the column restarts from its seeded perturbation and the
+    retry succeeds (fastfca.cpp:51-70).  The fast IP detects the singular W
+    and reruns the sweep the reference's way; W, L, H must match the oracle."""
+    x, W, L, H = make_case(2, 3000, seed=21)
+    W = W.copy()
+    W[1, :, 0] = 0.0
+    r = fit(x, W, L, H, 3, precision, record_trace=False, seed=7)
+    Wo, Lo, Ho, _, _, _ = oracle.fit(x, W, L, H, 3, record_trace=False, seed=7)
+    tol = 1e-9 if precision == "fp64" else 2e-3
+    assert (r.bin_status == 0).all()
+    for f in range(2):
+        assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= tol, f
+        assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= tol, f
