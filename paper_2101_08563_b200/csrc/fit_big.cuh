@@ -469,6 +469,48 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   // U(j, t) = |w_j^H x_t|^2: M lanes per frame, lane j owns column j of W;
   // the frame's owner lane gathers its M values and stores them to TMEM.
   auto u_pass = [&]() {
+    if constexpr (sizeof(R) == 4) {
+      // fp32: one thread per frame (the owner loads its record, coalesced),
+      // W columns from broadcast shared loads, packed FFMA2:
+      // y_m = sum_c conj(W(c,m)) x_c = sum_c Re W(c,m) x_c + i sum_c Im W(c,m) (Im x_c, -Re x_c),
+      // U(m) written straight to the frame's TMEM column.
+#pragma unroll 1
+      for (int s = 0; s < SLOTS; ++s) {
+        const int t0 = frame_of(s, lane);
+        const int t = t0 < Tl ? t0 : 0;
+        float2 xc[M];
+        const float4* xv = reinterpret_cast<const float4*>(xg + size_t(t) * M);
+#pragma unroll
+        for (int q = 0; q < M / 2; ++q) {
+          const float4 v = __ldg(xv + q);
+          xc[2 * q] = f2(v.x, v.y);
+          xc[2 * q + 1] = f2(v.z, v.w);
+        }
+        const unsigned ta = tm_u(s);
+#pragma unroll 2
+        for (int m = 0; m < M; ++m) {
+          float wc[2 * M];  // column m of W: (re, im) pairs
+          const unsigned a = unsigned(__cvta_generic_to_shared(Wr + m * M));
+#pragma unroll
+          for (int q = 0; q < M / 2; ++q)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(wc[4 * q]), "=f"(wc[4 * q + 1]), "=f"(wc[4 * q + 2]), "=f"(wc[4 * q + 3])
+                         : "r"(a + 16 * q));
+          float2 y1 = f2(0.f, 0.f), y2 = f2(0.f, 0.f);
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            y1 = fma2s(xc[c], wc[2 * c], y1);
+            y2 = fma2s(xc[c], wc[2 * c + 1], y2);
+          }
+          const float yr = y1.x + y2.y, yi = y1.y - y2.x;
+          const float u = yr * yr + yi * yi;
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(ta + unsigned(m)),
+                       "r"(__float_as_uint(u))
+                       : "memory");
+        }
+      }
+      tm_wait_st();
+    } else {
     constexpr int FPB = 32 / M;  // frames per batch
     const int j = lane % M, g = lane / M;
     C wc[M];
@@ -527,6 +569,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       tm_store_rec<M, R>(tm_u(s), uo);
     }
     tm_wait_st();
+    }
   };
 
   // ---------------------------------------------------- EM sweep n --------
