@@ -1,20 +1,24 @@
 """FastFCA IP+EM fit throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1]
-                    [--impl ours|reference] [--no-cpu-baseline]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+                    [--impl ours|reference] [--no-cpu-baseline] [--scaling strong|weak]
 
 A step is one full fastfca_fit (all `iters` IP+EM iterations) over the
 workload's synthetic mixtures -- SURVEY §8(d): the work unit is one TF-bin EM
 update, throughput = B*F*T*iters / t.
 
-Workload: BASELINE.json configs[1] ("c1": M=2, N=2, F=513, T=1250, 100 EM
-iterations), one mixture per GPU.  Under torchrun (N > 1) the N mixtures'
-flattened (mixture, bin) problems are split into contiguous balanced ranges,
-one per rank (frequency sharding: no exchange during the fit), so per-GPU
-work is fixed as N grows (scaling "weak"); the per-bin NLL slots are
-all-gathered over NCCL after the timed region to assemble each mixture's
-trace in bin order.  Other configs (--config c0|c2|c3|c4) are parity cases;
-c4 (256 mixtures) shards its fixed batch over the ranks (scaling "strong").
+Workload: BASELINE.json configs[3] ("c3": M=8, N=12, F=2049, T=8000, 30 EM
+iterations, one mixture) -- the configuration the metric ("... 1/2/4/8 B200")
+is quoted on; it fits one GPU (x 1.05 GB + H 0.79 GB).  Under torchrun
+(N > 1) the ONE mixture's 2049 bins (for c4: the 256 x 513 flattened
+(mixture, bin) problems) are split into contiguous balanced ranges, one per
+rank -- the reference's parallel_for over bins (parallel.cpp:16-45) moved
+onto GPUs: no exchange during the fit, total work fixed as N grows (scaling
+"strong").  The per-bin NLL slots are all-gathered over NCCL after the timed
+region and each mixture's trace is summed in bin order, so the trace is
+bit-identical for any N.  --scaling weak gives every rank its own mixture
+instead.  Other configs (--config c0|c1|c2|c4) are parity cases / secondary
+lines.
 
 value : device-resident inputs (x, H, W, L already in HBM), one fit kernel per
         step timed with CUDA events on the launching stream, L2 flushed
@@ -47,21 +51,53 @@ UNIT = "TF-bin-updates/s"
 
 
 def peaks() -> dict:
+    """HBM peak: the driver-written MEASURED_PEAKS.json, else the profiling
+    recipe's fallback.  FP32 (CUDA-core FFMA) peak: the FFMA loop of
+    tools/fp32_peak.cu measured on this pool's B200s (profiles/r2_fp32_peak.json,
+    committed), else SURVEY 8(d)'s nominal 75 TFLOP/s."""
+    out = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)",
+           "fp32_tflops": 75.0, "fp32_source": "fallback (SURVEY 8(d) nominal)"}
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        out.update(hbm_gbs=d["hbm_gbs"], source="measured (MEASURED_PEAKS.json)")
+    q = ROOT / "profiles" / "r2_fp32_peak.json"
+    if q.exists():
+        out.update(fp32_tflops=json.loads(q.read_text())["ffma_tflops"],
+                   fp32_source="measured FFMA loop (tools/fp32_peak.cu, profiles/r2_fp32_peak.json)")
+    return out
+
+
+def alg_bytes(M: int, N: int) -> int:
+    """Algorithmic bytes per TF-bin-iteration: x read once
+    (complex64), v read and written once (fp32)."""
+    return 8 * M + 8 * N
+
+
+def alg_flops(M: int, N: int) -> int:
+    """Algorithmic flops per TF-bin-iteration: Q 2M^3+5M^2+3M,
+    U 8M^2+3M, sigma^2 2MN, EM 11MN, NLL 3M."""
+    return 2 * M ** 3 + 13 * M ** 2 + 9 * M + 13 * M * N
+
+
+def config_dict(cfg, batch: int, world: int, scaling: str) -> dict:
+    """The line's `config` -- identical for the GPU arm and the reference arm."""
+    return {"workload": cfg.name, "M": cfg.M, "N": cfg.N, "F": cfg.F, "T": cfg.T,
+            "iters": cfg.iters, "batch": batch, "flavor": "em", "record_trace": True,
+            "parallelism": f"freq-shard x{world} ({scaling})",
+            "l2": "flushed between steps (256 MiB write)"}
 
 
 from paper_2101_08563_b200.shard import bin_order_trace, gather_slots, shard  # noqa: E402
 
 
-def workload(cfg, world: int):
-    """The benchmarked batch: one mixture per rank for single-mixture configs."""
-    if cfg.batch == 1 and world > 1:
-        return dataclasses.replace(cfg, batch=world), "weak"
-    return cfg, ("weak" if cfg.batch == 1 else "strong")
+def workload(cfg, world: int, scaling: str = "strong"):
+    """The benchmarked batch.  strong (default): the config as BASELINE.json
+    states it, its (mixture, bin) problems split over the ranks.  weak: one
+    copy of the config's batch per rank."""
+    if scaling == "weak" and world > 1:
+        return dataclasses.replace(cfg, batch=cfg.batch * world), "weak"
+    return cfg, "strong"
 
 
 class ClockSampler:
@@ -123,9 +159,9 @@ def build_inputs(cfg, lo: int, hi: int):
     for b in range(lo // F, (hi - 1) // F + 1):
         f0 = max(lo - b * F, 0)
         f1 = min(hi - b * F, F)
-        x = synth.mixture(cfg, b)
+        x = synth.mixture(cfg, b, slice(f0, f1))
         W, L, H = synth.init_params(cfg, b)
-        xs.append(x[f0:f1]); Ws.append(W[f0:f1]); Ls.append(L[f0:f1]); Hs.append(H[f0:f1])
+        xs.append(x); Ws.append(W[f0:f1]); Ls.append(L[f0:f1]); Hs.append(H[f0:f1])
     return (np.concatenate(xs), np.concatenate(Ws), np.concatenate(Ls), np.concatenate(Hs))
 
 
@@ -137,17 +173,17 @@ def oracle_sample(cfg, args, budget_s: float = 10.0):
     import oracle  # test infrastructure: the CPU baseline leg only
     from paper_2101_08563_b200 import synth
     cores = oracle.default_workers()
-    xall = synth.mixture(cfg, 0)
-    W, L, H = synth.init_params(cfg, 0)
     if args.cpu_bins:
         S = min(cfg.F, args.cpu_bins)
     else:
         cal_it = min(cfg.iters, 3)
-        x1 = xall[:1].astype(np.complex128)
-        _, _, _, _, _, s1 = oracle.fit(x1, W[:1], L[:1], H[:1], cal_it, workers=1)
+        x1 = synth.mixture(cfg, 0, slice(0, 1)).astype(np.complex128)
+        W, L, H = synth.init_params(cfg, 0, nbins=1)
+        _, _, _, _, _, s1 = oracle.fit(x1, W, L, H, cal_it, workers=1)
         per_bin = max(s1, 1e-6) * cfg.iters / cal_it
         S = int(min(cfg.F, max(cores, budget_s * cores / per_bin)))
-    x = xall[:S].astype(np.complex128)
+    x = synth.mixture(cfg, 0, slice(0, S)).astype(np.complex128)
+    W, L, H = synth.init_params(cfg, 0, nbins=S)
     sample = (f"{cfg.name}: first {S} of {cfg.F} bins of mixture 0, T={cfg.T}, {cfg.iters} "
               f"iters, fastfca_fit only, fp64 oracle port of the reference (the reference "
               f"itself needs Eigen3, absent)")
@@ -182,16 +218,15 @@ def run_reference(cfg, args, rank: int, world: int) -> None:
             times.append(secs)
     tot = sum(times)
     v = S * cfg.T * cfg.iters * len(times) / tot
-    wl, scaling = workload(cfg, world)
+    wl, scaling = workload(cfg, world, args.scaling)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE.json config shapes)",
-        "config": {"workload": cfg.name, "M": cfg.M, "N": cfg.N, "F": cfg.F, "T": cfg.T,
-                   "iters": cfg.iters, "batch": wl.batch, "sample_bins": S},
+        "data": "synthetic (seeded, BASELINE.json config shapes; paper data unavailable)",
+        "config": config_dict(cfg, wl.batch, world, scaling),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "sample_bins": S},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -199,9 +234,11 @@ def run_reference(cfg, args, rank: int, world: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c1"))
+    ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c3"))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--no-separate", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -228,7 +265,7 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2101_08563_b200 import _lib
 
-    cfg, scaling = workload(cfg0, world)
+    cfg, scaling = workload(cfg0, world, args.scaling)
     P = cfg.batch * cfg.F
     lo, hi = shard(P, world, rank)
     Pl = hi - lo
@@ -347,7 +384,9 @@ def main() -> None:
     esz = 16 if fp64 else 8
     sep_bytes = Pl * T * (esz * M + (esz // 2) * N + esz * N * M)
     separate = {"ms": sep_s * 1e3, "bytes": int(sep_bytes), "GB_per_s": sep_bytes / sep_s / 1e9,
+                "frac_hbm": sep_bytes / sep_s / 1e9 / peaks()["hbm_gbs"],
                 "bytes_per_frame": "x read + H read + N images written"}
+    del img
 
     # e2e through the reference-facing C-ABI with pinned host buffers.
     e2e = None
@@ -377,18 +416,22 @@ def main() -> None:
             t = torch.tensor([et], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
-        h2d = xr.numel() * 16 + Hr.numel() * 8 + Wpin.numel() * 16 + Lpin.numel() * 8
-        d2h = Hr.numel() * 8 + Wpin.numel() * 16 + Lpin.numel() * 8 + nll_h.numel() * 8
+        # whole-job bytes per step (all ranks' shards)
+        h2d = P * (T * M * 16 + T * N * 8 + M * M * 16 + M * N * 8)
+        d2h = P * (T * N * 8 + M * M * 16 + M * N * 8) + world * (iters + 1) * 8
         e2e = {"value": P * T * iters * len(times) / et, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * et / len(times), "launches_per_step": ectx.launches(),
                "timing": "host clock around the synchronous C-ABI call, max over ranks"}
 
     if rank == 0:
         pk = peaks()
-        b_alg = 8 * M + 8 * N  # bytes per TF-bin-iteration
+        b_alg, f_alg = alg_bytes(M, N), alg_flops(M, N)
         kern_s = (tot_ms / 1e3) / args.steps
-        achieved = Pl * T * iters * b_alg / kern_s / 1e9  # per GPU (rank 0's shard)
+        units_launch = Pl * T * iters  # per GPU (rank 0's shard), one launch per step
+        achieved = units_launch * b_alg / kern_s / 1e9
+        fl_achieved = units_launch * f_alg / kern_s / 1e12
+        frac_hbm, frac_fp32 = achieved / pk["hbm_gbs"], fl_achieved / pk["fp32_tflops"]
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
@@ -405,18 +448,26 @@ def main() -> None:
             "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if not fp64 else "f64",
             "data": "synthetic (seeded, BASELINE.json config shapes; paper data unavailable)",
-            "config": {"workload": cfg0.name, "M": M, "N": N, "F": cfg.F, "T": T,
-                       "iters": iters, "batch": cfg.batch, "flavor": "em",
-                       "record_trace": True, "parallelism": f"freq-shard x{world}",
-                       "l2": "flushed between steps (256 MiB write)"},
+            "config": config_dict(cfg0, cfg.batch, world, scaling),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                         "unit": "GB/s", "frac": frac_hbm, "traffic": traffic,
                          "peak_source": pk["source"],
                          "algorithmic_bytes_per_unit": b_alg,
+                         "units_per_launch": units_launch,
+                         "kernel": "the one fit kernel launched per step (big_fit_kernel for c3, "
+                                   "fit_kernel otherwise) = 100 % of the timed region",
+                         "fp32": {"bound": "fp32 CUDA cores", "achieved": fl_achieved,
+                                  "peak": pk["fp32_tflops"], "unit": "TFLOP/s", "frac": frac_fp32,
+                                  "algorithmic_flops_per_unit": f_alg,
+                                  "peak_source": pk["fp32_source"]},
+                         "min_bound": {"bound": "fp32" if frac_fp32 > frac_hbm else "hbm",
+                                       "frac": max(frac_fp32, frac_hbm),
+                                       "note": "fraction of min(HBM peak / B_alg, FP32 peak / F_alg)"
+                                               " units/s -- the binding roofline of this config"},
                          "note": "algorithmic bytes (8M+8N per TF-bin-iteration, SURVEY 8(d)) x"
-                                 " units per launch / kernel time; x and H stay in shared memory"
-                                 " for the whole fit, so DRAM traffic (traffic) is far below the"
-                                 " algorithmic bytes"},
+                                 " units per launch / kernel time; per-frame state stays on chip"
+                                 " (shared / tensor memory) for the whole fit, so DRAM traffic"
+                                 " (traffic) differs from the algorithmic bytes"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -365,6 +365,8 @@ int fit_host_chunked(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, 
     fp.F = d->mixture_bins > 0 ? d->mixture_bins : d->bins;
     fp.seed_bin0 = d->first_bin + lo;  // restart seed index (first_bin + p) % F
     fp.prob_offset = lo;
+    fp.work_total = P;  // streaming scratch: one allocation, disjoint rows per chunk
+    fp.work_first = lo;
     fp.x = xs + xo;
     fp.H = hs + ho;
     fp.W = reinterpret_cast<double2*>(dW) + size_t(lo) * M * M;

@@ -100,9 +100,16 @@ int launch_fit_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st) {
   if constexpr (!EXACT) {
     fp.resident = 0;
     fp.tloc = fp.T;
-    fp.work = ctx->get(kU, size_t(fp.nprob) * 2 * M * fp.T * sizeof(R), &err);
-    if (!fp.work)
+    // One scratch region for every problem of the CALL, this launch's rows
+    // at work_first: the chunks of the pipelined host fit run concurrently on
+    // their own streams and must neither share rows nor regrow (free) the
+    // buffer under each other.
+    const size_t per = size_t(2) * M * fp.T * sizeof(R);
+    const size_t nall = size_t(fp.work_total > 0 ? fp.work_total : fp.nprob);
+    char* base = static_cast<char*>(ctx->get(kU, nall * per, &err));
+    if (!base)
       return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: scratch alloc: ") + cudaGetErrorString(err));
+    fp.work = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
     return launch_fit_cfg<M, NT, EXACT, R, false, false, BLK>(ctx, fp, st, 1, dev_max);
   } else {
     (void)err;

@@ -50,40 +50,73 @@ def crandn(rng: np.random.Generator, shape) -> np.ndarray:
     return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2.0)
 
 
+def _mixture_chunk(cfg: Config, rng: np.random.Generator, nb: int) -> np.ndarray:
+    """nb bins of x, complex64 [nb, M, T], drawn from rng."""
+    M, N, T = cfg.M, cfg.N, cfg.T
+    if cfg.kind == "jd":
+        A = crandn(rng, (nb, M, M))
+        d = np.exp(rng.standard_normal((nb, N, M)))
+        v = np.exp(cfg.sigma_v * rng.standard_normal((nb, N, T)))
+        z = crandn(rng, (nb, N, M, T))
+        # s_n = sqrt(v_n) * A diag(sqrt(d_n)) z_n
+        y = z * np.sqrt(d)[..., None] * np.sqrt(v)[:, :, None, :]
+        s = np.einsum("fab,fnbt->fat", A, y)
+        s += np.sqrt(1e-3) * crandn(rng, (nb, M, T))
+    else:
+        B = crandn(rng, (nb, N, M, M))
+        R = B @ np.conj(np.swapaxes(B, -1, -2)) + 1e-2 * np.eye(M)
+        C = np.linalg.cholesky(R)
+        act = rng.random((nb, N, (T + 49) // 50)) < 0.5
+        a = np.repeat(act, 50, axis=-1)[..., :T]
+        v = rng.gamma(0.5, 1.0, (nb, N, T)) * a
+        z = crandn(rng, (nb, N, M, T))
+        s = np.einsum("fnab,fnbt->fat", C, z * np.sqrt(v)[:, :, None, :])
+    return s.astype(np.complex64)
+
+
+# Configs above this many source-image samples (c3: 1.6e9) draw every chunk of
+# bins from its own child stream, so chunks generate in parallel threads and a
+# frequency shard generates only its own bins.
+PARALLEL_STREAMS_ABOVE = 1 << 29
+
+
 def mixture(cfg: Config, b: int = 0, bins: slice | None = None) -> np.ndarray:
-    """x for mixture b: complex64 [F, M, T] (natural layout; the device SoA)."""
+    """x for mixture b: complex64 [F, M, T] (natural layout; the device SoA).
+    `bins` (a contiguous slice) restricts the result to those bins."""
     M, N, F, T = cfg.M, cfg.N, cfg.F, cfg.T
-    rng = np.random.Generator(np.random.PCG64([cfg.seed, 1, b]))
-    x = np.empty((F, M, T), np.complex64)
     chunk = max(1, (1 << 22) // (N * M * T))
-    for f0 in range(0, F, chunk):
-        f1 = min(F, f0 + chunk)
-        nb = f1 - f0
-        if cfg.kind == "jd":
-            A = crandn(rng, (nb, M, M))
-            d = np.exp(rng.standard_normal((nb, N, M)))
-            v = np.exp(cfg.sigma_v * rng.standard_normal((nb, N, T)))
-            z = crandn(rng, (nb, N, M, T))
-            # s_n = sqrt(v_n) * A diag(sqrt(d_n)) z_n
-            y = z * np.sqrt(d)[..., None] * np.sqrt(v)[:, :, None, :]
-            s = np.einsum("fab,fnbt->fat", A, y)
-            s += np.sqrt(1e-3) * crandn(rng, (nb, M, T))
-        else:
-            B = crandn(rng, (nb, N, M, M))
-            R = B @ np.conj(np.swapaxes(B, -1, -2)) + 1e-2 * np.eye(M)
-            C = np.linalg.cholesky(R)
-            act = rng.random((nb, N, (T + 49) // 50)) < 0.5
-            a = np.repeat(act, 50, axis=-1)[..., :T]
-            v = rng.gamma(0.5, 1.0, (nb, N, T)) * a
-            z = crandn(rng, (nb, N, M, T))
-            s = np.einsum("fnab,fnbt->fat", C, z * np.sqrt(v)[:, :, None, :])
-        x[f0:f1] = s.astype(np.complex64)
-    return x if bins is None else x[bins]
+    lo, hi, step = (0, F, 1) if bins is None else bins.indices(F)
+    assert step == 1
+    if F * N * M * T <= PARALLEL_STREAMS_ABOVE:
+        rng = np.random.Generator(np.random.PCG64([cfg.seed, 1, b]))
+        x = np.empty((F, M, T), np.complex64)
+        for f0 in range(0, F, chunk):
+            f1 = min(F, f0 + chunk)
+            x[f0:f1] = _mixture_chunk(cfg, rng, f1 - f0)
+        return x if bins is None else x[bins]
+    import concurrent.futures as cf
+    import os
+    x = np.empty((max(hi - lo, 0), M, T), np.complex64)
+
+    def work(k: int) -> None:
+        f0, f1 = k * chunk, min(F, (k + 1) * chunk)
+        part = _mixture_chunk(cfg, np.random.Generator(np.random.PCG64([cfg.seed, 1, b, k])),
+                              f1 - f0)
+        a, e = max(f0, lo), min(f1, hi)
+        x[a - lo:e - lo] = part[a - f0:e - f0]
+
+    ks = range(lo // chunk, (max(hi, lo + 1) - 1) // chunk + 1) if hi > lo else range(0)
+    with cf.ThreadPoolExecutor(min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(work, ks))
+    return x
 
 
-def init_params(cfg: Config, b: int = 0):
-    """(W, L, H) natural layout: W [F,M,M] complex128, L [F,M,N], H [F,N,T]."""
+def init_params(cfg: Config, b: int = 0, nbins: int | None = None):
+    """(W, L, H) natural layout: W [F,M,M] complex128, L [F,M,N], H [F,N,T].
+    nbins: only the first nbins bins (the same values: H is drawn bin by bin
+    from one stream)."""
     M, N, F, T = cfg.M, cfg.N, cfg.F, cfg.T
+    F = F if nbins is None else min(F, nbins)
     rng = np.random.Generator(np.random.PCG64([cfg.seed, 2, b]))
     W = np.broadcast_to(np.eye(M, dtype=np.complex128), (F, M, M)).copy()
     L = np.ones((F, M, N))

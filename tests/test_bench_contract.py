@@ -34,3 +34,27 @@ def test_reference_arm_prints_contract_line(built):
 
 def test_reference_arm_other_ranks_exit_quietly(built):
     assert _run({"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_default_workload_is_c3_and_arms_share_config():
+    """The headline config is BASELINE configs[3]; both arms print the same
+    `config` dict (the driver compares them), strong scaling shards ONE
+    mixture's bins."""
+    import argparse
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_2101_08563_b200 import synth
+    src = (ROOT / "bench.py").read_text()
+    assert 'os.environ.get("FFCA_BENCH_CONFIG", "c3")' in src
+    c3 = synth.CONFIGS["c3"]
+    for world in (1, 2, 8):
+        wl, scaling = bench.workload(c3, world)
+        assert scaling == "strong" and wl.batch == 1  # one mixture, bins split over ranks
+        a = bench.config_dict(c3, wl.batch, world, scaling)
+        assert a["workload"] == "c3" and (a["M"], a["N"], a["F"], a["T"], a["iters"]) == (8, 12, 2049, 8000, 30)
+    wl, scaling = bench.workload(c3, 4, "weak")
+    assert scaling == "weak" and wl.batch == 4
+    assert bench.alg_bytes(8, 12) == 160 and bench.alg_flops(8, 12) == 3176
+    assert src.count("config_dict(") >= 3  # defined once, used by both arms

@@ -229,11 +229,33 @@ def test_pipelined_host_fit_matches_single_launch(gpu, precision, monkeypatch):
 
 
 # A bin beyond a 16-CTA cluster's shared memory streams its records from
-# global memory (the !RES variant); config 3's M, N with T = 20000 frames.
+# global memory (the !RES variant).  M = 8 with N = 10 sources (N = 12 belongs
+# to the large-bin kernel, tests/test_gpu_big.py) and T = 24000 frames.
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_streaming_bin_matches_oracle(gpu, precision):
-    x, W, L, H = make_case(8, 12, 1, 20000, seed=23)
+    x, W, L, H = make_case(8, 10, 1, 24000, seed=23)
     r = gpu_fit(x, W, L, H, 2, precision)
     Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, 2)
     rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
     assert rel.max() <= NLL_TOL[precision], rel.max()
+
+
+# Streaming bins through the pipelined host fit (FFCA_FIT_CHUNKS = 3 chunks
+# on 3 streams): the chunks' kernels run concurrently, so each must work in
+# its own rows of the one U/Phi scratch allocation.  Uneven chunks (7 bins).
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_streaming_bins_chunked_match_oracle(gpu, precision, monkeypatch):
+    x, W, L, H = make_case(8, 10, 7, 24000, seed=29)
+    monkeypatch.setenv("FFCA_FIT_CHUNKS", "3")
+    r = gpu_fit(x, W, L, H, 2, precision)
+    monkeypatch.delenv("FFCA_FIT_CHUNKS")
+    r1 = gpu_fit(x[:1], W[:1], L[:1], H[:1], 2, precision)
+    Wo, Lo, Ho, nll_o, slots_o, _ = oracle.fit(x, W, L, H, 2)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL[precision], rel.max()
+    tol = 1e-9 if precision == "fp64" else 2e-3
+    for f in range(7):
+        e = np.linalg.norm(np.asarray(r.params.act[f]) - Ho[f]) / np.linalg.norm(Ho[f])
+        assert e <= tol, (f, e)
+    # a chunked bin equals the same bin fitted alone, bit for bit
+    assert np.array_equal(np.asarray(r.params.act[0]), np.asarray(r1.params.act[0]))
