@@ -1,5 +1,8 @@
 // fastfca.hpp -- the FastFCA fit / separate entry points, B200 backend
-// (drop-in for reference proj/include/fastfca/fastfca.hpp:16-66).
+// (drop-in for reference proj/include/fastfca/fastfca.hpp:16-66 and :76-81;
+// not provided: fastfca_mwf :60-61, ajd_cost :68-71, reconstruct_scms :83-84
+// -- explicit filter matrices and diagnostics outside the fit/separate path,
+// SURVEY section 8 out of scope).
 //
 // Same names, argument order, defaults and error behaviour as the reference:
 // std::invalid_argument on shape mismatch, NumericalError on a singular IP
@@ -37,6 +40,28 @@ struct GpuOptions {
   Precision precision = Precision::fp32;
 };
 
+// The per-step functions (fastfca.hpp:28-53), each a single-bin fp64 launch
+// of libffca.so (csrc/steps.cu); the fit kernels fuse the same steps.
+// weighted_cov: Q_m = symmetrize((1/J) sum_j Xhat_j / sigma2_mj) at frequency
+// i (fastfca.cpp:22-34; sigma2_row is 1 x blocks).
+CMat weighted_cov(const SampleCovSet& covs, int i, const RMat& sigma2_row);
+// One IP sweep over the columns of W at frequency i (fastfca.cpp:36-72):
+// seeded single restart of a singular column, then NumericalError.
+void ip_update_w(const SampleCovSet& covs, int i, CMat& w, const RMat& loading, const RMat& act,
+                 std::uint64_t restart_seed = 0);
+// G_n = (L_{:,n} H_{n,:}) / floor_positive(L H) (fastfca.cpp:74-78).
+RMat source_gain(const RMat& loading, const RMat& act, int n);
+// IS-NMF updates of (L, H) against the decorrelated powers U: per source with
+// the running factors (EM, fastfca.cpp:80-99) or whole-matrix multiplicative
+// steps, L first (MM, fastfca.cpp:101-117).
+void em_update_lh(const RMat& u, RMat& loading, RMat& act, bool update_loading = true,
+                  double eps = 0.0);
+void mm_update_lh(const RMat& u, RMat& loading, RMat& act, bool update_loading = true,
+                  double eps = 0.0);
+
+// The reference signatures run the fp32 data path (GpuOptions{}); pass
+// GpuOptions{.precision = Precision::fp64} for the reference's arithmetic
+// (IP residual test at 1e-8 instead of 64 FLT_EPSILON).
 FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init, LhFlavor flavor,
                              int iters, const FitOptions& fit = {},
                              const FastFcaOptions& opts = {});

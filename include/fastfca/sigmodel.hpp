@@ -56,7 +56,15 @@ struct FastFcaParams {  // sigmodel.hpp:72-78
   std::vector<CMat> decorr;
   std::vector<RMat> loading;
   std::vector<RMat> act;
+  // Shape / finiteness / positivity / non-singular-W check with the
+  // reference's std::invalid_argument and NumericalError (sigmodel.cpp:74-91);
+  // the determinant test runs on the GPU (log_abs_det2).
+  void validate() const;
 };
+
+// ln|det W|^2 (sigmodel.cpp:118-129) on the GPU; NumericalError when W is
+// numerically singular.
+double log_abs_det2(const CMat& w);
 
 // Negative log-likelihood (sigmodel.cpp:155-162, 215-222) evaluated on the GPU
 // in fp64 (check-mode kernels); per-bin values are summed in bin order.

@@ -232,6 +232,43 @@ int ffca_istft_device(ffca_ctx* ctx, int channels, int frames, int frame_len, in
                       int padding, long long out_len, int precision, const void* spec_dev,
                       void* samples_dev, void* stream);
 
+/* ---- the reference's public per-step functions, one bin per call ----
+ * (fastfca.hpp:30-53; its unit tests call them directly,
+ * test_fastfca.cpp:82-228).  fp64 throughout, a few small launches each: the
+ * fit kernels fuse these steps, these entry points expose them one by one.
+ * x: the bin's snapshots [blocks][dim] complex (is_block_covs == 0) or its
+ * block covariances [blocks][dim*dim] col-major (is_block_covs != 0). */
+
+/* weighted_cov (fastfca.cpp:22-34): q [dim*dim] complex col-major =
+ * symmetrize((1/blocks) sum_j X_j / sigma2_row[j]). */
+int ffca_weighted_cov(ffca_ctx* ctx, int dim, int blocks, int is_block_covs, const double* x,
+                      const double* sigma2_row, double* q);
+
+/* ip_update_w (fastfca.cpp:36-72): one IP sweep over the columns of w
+ * (in/out, dim*dim complex col-major) with sigma^2 = loading*act +
+ * var_eps(power); restart draws follow mix_seed(restart_seed, bin_index).
+ * FFCA_NUMERICAL with the reference's message when a column stays singular
+ * after its restart (w is then left unchanged). */
+int ffca_ip_update_w(ffca_ctx* ctx, int dim, int sources, int blocks, int is_block_covs,
+                     const double* x, double power, double* w, const double* loading,
+                     const double* act, uint64_t restart_seed, int bin_index);
+
+/* log_abs_det2 (sigmodel.cpp:118-129): *out = ln|det w|^2; FFCA_NUMERICAL
+ * ("singular decorrelation matrix") when a pivot is zero or non-finite. */
+int ffca_log_abs_det2(ffca_ctx* ctx, int dim, const double* w, double* out);
+
+/* source_gain (fastfca.cpp:74-78): gain [dim x frames] col-major =
+ * L(:,n) H(n,:) / floor_positive(L H). */
+int ffca_source_gain(ffca_ctx* ctx, int dim, int sources, int frames, const double* loading,
+                     const double* act, int n, double* gain);
+
+/* em_update_lh / mm_update_lh (fastfca.cpp:80-117): u [dim x frames]
+ * col-major decorrelated powers; loading, act in/out. */
+int ffca_em_update_lh(ffca_ctx* ctx, int dim, int sources, int frames, const double* u,
+                      double* loading, double* act, int update_loading, double eps);
+int ffca_mm_update_lh(ffca_ctx* ctx, int dim, int sources, int frames, const double* u,
+                      double* loading, double* act, int update_loading, double eps);
+
 /* Number of kernels the last call on this context launched (bench evidence). */
 int ffca_last_launch_count(const ffca_ctx* ctx);
 

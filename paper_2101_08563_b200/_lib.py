@@ -30,6 +30,8 @@ EXPORTS = (
     "ffca_stft_frame_count", "ffca_stft", "ffca_istft", "ffca_stft_device", "ffca_istft_device",
     "ffca_block_covs", "ffca_fit_covs", "ffca_ica_fit_covs", "ffca_nll_bins_covs",
     "ffca_decorrelated_powers_covs", "ffca_block_covs_device", "ffca_fit_covs_device",
+    "ffca_weighted_cov", "ffca_ip_update_w", "ffca_source_gain", "ffca_em_update_lh",
+    "ffca_mm_update_lh", "ffca_log_abs_det2",
 )
 STFT_CENTERED, STFT_FULL_FRAMES = 0, 1
 
@@ -110,6 +112,12 @@ def lib() -> C.CDLL:
                                            P, P, P, P, P, P]
         L.ffca_power_scale_device.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]
         L.ffca_last_launch_count.argtypes = [P]
+        L.ffca_weighted_cov.argtypes = [P, i, i, i, P, P, P]
+        L.ffca_ip_update_w.argtypes = [P, i, i, i, i, P, C.c_double, P, P, P, C.c_uint64, i]
+        L.ffca_source_gain.argtypes = [P, i, i, i, P, P, i, P]
+        L.ffca_em_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
+        L.ffca_mm_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
+        L.ffca_log_abs_det2.argtypes = [P, i, P, P]
         L.ffca_debug_set_timing.argtypes = [P, P]
         _ = dp
         _lib = L

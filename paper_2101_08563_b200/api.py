@@ -363,6 +363,97 @@ def decorrelated_powers(covs: SampleCovSet, w: np.ndarray, *, floor_rel: float |
     return np.ascontiguousarray(np.swapaxes(out, -1, -2))
 
 
+# ----------------------------------------------------- per-step functions --
+# fastfca.hpp:28-53: each a single-bin fp64 launch (csrc/steps.cu).  Arrays are
+# the natural layouts (x [dim, frames], w [dim, dim], loading [dim, sources],
+# act [sources, frames], u [dim, frames]); results are new arrays.
+def _bin_stats(covs: SampleCovSet, i: int):
+    if not 0 <= i < covs.bins:
+        raise InvalidArgument("bin out of range")
+    if covs.has_snapshots():
+        return np.ascontiguousarray(covs.snapshots[i].T, np.complex128), 0
+    return np.ascontiguousarray(np.swapaxes(covs.mats[i], -1, -2), np.complex128), 1
+
+
+def _colmajor(a, dtype=np.float64) -> np.ndarray:
+    return np.array(np.asarray(a).T, dtype=dtype, order="C", copy=True)
+
+
+def weighted_cov(covs: SampleCovSet, i: int, sigma2_row, *, device: int | None = None) -> np.ndarray:
+    """Q = symmetrize((1/J) sum_j X_j / sigma2_row[j]) (fastfca.cpp:22-34)."""
+    x, blk = _bin_stats(covs, i)
+    sig = np.ascontiguousarray(np.asarray(sigma2_row, np.float64).ravel())
+    if sig.size != covs.blocks:
+        raise InvalidArgument("weighted_cov: variance row length mismatch")
+    M = covs.dim
+    q = np.empty((M, M), np.complex128)
+    _lib.check(_lib.lib().ffca_weighted_cov(_lib.context(device).handle, M, covs.blocks, blk,
+                                            _lib.ptr(x), _lib.ptr(sig), _lib.ptr(q)))
+    return np.ascontiguousarray(q.T)
+
+
+def ip_update_w(covs: SampleCovSet, i: int, w, loading, act, restart_seed: int = 0, *,
+                device: int | None = None) -> np.ndarray:
+    """One IP sweep over the columns of w at bin i (fastfca.cpp:36-72); returns the new w."""
+    x, blk = _bin_stats(covs, i)
+    M = covs.dim
+    loading, act = np.asarray(loading), np.asarray(act)
+    if np.shape(w) != (M, M) or loading.shape[0] != M or act.shape != (loading.shape[1], covs.blocks):
+        raise InvalidArgument("ip_update_w: shape mismatch")
+    W, L, H = _colmajor(w, np.complex128), _colmajor(loading), _colmajor(act)
+    _lib.check(_lib.lib().ffca_ip_update_w(_lib.context(device).handle, M, loading.shape[1],
+                                           covs.blocks, blk, _lib.ptr(x), float(covs.power(i)),
+                                           _lib.ptr(W), _lib.ptr(L), _lib.ptr(H),
+                                           int(restart_seed), int(i)))
+    return np.ascontiguousarray(W.T)
+
+
+def source_gain(loading, act, n: int, *, device: int | None = None) -> np.ndarray:
+    """G_n = L_n H_n / floor_positive(L H) (fastfca.cpp:74-78), [dim, frames]."""
+    loading, act = np.asarray(loading), np.asarray(act)
+    if act.shape[0] != loading.shape[1]:
+        raise InvalidArgument("source_gain: shape mismatch")
+    M, N, T = loading.shape[0], loading.shape[1], act.shape[1]
+    g = np.empty((T, M))
+    L, H = _colmajor(loading), _colmajor(act)
+    _lib.check(_lib.lib().ffca_source_gain(_lib.context(device).handle, M, N, T, _lib.ptr(L),
+                                           _lib.ptr(H), int(n), _lib.ptr(g)))
+    return np.ascontiguousarray(g.T)
+
+
+def _lh_update(fn, u, loading, act, update_loading, eps, device):
+    u, loading, act = np.asarray(u), np.asarray(loading), np.asarray(act)
+    M, T = u.shape
+    N = loading.shape[1]
+    if loading.shape[0] != M or act.shape != (N, T):
+        raise InvalidArgument("lh update: shape mismatch")
+    U, L, H = _colmajor(u), _colmajor(loading), _colmajor(act)
+    _lib.check(fn(_lib.context(device).handle, M, N, T, _lib.ptr(U), _lib.ptr(L), _lib.ptr(H),
+                  1 if update_loading else 0, float(eps)))
+    return np.ascontiguousarray(L.T), np.ascontiguousarray(H.T)
+
+
+def em_update_lh(u, loading, act, update_loading: bool = True, eps: float = 0.0, *,
+                 device: int | None = None):
+    """em_update_lh (fastfca.cpp:80-99); returns the new (loading, act)."""
+    return _lh_update(_lib.lib().ffca_em_update_lh, u, loading, act, update_loading, eps, device)
+
+
+def mm_update_lh(u, loading, act, update_loading: bool = True, eps: float = 0.0, *,
+                 device: int | None = None):
+    """mm_update_lh (fastfca.cpp:101-117); returns the new (loading, act)."""
+    return _lh_update(_lib.lib().ffca_mm_update_lh, u, loading, act, update_loading, eps, device)
+
+
+def log_abs_det2(w, *, device: int | None = None) -> float:
+    """ln|det w|^2 (sigmodel.cpp:118-129); NumericalError when singular."""
+    W = _colmajor(w, np.complex128)
+    out = np.zeros(1)
+    _lib.check(_lib.lib().ffca_log_abs_det2(_lib.context(device).handle, W.shape[0], _lib.ptr(W),
+                                            _lib.ptr(out)))
+    return float(out[0])
+
+
 # ------------------------------------------------------------------- stft --
 def sqrt_hann_window(frame_len: int) -> np.ndarray:
     """stft.cpp:33-39 (a constant table)."""

@@ -526,4 +526,107 @@ std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFca
   return images;
 }
 
+// ------------------------------------------------------- per-step functions --
+// fastfca.hpp:28-53 -- host work is validation and container <-> flat buffer
+// copies; the arithmetic is csrc/steps.cu (single-bin fp64 launches).
+
+namespace {
+
+// The bin's statistics as the flat buffer the step ABI takes: snapshots
+// [blocks][dim] or block covariances [blocks][dim*dim].
+std::vector<double> bin_stats(const SampleCovSet& covs, int i, const char* what) {
+  if (i < 0 || i >= covs.bins) throw std::invalid_argument(std::string(what) + ": bin out of range");
+  check_covs(covs, what);
+  const int M = covs.dim, J = covs.blocks;
+  std::vector<double> x;
+  if (covs.has_snapshots()) {
+    x.resize(size_t(J) * M * 2);
+    std::memcpy(x.data(), covs.snapshots[i].data(), sizeof(double) * x.size());
+  } else {
+    x.resize(size_t(J) * M * M * 2);
+    for (int j = 0; j < J; ++j)
+      std::memcpy(x.data() + size_t(j) * M * M * 2, covs.mats[i][j].data(), sizeof(double) * M * M * 2);
+  }
+  return x;
+}
+
+}  // namespace
+
+CMat weighted_cov(const SampleCovSet& covs, int i, const RMat& sigma2_row) {
+  const std::vector<double> x = bin_stats(covs, i, "weighted_cov");
+  if (sigma2_row.size() != covs.blocks)
+    throw std::invalid_argument("weighted_cov: variance row length mismatch");
+  CMat q(covs.dim, covs.dim);
+  raise(ffca_weighted_cov(context(0), covs.dim, covs.blocks, covs.has_snapshots() ? 0 : 1, x.data(),
+                          sigma2_row.data(), reinterpret_cast<double*>(q.data())));
+  return q;
+}
+
+void ip_update_w(const SampleCovSet& covs, int i, CMat& w, const RMat& loading, const RMat& act,
+                 std::uint64_t restart_seed) {
+  const std::vector<double> x = bin_stats(covs, i, "ip_update_w");
+  const int M = covs.dim;
+  if (w.rows() != M || w.cols() != M || loading.rows() != M || act.rows() != loading.cols() ||
+      act.cols() != covs.blocks)
+    throw std::invalid_argument("ip_update_w: shape mismatch");
+  raise(ffca_ip_update_w(context(0), M, int(loading.cols()), covs.blocks,
+                         covs.has_snapshots() ? 0 : 1, x.data(), covs.power(i),
+                         reinterpret_cast<double*>(w.data()), loading.data(), act.data(),
+                         restart_seed, i));
+}
+
+RMat source_gain(const RMat& loading, const RMat& act, int n) {
+  if (act.rows() != loading.cols()) throw std::invalid_argument("source_gain: shape mismatch");
+  RMat g(loading.rows(), act.cols());
+  raise(ffca_source_gain(context(0), int(loading.rows()), int(loading.cols()), int(act.cols()),
+                         loading.data(), act.data(), n, g.data()));
+  return g;
+}
+
+namespace {
+void check_lh(const RMat& u, const RMat& loading, const RMat& act, const char* what) {
+  if (loading.rows() != u.rows() || act.rows() != loading.cols() || act.cols() != u.cols())
+    throw std::invalid_argument(std::string(what) + ": shape mismatch");
+}
+}  // namespace
+
+void em_update_lh(const RMat& u, RMat& loading, RMat& act, bool update_loading, double eps) {
+  check_lh(u, loading, act, "em_update_lh");
+  raise(ffca_em_update_lh(context(0), int(u.rows()), int(loading.cols()), int(u.cols()), u.data(),
+                          loading.data(), act.data(), update_loading ? 1 : 0, eps));
+}
+
+void mm_update_lh(const RMat& u, RMat& loading, RMat& act, bool update_loading, double eps) {
+  check_lh(u, loading, act, "mm_update_lh");
+  raise(ffca_mm_update_lh(context(0), int(u.rows()), int(loading.cols()), int(u.cols()), u.data(),
+                          loading.data(), act.data(), update_loading ? 1 : 0, eps));
+}
+
+double log_abs_det2(const CMat& w) {
+  if (w.rows() != w.cols() || w.rows() < 1) throw std::invalid_argument("log_abs_det2: not square");
+  double out = 0.0;
+  raise(ffca_log_abs_det2(context(0), int(w.rows()), reinterpret_cast<const double*>(w.data()), &out));
+  return out;
+}
+
+void FastFcaParams::validate() const {  // sigmodel.cpp:74-91
+  if (int(decorr.size()) != bins || int(loading.size()) != bins || int(act.size()) != bins)
+    throw std::invalid_argument("FastFcaParams: bin count mismatch");
+  for (int i = 0; i < bins; ++i) {
+    if (decorr[i].rows() != dim || decorr[i].cols() != dim)
+      throw std::invalid_argument("FastFcaParams: decorrelation shape");
+    for (long k = 0; k < decorr[i].size(); ++k)
+      if (!std::isfinite(decorr[i].data()[k].real()) || !std::isfinite(decorr[i].data()[k].imag()))
+        throw std::invalid_argument("FastFcaParams: non-finite decorrelation");
+    log_abs_det2(decorr[i]);  // throws NumericalError when singular
+    if (loading[i].rows() != dim || loading[i].cols() != sources || act[i].rows() != sources ||
+        act[i].cols() != frames)
+      throw std::invalid_argument("FastFcaParams: loading/act shape");
+    bool pos = true;
+    for (long k = 0; k < loading[i].size(); ++k) pos = pos && loading[i].data()[k] > 0.0;
+    for (long k = 0; k < act[i].size(); ++k) pos = pos && act[i].data()[k] > 0.0;
+    if (!pos) throw std::invalid_argument("FastFcaParams: nonpositive loading/act");
+  }
+}
+
 }  // namespace fastfca

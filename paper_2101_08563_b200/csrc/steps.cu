@@ -105,6 +105,16 @@ __global__ void step_ip_kernel(double2* w, const double* qpack, double inv_block
   *status = ok ? kStatusOk : (kStatusIpSingular | (bad << 8));
 }
 
+// log_abs_det2 (sigmodel.cpp:118-129): LU with partial pivoting, one thread.
+template <int M>
+__global__ void step_logdet_kernel(const double2* w, double* out, int* status) {
+  if (threadIdx.x != 0) return;
+  double v = 0.0;
+  const bool ok = log_abs_det2<M, double>(w, v);
+  *out = v;
+  *status = ok ? kStatusOk : kStatusSingularW;
+}
+
 // source_gain (fastfca.cpp:74-78): G = L_n H_n / floor_positive(L H).
 __global__ void __launch_bounds__(kStepThreads)
     step_gain_kernel(const double* __restrict__ L, const double* __restrict__ H, int M, int N,
@@ -352,6 +362,41 @@ int ffca_ip_update_w(ffca_ctx* ctx, int dim, int sources, int blocks, int is_blo
                                             std::to_string(status >> 8));
   FFCA_CUDA(cudaMemcpyAsync(w, dw.p, size_t(M) * M * 16, cudaMemcpyDeviceToHost, st));
   FFCA_CUDA(cudaStreamSynchronize(st));
+  return FFCA_OK;
+}
+
+int ffca_log_abs_det2(ffca_ctx* ctx, int dim, const double* w, double* out) {
+  if (!ctx || !w || !out)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_log_abs_det2: null argument");
+  if (dim < 1 || dim > 8)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_log_abs_det2: dim outside 1..8");
+  ctx->launches = 0;
+  DeviceScope g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  DevBuf dw, dout, dstat;
+  if (dw.alloc(size_t(dim) * dim * 16) || dout.alloc(8) || dstat.alloc(4))
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca_log_abs_det2: device alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dw.p, w, size_t(dim) * dim * 16, cudaMemcpyHostToDevice, st));
+  auto* W = dw.as<double2>();
+  double* O = dout.as<double>();
+  int* S = dstat.as<int>();
+  switch (dim) {
+    case 1: step_logdet_kernel<1><<<1, 32, 0, st>>>(W, O, S); break;
+    case 2: step_logdet_kernel<2><<<1, 32, 0, st>>>(W, O, S); break;
+    case 3: step_logdet_kernel<3><<<1, 32, 0, st>>>(W, O, S); break;
+    case 4: step_logdet_kernel<4><<<1, 32, 0, st>>>(W, O, S); break;
+    case 5: step_logdet_kernel<5><<<1, 32, 0, st>>>(W, O, S); break;
+    case 6: step_logdet_kernel<6><<<1, 32, 0, st>>>(W, O, S); break;
+    case 7: step_logdet_kernel<7><<<1, 32, 0, st>>>(W, O, S); break;
+    default: step_logdet_kernel<8><<<1, 32, 0, st>>>(W, O, S); break;
+  }
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  int status = 0;
+  FFCA_CUDA(cudaMemcpyAsync(&status, S, 4, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaMemcpyAsync(out, O, 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  if (status == kStatusSingularW) return ffca_set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
   return FFCA_OK;
 }
 
