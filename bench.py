@@ -424,6 +424,37 @@ def main() -> None:
                "ms_per_step": 1e3 * et / len(times), "launches_per_step": ectx.launches(),
                "timing": "host clock around the synchronous C-ABI call, max over ranks"}
 
+    # e2e through the reference's C++ API (include/fastfca, csrc/shim.cpp):
+    # fastfca::fastfca_fit on host containers -- container -> pinned staging
+    # copies on host threads, the same pipelined C-ABI call, copies back into
+    # the result containers.  tools/cpp_e2e.cpp, rank 0 / single GPU only.
+    e2e_cpp = None
+    if not args.no_e2e and world == 1 and (ROOT / "tools" / "cpp_e2e.so").exists():
+        import ctypes as C
+        cpp = C.CDLL(str(ROOT / "tools" / "cpp_e2e.so"))
+        nst = min(args.steps, 5)
+        ms = np.zeros(nst)
+        nll_last = C.c_double(0.0)
+        err = C.create_string_buffer(512)
+        xh = np.ascontiguousarray(np.swapaxes(x, -1, -2)).astype(np.complex128)
+        Wh = np.ascontiguousarray(np.swapaxes(W0, -1, -2))
+        Lh = np.ascontiguousarray(np.swapaxes(L0, -1, -2))
+        Hh = np.ascontiguousarray(np.swapaxes(H0, -1, -2))
+        cpp.ffca_cpp_e2e.argtypes = [C.c_int] * 7 + [C.c_void_p] * 5 + [C.POINTER(C.c_double),
+                                                                      C.c_char_p, C.c_int]
+        rc = cpp.ffca_cpp_e2e(Pl, M, N, T, iters, 2, nst, xh.ctypes.data, Wh.ctypes.data,
+                              Lh.ctypes.data, Hh.ctypes.data, ms.ctypes.data, C.byref(nll_last),
+                              err, 512)
+        if rc == 0:
+            med = float(np.median(ms))
+            e2e_cpp = {"value": P * T * iters / (med / 1e3), "unit": UNIT, "ms_per_step": med,
+                       "nll_last": nll_last.value,
+                       "timing": "host clock around fastfca::fastfca_fit (SampleCovSet/FastFcaParams "
+                                 f"in, FastFcaFitResult out), median of {nst} after 2 warm-ups"}
+        else:
+            e2e_cpp = {"error": err.value.decode(errors="replace")}
+        del xh, Hh
+
     if rank == 0:
         pk = peaks()
         b_alg, f_alg = alg_bytes(M, N), alg_flops(M, N)
@@ -470,6 +501,7 @@ def main() -> None:
                                  " (traffic) differs from the algorithmic bytes"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_cpp_api": e2e_cpp,
             "gpu_launches": launches,
             "trace_off": trace_off,
             "separate": separate,

@@ -38,6 +38,7 @@ enum class Precision { fp32, fp64 };
 struct GpuOptions {
   std::vector<int> devices = {0};  // bins are split into contiguous ranges, one per device
   Precision precision = Precision::fp32;
+  int host_threads = 0;  // container <-> staging copies; 0 = hardware concurrency (at most 16)
 };
 
 // The per-step functions (fastfca.hpp:28-53), each a single-bin fp64 launch

@@ -87,6 +87,12 @@ int ffca_device_count(void);
 int ffca_ctx_create(int device, ffca_ctx** out);
 void ffca_ctx_destroy(ffca_ctx* ctx);
 
+/* Page-locked host staging owned by the context (slots 0..7, grow-only, freed
+ * with the context).  Host buffers passed to ffca_fit from such memory make
+ * its chunked H2D / fit / D2H pipeline asynchronous; any host memory works,
+ * pageable buffers just serialise the copies.  NULL on failure. */
+void* ffca_pinned_buffer(ffca_ctx* ctx, int slot, size_t bytes);
+
 /* fastfca_fit (fastfca.hpp:55-58, fastfca.cpp:146-191) over `batch`
  * independent mixtures.  W, L, H are the init on entry and the fitted
  * parameters on return (silent bins and iters == 0 keep the init bit-exactly).
@@ -271,6 +277,13 @@ int ffca_mm_update_lh(ffca_ctx* ctx, int dim, int sources, int frames, const dou
 
 /* Number of kernels the last call on this context launched (bench evidence). */
 int ffca_last_launch_count(const ffca_ctx* ctx);
+
+/* Diagnostics: the IP restart generator as the device runs it (fastfca.cpp:
+ * 13-18, 40-41: std::mt19937_64 seeded with mix_seed(seed, bin_index) feeding
+ * std::normal_distribution<double>): n raw 64-bit draws and n normal draws
+ * of a freshly seeded generator; *mixed_seed (nullable) = mix_seed. */
+int ffca_debug_restart_draws(ffca_ctx* ctx, uint64_t seed, int bin_index, int n,
+                             uint64_t* mixed_seed, uint64_t* raw, double* normals);
 
 /* Diagnostics: subsequent ffca_fit_device launches on this context record
  * per-problem phase cycle counters into dev_counters ([P][16] uint64, device

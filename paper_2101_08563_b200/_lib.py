@@ -31,7 +31,8 @@ EXPORTS = (
     "ffca_block_covs", "ffca_fit_covs", "ffca_ica_fit_covs", "ffca_nll_bins_covs",
     "ffca_decorrelated_powers_covs", "ffca_block_covs_device", "ffca_fit_covs_device",
     "ffca_weighted_cov", "ffca_ip_update_w", "ffca_source_gain", "ffca_em_update_lh",
-    "ffca_mm_update_lh", "ffca_log_abs_det2",
+    "ffca_mm_update_lh", "ffca_log_abs_det2", "ffca_debug_restart_draws",
+    "ffca_pinned_buffer",
 )
 STFT_CENTERED, STFT_FULL_FRAMES = 0, 1
 
@@ -118,6 +119,9 @@ def lib() -> C.CDLL:
         L.ffca_em_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
         L.ffca_mm_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
         L.ffca_log_abs_det2.argtypes = [P, i, P, P]
+        L.ffca_pinned_buffer.argtypes = [P, i, C.c_size_t]
+        L.ffca_pinned_buffer.restype = P
+        L.ffca_debug_restart_draws.argtypes = [P, C.c_uint64, i, i, P, P, P]
         L.ffca_debug_set_timing.argtypes = [P, P]
         _ = dp
         _lib = L

@@ -108,9 +108,21 @@ def build_oracle() -> None:
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
 
 
+def build_cpp_e2e() -> Path:
+    """bench.py's C++-API end-to-end leg (tools/cpp_e2e.cpp) against libffca.so."""
+    src = ROOT / "tools" / "cpp_e2e.cpp"
+    out = ROOT / "tools" / "cpp_e2e.so"
+    if _stale(out, src, [LIB, *sorted((ROOT / "include").rglob("*.h*"))]):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wno-class-memaccess",
+              "-I", str(ROOT / "include"), str(src), "-L", str(PKG), "-lffca",
+              "-Wl,-rpath," + str(PKG), "-pthread", "-o", str(out)])
+    return out
+
+
 def build_all(verbose: bool = False) -> None:
     build_oracle()
     build_lib(verbose=verbose)
+    build_cpp_e2e()
 
 
 if __name__ == "__main__":

@@ -117,7 +117,9 @@ struct PolarNormal {
     do {
       x = 2.0 * canonical(g) - 1.0;
       y = 2.0 * canonical(g) - 1.0;
-      r2 = x * x + y * y;
+      // separately rounded products and sum, as the reference's baseline
+      // x86-64 build evaluates libstdc++'s x * x + y * y (no FMA contraction)
+      r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
     } while (r2 > 1.0 || r2 == 0.0);
     const double mult = sqrt(-2.0 * log(r2) / r2);
     saved = x * mult;

@@ -75,34 +75,6 @@ int launch_fit(ffca_ctx* ctx, int M, FitParams& fp, cudaStream_t st) {
   return set_err(FFCA_INVALID_ARGUMENT, "ffca: unsupported dim");
 }
 
-template <int M, typename R, typename OutC>
-int launch_sep_m(ffca_ctx* ctx, const void* xs, const double* W, const double* L, const void* Hs,
-                 int P, int N, int T, OutC* out, cudaStream_t st) {
-  using C = cplx_t<R>;
-  separate_kernel<M, R, OutC><<<P, 256, 0, st>>>(
-      reinterpret_cast<const C*>(xs), reinterpret_cast<const double2*>(W), L,
-      reinterpret_cast<const R*>(Hs), P, N, T, out);
-  ctx->launches++;
-  FFCA_CUDA(cudaGetLastError());
-  return FFCA_OK;
-}
-
-template <typename R, typename OutC>
-int launch_sep(ffca_ctx* ctx, int M, const void* xs, const double* W, const double* L,
-               const void* Hs, int P, int N, int T, OutC* out, cudaStream_t st) {
-  switch (M) {
-    case 1: return launch_sep_m<1, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 2: return launch_sep_m<2, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 3: return launch_sep_m<3, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 4: return launch_sep_m<4, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 5: return launch_sep_m<5, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 6: return launch_sep_m<6, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 7: return launch_sep_m<7, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-    case 8: return launch_sep_m<8, R>(ctx, xs, W, L, Hs, P, N, T, out, st);
-  }
-  return set_err(FFCA_INVALID_ARGUMENT, "ffca: unsupported dim");
-}
-
 // Stage host fp64 x and H on the device and convert them to the compute type.
 // x keeps its fp64 staging copy in slot kX (power_scale reads it).
 template <typename R>
@@ -529,10 +501,29 @@ void ffca_ctx_destroy(ffca_ctx* ctx) {
   DeviceGuard g(ctx->device);
   for (auto& b : ctx->bufs)
     if (b.p) cudaFree(b.p);
+  for (auto& b : ctx->pinned)
+    if (b.p) cudaFreeHost(b.p);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto& s : ctx->cstream)
     if (s) cudaStreamDestroy(s);
   delete ctx;
+}
+
+void* ffca_pinned_buffer(ffca_ctx* ctx, int slot, size_t bytes) {
+  if (!ctx || slot < 0 || slot >= 8) return nullptr;
+  DeviceGuard g(ctx->device);
+  ffca_ctx::Buf& b = ctx->pinned[slot];
+  if (b.p && b.n >= bytes) return b.p;
+  if (b.p) cudaFreeHost(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  if (cudaHostAlloc(&b.p, bytes < 4096 ? 4096 : bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return nullptr;
+  }
+  b.n = bytes;
+  return b.p;
 }
 
 int ffca_last_launch_count(const ffca_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -747,9 +738,7 @@ int ffca_separate(ffca_ctx* ctx, const ffca_dims* d, int precision, const double
   if (!dW || !dL || !dimg) return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
   FFCA_CUDA(cudaMemcpyAsync(dW, W, size_t(P) * M * M * 16, cudaMemcpyHostToDevice, st));
   FFCA_CUDA(cudaMemcpyAsync(dL, L, size_t(P) * M * N * 8, cudaMemcpyHostToDevice, st));
-  rc = (precision == FFCA_PREC_FP64)
-           ? launch_sep<double>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, st)
-           : launch_sep<float>(ctx, M, xs, dW, dL, hs, P, N, T, dimg, st);
+  rc = launch_separate(ctx, M, precision == FFCA_PREC_FP64, true, xs, dW, dL, hs, P, N, T, dimg, st);
   if (rc) return rc;
   FFCA_CUDA(cudaMemcpyAsync(images, dimg, nimg * 16, cudaMemcpyDeviceToHost, st));
   FFCA_CUDA(cudaStreamSynchronize(st));
@@ -850,11 +839,8 @@ int ffca_separate_device(ffca_ctx* ctx, int problems, int dim, int sources, int 
   DeviceGuard g(ctx->device);
   ctx->launches = 0;
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return precision == FFCA_PREC_FP64
-             ? launch_sep<double>(ctx, dim, x_dev, W, L, H_dev, problems, sources, frames,
-                                  static_cast<double2*>(images_dev), st)
-             : launch_sep<float>(ctx, dim, x_dev, W, L, H_dev, problems, sources, frames,
-                                 static_cast<float2*>(images_dev), st);
+  return launch_separate(ctx, dim, precision == FFCA_PREC_FP64, false, x_dev, W, L, H_dev, problems,
+                         sources, frames, images_dev, st);
 }
 
 int ffca_power_scale_device(ffca_ctx* ctx, int problems, int dim, int frames, int precision,

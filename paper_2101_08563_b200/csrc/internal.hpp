@@ -31,6 +31,7 @@ struct ffca_ctx {
     size_t n = 0;
   };
   Buf bufs[16];
+  Buf pinned[8];  // page-locked host staging (ffca_pinned_buffer)
   // Grow-only device scratch, slot k.
   void* get(int k, size_t bytes, cudaError_t* err) {
     Buf& b = bufs[k];
@@ -48,7 +49,7 @@ struct ffca_ctx {
 
 namespace ffca {
 
-enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kWave, kSpec, kFrames, kNumSlots };
+enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kWave, kSpec, kFrames, kSepRec, kNumSlots };
 
 // Threads per fit CTA: about 4 frames per thread, capped at the kernel's
 // launch bound; a multiple of 32*M when the weighted-covariance pass is split
@@ -75,6 +76,13 @@ FFCA_DECLARE_FIT_LAUNCHER(5)
 FFCA_DECLARE_FIT_LAUNCHER(6)
 FFCA_DECLARE_FIT_LAUNCHER(7)
 FFCA_DECLARE_FIT_LAUNCHER(8)
+
+// fastfca_separate (separate.cu).  xs / Hs: device x [P][T][M], H [P][T][N] in
+// the compute type; out: images [N][P][T][M] in the compute type, or fp64
+// images from the fp32 compute path when out_double (host-path staging).
+int launch_separate(ffca_ctx* ctx, int M, bool fp64, bool out_double, const void* xs,
+                    const double* W, const double* L, const void* Hs, int P, int N, int T,
+                    void* out, cudaStream_t st);
 
 // Large-bin kernel (fit_big.cu): sets *handled when it took the fit.
 int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp64, bool* handled);

@@ -49,50 +49,114 @@ int prec(const GpuOptions& g) {
   return g.precision == Precision::fp64 ? FFCA_PREC_FP64 : FFCA_PREC_FP32;
 }
 
-// Contiguous host copies of bins [lo, hi) in the ABI's (reference) layout.
+// Host staging of the ABI's flat buffers.  The large ones (x, H) live in
+// page-locked memory owned by the device context (ffca_pinned_buffer), so the
+// library's chunked H2D / fit / D2H pipeline runs truly asynchronously; small
+// ones (power, W, L) are plain vectors.
+struct HostBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  std::vector<double> own;
+  void resize(size_t count, ffca_ctx* ctx = nullptr, int slot = -1) {
+    n = count;
+    p = nullptr;
+    if (ctx && slot >= 0 && count > 0)
+      p = static_cast<double*>(ffca_pinned_buffer(ctx, slot, count * sizeof(double)));
+    if (!p) {
+      own.resize(count);
+      p = own.data();
+    }
+  }
+  double* data() { return p; }
+  const double* data() const { return p; }
+  bool empty() const { return n == 0; }
+};
+
+// Contiguous host copies of bins in the ABI's (reference) layout.
 // x: the snapshots [bin][frame][dim], or for a block set (no snapshots) the
 // block covariances [bin][block][dim*dim] (ffca.h *_covs entry points).
 // power: power_scale, or empty for a block set without one (the library
 // then takes SampleCovSet::power()'s trace fallback, sigmodel.cpp:50-55).
 struct Packed {
-  std::vector<double> x, power, W, L, H;
+  HostBuf x, power, W, L, H;
   bool snap = true;
   const double* pw() const { return power.empty() ? nullptr : power.data(); }
 };
 
-void pack_bins(const SampleCovSet& covs, const FastFcaParams& p, int lo, int hi, Packed& out) {
-  const int M = covs.dim, N = p.sources, T = covs.blocks, n = hi - lo;
+int host_threads(const GpuOptions& g, int work) {
+  int n = g.host_threads > 0 ? g.host_threads : int(std::thread::hardware_concurrency());
+  n = std::max(1, std::min(n, 16));
+  return std::max(1, std::min(n, work));
+}
+
+// fn(i) for i in [0, count) on nt host threads (contiguous ranges).
+template <typename Fn>
+void parallel_bins(int count, int nt, Fn fn) {
+  if (nt <= 1 || count < 2 * nt) {
+    for (int i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([=] {
+      const int lo = int((long long)count * t / nt), hi = int((long long)count * (t + 1) / nt);
+      for (int i = lo; i < hi; ++i) fn(i);
+    });
+  for (auto& t : th) t.join();
+}
+
+// Size `out` for `total` bins of this shape; ctx != null puts x and H in the
+// context's pinned staging.
+void size_packed(const SampleCovSet& covs, int sources, int total, Packed& out, ffca_ctx* ctx) {
+  const int M = covs.dim, N = sources, T = covs.blocks;
   out.snap = covs.has_snapshots();
   const size_t rec = out.snap ? size_t(M) * 2 : size_t(M) * M * 2;  // doubles per frame / block
   const bool has_pw = long(covs.power_scale.size()) == covs.bins;
-  out.x.resize(size_t(n) * T * rec);
-  out.power.resize(has_pw ? n : 0);
-  out.W.resize(size_t(n) * M * M * 2);
-  out.L.resize(size_t(n) * M * N);
-  out.H.resize(size_t(n) * N * T);
-  for (int i = lo; i < hi; ++i) {
-    const size_t k = size_t(i - lo);
+  out.x.resize(size_t(total) * T * rec, ctx, 0);
+  out.power.resize(has_pw ? total : 0);
+  out.W.resize(size_t(total) * M * M * 2);
+  out.L.resize(size_t(total) * M * N);
+  out.H.resize(size_t(total) * N * T, ctx, 1);
+}
+
+// Bins [lo, hi) of (covs, p) into rows [at, at + hi - lo) of `out`.
+void pack_into(const SampleCovSet& covs, const FastFcaParams& p, int lo, int hi, Packed& out,
+               int at, int nt) {
+  const int M = covs.dim, N = p.sources, T = covs.blocks;
+  const size_t rec = out.snap ? size_t(M) * 2 : size_t(M) * M * 2;
+  const bool has_pw = !out.power.empty();
+  parallel_bins(hi - lo, nt, [&, lo, at](int j) {
+    const int i = lo + j;
+    const size_t k = size_t(at + j);
     if (out.snap) {
       std::memcpy(out.x.data() + k * T * rec, covs.snapshots[i].data(), sizeof(double) * T * rec);
     } else {
-      for (int j = 0; j < T; ++j)
-        std::memcpy(out.x.data() + (k * T + j) * rec, covs.mats[i][j].data(), sizeof(double) * rec);
+      for (int jb = 0; jb < T; ++jb)
+        std::memcpy(out.x.data() + (k * T + jb) * rec, covs.mats[i][jb].data(), sizeof(double) * rec);
     }
-    if (has_pw) out.power[k] = covs.power_scale(i);
+    if (has_pw) out.power.data()[k] = covs.power_scale(i);
     std::memcpy(out.W.data() + k * M * M * 2, p.decorr[i].data(), sizeof(double) * M * M * 2);
     std::memcpy(out.L.data() + k * M * N, p.loading[i].data(), sizeof(double) * M * N);
     std::memcpy(out.H.data() + k * N * T, p.act[i].data(), sizeof(double) * N * T);
-  }
+  });
 }
 
-void unpack_bins(const Packed& in, int lo, int hi, FastFcaParams& p) {
+void pack_bins(const SampleCovSet& covs, const FastFcaParams& p, int lo, int hi, Packed& out,
+               ffca_ctx* ctx = nullptr, int nt = 1) {
+  size_packed(covs, p.sources, hi - lo, out, ctx);
+  pack_into(covs, p, lo, hi, out, 0, nt);
+}
+
+// Rows [at, at + hi - lo) of `in` into bins [lo, hi) of p.
+void unpack_bins(const Packed& in, int lo, int hi, FastFcaParams& p, int at = 0, int nt = 1) {
   const int M = p.dim, N = p.sources, T = p.frames;
-  for (int i = lo; i < hi; ++i) {
-    const size_t k = size_t(i - lo);
+  parallel_bins(hi - lo, nt, [&, lo, at](int j) {
+    const int i = lo + j;
+    const size_t k = size_t(at + j);
     std::memcpy(p.decorr[i].data(), in.W.data() + k * M * M * 2, sizeof(double) * M * M * 2);
     std::memcpy(p.loading[i].data(), in.L.data() + k * M * N, sizeof(double) * M * N);
     std::memcpy(p.act[i].data(), in.H.data() + k * N * T, sizeof(double) * N * T);
-  }
+  });
 }
 
 // A set the kernels can read: snapshots (dim x blocks each) with power_scale,
@@ -409,20 +473,30 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
   check_fit_shapes(covs, init);
   if (iters < 0) throw std::invalid_argument("fastfca_fit: negative iteration count");
   FastFcaFitResult result;
-  result.params = init;  // fastfca.cpp:153-154
   const int F = covs.bins;
+  {
+    // result.params = init (fastfca.cpp:153-154); the activations -- the bulk,
+    // 1.6 GB of fresh pages at BASELINE config 3 -- are copied on host threads.
+    FastFcaParams& rp = result.params;
+    rp.dim = init.dim, rp.bins = init.bins, rp.frames = init.frames, rp.sources = init.sources;
+    rp.decorr = init.decorr;
+    rp.loading = init.loading;
+    rp.act.resize(init.act.size());
+    parallel_bins(int(init.act.size()), host_threads(gpu, F), [&](int i) { rp.act[i] = init.act[i]; });
+  }
   const ffca_fit_opts o = fit_opts(flavor, iters, fit, opts, gpu);
   std::vector<double> slots(fit.record_trace ? size_t(iters + 1) * F : 0);
   over_devices(gpu.devices, F, [&](int dev, int lo, int hi) {
     Packed pk;
-    pack_bins(covs, init, lo, hi, pk);
     const int n = hi - lo;
+    const int nt = host_threads(gpu, n);
+    pack_bins(covs, init, lo, hi, pk, context(dev), nt);
     std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
     ffca_dims d{1, n, covs.dim, init.sources, covs.blocks, lo, F};
     raise((pk.snap ? ffca_fit : ffca_fit_covs)(context(dev), &d, &o, pk.x.data(), pk.pw(),
                                                pk.W.data(), pk.L.data(), pk.H.data(), nullptr,
                                                fit.record_trace ? sl.data() : nullptr, nullptr));
-    if (iters > 0) unpack_bins(pk, lo, hi, result.params);
+    if (iters > 0) unpack_bins(pk, lo, hi, result.params, 0, nt);
     for (int t = 0; fit.record_trace && t <= iters; ++t)
       for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
   });
@@ -462,30 +536,17 @@ std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>&
   for (int b = 0; b < B; ++b) out[b].params = init[b];
   over_devices(gpu.devices, B, [&](int dev, int lo, int hi) {  // whole mixtures per device
     const int nb = hi - lo;
-    std::vector<Packed> pk(nb);
+    const int nt = host_threads(gpu, F);
     Packed all;
-    for (int b = lo; b < hi; ++b) {
-      pack_bins(covs[b], init[b], 0, F, pk[b - lo]);
-      using Field = std::vector<double> Packed::*;
-      for (Field v : {&Packed::x, &Packed::power, &Packed::W, &Packed::L, &Packed::H})
-        (all.*v).insert((all.*v).end(), (pk[b - lo].*v).begin(), (pk[b - lo].*v).end());
-    }
+    size_packed(covs[0], init[0].sources, nb * F, all, context(dev));
+    for (int b = lo; b < hi; ++b) pack_into(covs[b], init[b], 0, F, all, (b - lo) * F, nt);
     std::vector<double> nll(fit.record_trace ? size_t(nb) * (iters + 1) : 0);
     ffca_dims d{nb, F, covs[0].dim, init[0].sources, covs[0].blocks, 0, 0};
     raise((covs[0].has_snapshots() ? ffca_fit : ffca_fit_covs)(
         context(dev), &d, &o, all.x.data(), all.pw(), all.W.data(), all.L.data(), all.H.data(),
         fit.record_trace ? nll.data() : nullptr, nullptr, nullptr));
-    if (iters > 0) {
-      const int M = covs[0].dim, N = init[0].sources, T = covs[0].blocks;
-      for (int b = lo; b < hi; ++b) {
-        Packed one;
-        const size_t k = size_t(b - lo);
-        one.W.assign(all.W.begin() + k * F * M * M * 2, all.W.begin() + (k + 1) * F * M * M * 2);
-        one.L.assign(all.L.begin() + k * F * M * N, all.L.begin() + (k + 1) * F * M * N);
-        one.H.assign(all.H.begin() + k * F * N * T, all.H.begin() + (k + 1) * F * N * T);
-        unpack_bins(one, 0, F, out[b].params);
-      }
-    }
+    if (iters > 0)
+      for (int b = lo; b < hi; ++b) unpack_bins(all, 0, F, out[b].params, (b - lo) * F, nt);
     if (fit.record_trace)
       for (int b = lo; b < hi; ++b)
         out[b].nll.assign(nll.begin() + size_t(b - lo) * (iters + 1),

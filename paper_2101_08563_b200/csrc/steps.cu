@@ -105,6 +105,20 @@ __global__ void step_ip_kernel(double2* w, const double* qpack, double inv_block
   *status = ok ? kStatusOk : (kStatusIpSingular | (bad << 8));
 }
 
+// Diagnostics: the restart generator's streams (common.cuh Mt19937_64 /
+// PolarNormal seeded with mix_seed(seed, bin), fastfca.cpp:40-41) -- n raw
+// 64-bit draws, and n normal draws from a freshly seeded copy.
+__global__ void debug_rng_kernel(unsigned long long seed, int bin, int n, RestartRng* rr,
+                                 unsigned long long* raw, double* normals) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  rr->mt.seed(mix_seed(seed, bin));
+  for (int k = 0; k < n; ++k) raw[k] = rr->mt.next();
+  rr->mt.seed(mix_seed(seed, bin));
+  rr->gauss.saved = 0.0;
+  rr->gauss.has_saved = false;
+  for (int k = 0; k < n; ++k) normals[k] = rr->gauss(rr->mt);
+}
+
 // log_abs_det2 (sigmodel.cpp:118-129): LU with partial pivoting, one thread.
 template <int M>
 __global__ void step_logdet_kernel(const double2* w, double* out, int* status) {
@@ -362,6 +376,27 @@ int ffca_ip_update_w(ffca_ctx* ctx, int dim, int sources, int blocks, int is_blo
                                             std::to_string(status >> 8));
   FFCA_CUDA(cudaMemcpyAsync(w, dw.p, size_t(M) * M * 16, cudaMemcpyDeviceToHost, st));
   FFCA_CUDA(cudaStreamSynchronize(st));
+  return FFCA_OK;
+}
+
+int ffca_debug_restart_draws(ffca_ctx* ctx, uint64_t seed, int bin_index, int n,
+                             uint64_t* mixed_seed, uint64_t* raw, double* normals) {
+  if (!ctx || !raw || !normals || n < 1)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_debug_restart_draws: bad argument");
+  ctx->launches = 0;
+  DeviceScope g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  DevBuf drng, draw, dn;
+  if (drng.alloc(sizeof(RestartRng)) || draw.alloc(size_t(n) * 8) || dn.alloc(size_t(n) * 8))
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca_debug_restart_draws: device alloc failed");
+  debug_rng_kernel<<<1, 32, 0, st>>>(seed, bin_index, n, drng.as<RestartRng>(),
+                                     draw.as<unsigned long long>(), dn.as<double>());
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  FFCA_CUDA(cudaMemcpyAsync(raw, draw.p, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaMemcpyAsync(normals, dn.p, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  if (mixed_seed) *mixed_seed = mix_seed(seed, bin_index);
   return FFCA_OK;
 }
 
