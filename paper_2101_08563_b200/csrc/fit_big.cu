@@ -1,6 +1,6 @@
 // fit_big.cu -- instantiations and launcher of the large-bin fit kernel
 // (fit_big.cuh): M = 8, N = 12 (BASELINE config 3) in fp32 and the fp64
-// check mode.
+// check mode, and M = 4, N = 6 (BASELINE config 2) in fp32.
 #include <cstdlib>
 
 #include "fit_big.cuh"
@@ -10,7 +10,7 @@ namespace ffca {
 
 namespace {
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, int MINB = 1>
 int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
   using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
   *handled = false;
@@ -24,11 +24,11 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
   *handled = true;
   if (fp.nprob == 0) return FFCA_OK;
   if (C == 1) {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     kern<<<fp.nprob, NTHR, lay.total, st>>>(fp, lay);
   } else {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true, MINB>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
@@ -62,6 +62,13 @@ int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp
     if (fp64) return launch_big_t<8, 12, double, 4, 448, 2>(ctx, fp, st, handled);
     return launch_big_t<8, 12, float, 8, 512, 1>(ctx, fp, st, handled);
   }
+  // BASELINE config 2 (M = 4, N = 6, T = 2000): 256 threads x 8 frame slots
+  // hold a 2048-frame bin in one CTA; three CTAs (three bins) share an SM
+  // (66 KB of H planes and 128 tensor-memory columns each), so one bin's
+  // reductions and IP overlap the others' frame passes.  Short bins stay with
+  // fit_kernel (one resident CTA in shared memory is cheaper there).
+  if (M == 4 && fp.N == 6 && !fp64 && fp.T > 512)
+    return launch_big_t<4, 6, float, 8, 256, 1, 3>(ctx, fp, st, handled);
   return FFCA_OK;
 }
 

@@ -95,6 +95,8 @@ struct BigCfg {
   static constexpr int MW = M / MS;                // weights per covariance lane
   static constexpr int KA = NP * MW;               // accumulators per covariance lane
   static constexpr int GS = M * MS;                // covariance lanes per frame
+  static constexpr int KAP = ((KA + 32 / GS - 1) / (32 / GS)) * (32 / GS);  // padded so that the
+                                                   // in-warp reduce-scatter halves evenly
   static constexpr int KRED = 2 * M + 1;           // EM sweep partials
   static constexpr int KQ = M * M * M;             // covariance totals
   static constexpr int WPR = M * int(sizeof(R)) / 4;  // TMEM columns per record
@@ -102,15 +104,17 @@ struct BigCfg {
   static constexpr int WGROUPS = (NW + 3) / 4;     // warps sharing a TMEM lane quarter
   static constexpr int PW = pow2_at_least(NW);
   static constexpr int HW = PW / 2 > 0 ? PW / 2 : 1;  // warps publishing in the first tree step
-  static constexpr int CNT = [] {
-    int c = KA;
-    for (int o = 16; o >= GS; o >>= 1) c /= 2;
+  static constexpr int CNT = KAP / (32 / GS);  // covariance partials per lane after the
+                                               // in-warp reduce-scatter
+  static constexpr int TMCOLS = [] {           // tensor-memory columns (a power of two >= 32)
+    int c = 32;
+    while (c < SLOTS * SCOL * WGROUPS) c <<= 1;
     return c;
-  }();  // covariance partials per lane after the in-warp reduce-scatter
+  }();
   static_assert(32 % GS == 0 && 32 % M == 0, "lanes per frame must divide a warp");
   static_assert(NTHR % 32 == 0, "whole warps");
   static_assert(SLOTS * SCOL * WGROUPS <= 512, "tensor memory columns");
-  static_assert(WPR == 8 || WPR == 16, "record width");
+  static_assert(WPR == 4 || WPR == 8 || WPR == 16, "record width");
 
   static int al(int v) { return (v + 15) & ~15; }
   static BigLayout layout(int csize) {
@@ -188,6 +192,20 @@ __device__ __forceinline__ void cluster_wait() {
 // 32x32b register transfers: thread l of the warp reads / writes TMEM lane
 // (quarter base + l), columns [col, col + n).  Raw 32-bit words; a double is
 // two columns (low word first).
+__device__ __forceinline__ void tm_ld4(unsigned a, unsigned (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void tm_st4(unsigned a, const unsigned (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <int NWORDS>
+__device__ __forceinline__ void tm_ld(unsigned a, unsigned (&v)[NWORDS]);
+template <int NWORDS>
+__device__ __forceinline__ void tm_st(unsigned a, const unsigned (&v)[NWORDS]);
 __device__ __forceinline__ void tm_ld8(unsigned a, unsigned (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
@@ -218,54 +236,60 @@ __device__ __forceinline__ void tm_st16(unsigned a, const unsigned (&v)[16]) {
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
+template <> __device__ __forceinline__ void tm_ld<4>(unsigned a, unsigned (&v)[4]) { tm_ld4(a, v); }
+template <> __device__ __forceinline__ void tm_ld<8>(unsigned a, unsigned (&v)[8]) { tm_ld8(a, v); }
+template <> __device__ __forceinline__ void tm_ld<16>(unsigned a, unsigned (&v)[16]) { tm_ld16(a, v); }
+template <> __device__ __forceinline__ void tm_st<4>(unsigned a, const unsigned (&v)[4]) { tm_st4(a, v); }
+template <> __device__ __forceinline__ void tm_st<8>(unsigned a, const unsigned (&v)[8]) { tm_st8(a, v); }
+template <> __device__ __forceinline__ void tm_st<16>(unsigned a, const unsigned (&v)[16]) { tm_st16(a, v); }
+
+// Words <-> values of the compute type.
+template <int M, typename R>
+__device__ __forceinline__ void words_to(const unsigned* w, R (&v)[M]) {
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if constexpr (sizeof(R) == 4) v[m] = __uint_as_float(w[m]);
+    else v[m] = __hiloint2double(int(w[2 * m + 1]), int(w[2 * m]));
+  }
+}
 // One record of M values in the compute type.
 template <int M, typename R>
 __device__ __forceinline__ void tm_load_rec(unsigned a, R (&v)[M]) {
-  static_assert(M == 8, "records are 8 values");
-  if constexpr (sizeof(R) == 4) {
-    unsigned w[8];
-    tm_ld8(a, w);
-    tm_wait_ld();
-#pragma unroll
-    for (int m = 0; m < M; ++m) v[m] = __uint_as_float(w[m]);
-  } else {
-    unsigned w[16];
-    tm_ld16(a, w);
-    tm_wait_ld();
-#pragma unroll
-    for (int m = 0; m < M; ++m) v[m] = __hiloint2double(int(w[2 * m + 1]), int(w[2 * m]));
-  }
+  constexpr int NWD = M * int(sizeof(R)) / 4;
+  unsigned w[NWD];
+  tm_ld<NWD>(a, w);
+  tm_wait_ld();
+  words_to<M, R>(w, v);
 }
-// Two adjacent records (U then Phi) in one transfer.
+// Two adjacent records (U then Phi) in one transfer when they fit 16 words.
 template <int M, typename R>
 __device__ __forceinline__ void tm_load_rec2(unsigned a, R (&u)[M], R (&ph)[M]) {
-  if constexpr (sizeof(R) == 4) {
-    unsigned w[16];
-    tm_ld16(a, w);
+  constexpr int NWD = M * int(sizeof(R)) / 4;
+  if constexpr (2 * NWD <= 16) {
+    unsigned w[2 * NWD];
+    tm_ld<2 * NWD>(a, w);
     tm_wait_ld();
-#pragma unroll
-    for (int m = 0; m < M; ++m) u[m] = __uint_as_float(w[m]), ph[m] = __uint_as_float(w[M + m]);
+    words_to<M, R>(w, u);
+    words_to<M, R>(w + NWD, ph);
   } else {
     tm_load_rec<M, R>(a, u);
-    tm_load_rec<M, R>(a + 16, ph);
+    tm_load_rec<M, R>(a + NWD, ph);
   }
 }
 template <int M, typename R>
 __device__ __forceinline__ void tm_store_rec(unsigned a, const R (&v)[M]) {
-  if constexpr (sizeof(R) == 4) {
-    unsigned w[8];
+  constexpr int NWD = M * int(sizeof(R)) / 4;
+  unsigned w[NWD];
 #pragma unroll
-    for (int m = 0; m < M; ++m) w[m] = __float_as_uint(v[m]);
-    tm_st8(a, w);
-  } else {
-    unsigned w[16];
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
+  for (int m = 0; m < M; ++m) {
+    if constexpr (sizeof(R) == 4) {
+      w[m] = __float_as_uint(v[m]);
+    } else {
       w[2 * m] = unsigned(__double2loint(v[m]));
       w[2 * m + 1] = unsigned(__double2hiint(v[m]));
     }
-    tm_st16(a, w);
   }
+  tm_st<NWD>(a, w);
 }
 
 // Packed fp32 pairs (FFMA2 / FMUL2 on sm_100): the frame loops are issue
@@ -278,14 +302,15 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(
 __device__ __forceinline__ float2 fmul2s(float2 a, float s) { return __fmul2_rn(a, f2(s, s)); }
 __device__ __forceinline__ float2 fneg2(float2 a) { return f2(-a.x, -a.y); }
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL>
-__global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout lay) {
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL, int MINB = 1>
+__global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLayout lay) {
   using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
   using C = cplx_t<R>;
   using V = typename Vec16<R>::type;
   constexpr int VE = Cfg::VE, NHP = Cfg::NHP, NW = Cfg::NW, PW = Cfg::PW, HW = Cfg::HW;
   constexpr int D = Cfg::D, NP = Cfg::NP, MW = Cfg::MW, KA = Cfg::KA, GS = Cfg::GS;
   constexpr int KRED = Cfg::KRED, KQ = Cfg::KQ, WPR = Cfg::WPR, SCOL = Cfg::SCOL, CNT = Cfg::CNT;
+  constexpr int KAP = Cfg::KAP, TMCOLS = Cfg::TMCOLS;
   using B = R;
   using BM = SMath<B>;
   namespace cg = cooperative_groups;
@@ -307,6 +332,9 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   const int Tl = int((long long)T * (crank + 1) / csize) - t0g;
   const bool lead = crank == 0;
   const int ps = lay.ps;
+  // Frame slots in use: short bins skip the empty ones (an even count, the
+  // fp32 EM sweep takes two slots per trip).
+  const int nsl = min(SLOTS, (((Tl + NTHR - 1) / NTHR) + 1) & ~1);
   // Phase timing (diagnostics build, -DFFCA_PHASE_TIMING): thread 0 of each
   // CTA accumulates clock64 deltas; CTA rank 0 reports them per bin.
   // 0 U pass, 1 EM frames, 2 EM reduce/update, 3 balance, 4 A1, 5 A2 frames,
@@ -359,10 +387,10 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   const C* xg = reinterpret_cast<const C*>(p.x) + (size_t(b) * T + t0g) * M;
   R* Hg = reinterpret_cast<R*>(p.H) + (size_t(b) * T + t0g) * N;
 
-  // ---- tensor memory: all 512 columns (one CTA per SM).
+  // ---- tensor memory: TMCOLS columns (all 512 for the one-CTA-per-SM shapes).
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-        unsigned(__cvta_generic_to_shared(&sc->tmem))));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+        unsigned(__cvta_generic_to_shared(&sc->tmem))), "n"(TMCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   // ---- load the bin: H into planes (pad entries 0), W, L, scalars.
@@ -475,7 +503,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       // y_m = sum_c conj(W(c,m)) x_c = sum_c Re W(c,m) x_c + i sum_c Im W(c,m) (Im x_c, -Re x_c),
       // U(m) written straight to the frame's TMEM column.
 #pragma unroll 1
-      for (int s = 0; s < SLOTS; ++s) {
+      for (int s = 0; s < nsl; ++s) {
         const int t0 = frame_of(s, lane);
         const int t = t0 < Tl ? t0 : 0;
         float2 xc[M];
@@ -517,7 +545,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
 #pragma unroll
     for (int c = 0; c < M; ++c) wc[c] = Wr[c + j * M];
 #pragma unroll 1
-    for (int s = 0; s < SLOTS; ++s) {
+    for (int s = 0; s < nsl; ++s) {
       R uo[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) uo[m] = R(0);
@@ -597,7 +625,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       for (int q = 0; q < MP; ++q) a2[q] = f2(0.f, 0.f), p2[q] = f2(0.f, 0.f);
       float hacc = 0.f;
 #pragma unroll 1
-      for (int s = 0; s < SLOTS; s += 2) {
+      for (int s = 0; s < nsl; s += 2) {
         int t[2];
         bool ok[2];
         float2 u[2][MP], ph[2][MP], lh[2][MP];
@@ -663,7 +691,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
       acc[M] = hacc;
     } else {
 #pragma unroll 1
-    for (int s = 0; s < SLOTS; ++s) {
+    for (int s = 0; s < nsl; ++s) {
       const int t0 = frame_of(s, lane);
       const bool ok = t0 < Tl;
       const int t = ok ? t0 : 0;
@@ -744,7 +772,7 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
 #pragma unroll
     for (int k = 0; k <= M; ++k) nacc[k] = R(0);
 #pragma unroll 1
-    for (int s = 0; s < SLOTS; ++s) {
+    for (int s = 0; s < nsl; ++s) {
       const int t0 = frame_of(s, lane);
       const bool ok = t0 < Tl;
       const int t = ok ? t0 : 0;
@@ -784,15 +812,15 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
   auto a2_pass = [&](bool want_q, const R (&nacc)[M + 1], double (&nll_tot)[M + 1]) {
     constexpr int FPB = 32 / GS;  // frames per batch
     const int a = lane % M, mh = (lane / M) % MS, g = lane / GS;
-    R acc[KA];
+    R acc[KAP];  // [jj * MW + mm], zero padding up to KAP
 #pragma unroll
-    for (int k = 0; k < KA; ++k) acc[k] = R(0);
+    for (int k = 0; k < KAP; ++k) acc[k] = R(0);
     int coff[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) coff[d] = (a + d) % M;
     if (want_q) {
 #pragma unroll 1
-      for (int s = 0; s < SLOTS; ++s) {
+      for (int s = 0; s < nsl; ++s) {
         R ro[M];  // this lane's own frame weights 1/sigma^2
         tm_load_rec<M, R>(tm_u(s), ro);
 #pragma unroll 2
@@ -849,13 +877,13 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
     // Lanes of equal role (lane mod GS) hold partials of the same products:
     // reduce-scatter over the frame groups of the warp.
     int base = 0;
-    int cnt = KA;
+    int cnt = KAP;
 #pragma unroll
     for (int o = 16; o >= GS; o >>= 1) {
       const bool up = (lane & o) != 0;
-      const int h2 = cnt / 2;  // KA is even for M >= 2
+      const int h2 = cnt / 2;  // KAP halves evenly down to CNT
 #pragma unroll
-      for (int i = 0; i < KA / 2; ++i) {
+      for (int i = 0; i < KAP / 2; ++i) {
         if (i < h2) {
           const R send = up ? acc[i] : acc[i + h2];
           const R keep = up ? acc[i + h2] : acc[i];
@@ -898,7 +926,9 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
           const int m = rmh * MW + mm;
           int idx = -1;
           double val = double(acc[i]);
-          if (j == 0) {
+          if (k >= KA) {
+            idx = -1;  // padding
+          } else if (j == 0) {
             idx = ra * M + ra;
           } else {
             const int d = (j + 1) / 2;
@@ -1161,7 +1191,8 @@ __global__ void __launch_bounds__(NTHR, 1) big_fit_kernel(FitParams p, BigLayout
 #undef FFCA_BTIC
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(sc->tmem));
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(sc->tmem), "n"(TMCOLS));
   if constexpr (CL) {  // no CTA exits while others may read its shared memory
     cluster_arrive();
     cluster_wait();

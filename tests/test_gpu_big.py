@@ -1,7 +1,8 @@
 """GPU parity of the large-bin fit kernel (csrc/fit_big.cuh: M = 8, N = 12,
-BASELINE config 3's channel/source counts) against the fp64 oracle, through
-the C-ABI.  Frame counts are chosen so the bin runs on one CTA and on 2-7 CTA
-clusters (fp32: 2688 frames per CTA, fp64: 1152).
+BASELINE config 3's channel/source counts, and M = 4, N = 6, config 2's, in
+fp32) against the fp64 oracle, through the C-ABI.  Frame counts are chosen so
+the bin runs on one CTA and on clusters (M = 8: 4096 frames per CTA in fp32,
+1792 in fp64; M = 4: 2048).
 
 Tolerances (BASELINE.json north_star): fp32 NLL 1e-5 relative per iteration
 and separated STFTs 1e-3 relative L2; fp64 check mode 1e-10 for both.
@@ -20,8 +21,8 @@ NLL_TOL = {"fp32": 1e-5, "fp64": 1e-10}
 SEP_TOL = {"fp32": 1e-3, "fp64": 1e-10}
 
 
-def make_case(F, T, seed, sigma_v=2.0):
-    cfg = synth.small(8, 12, F, T, seed=seed, sigma_v=sigma_v)
+def make_case(F, T, seed, sigma_v=2.0, M=8, N=12, kind="jd"):
+    cfg = synth.small(M, N, F, T, seed=seed, sigma_v=sigma_v, kind=kind)
     x = synth.mixture(cfg).astype(np.complex128)
     W, L, H = synth.init_params(cfg)
     return x, W, L, H
@@ -113,3 +114,54 @@ def test_big_ip_restart_matches_oracle(gpu, precision):
     for f in range(2):
         assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= tol, f
         assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= tol, f
+
+
+# ---- M = 4, N = 6 (BASELINE config 2's shape): the same kernel with 256
+# threads x 8 frame slots per CTA, three CTAs per SM.  T = 700 and 2000 run on
+# one CTA (T = 700 with empty frame slots skipped), 5000 on a 3-CTA cluster.
+@pytest.mark.parametrize("kind", ["jd", "fullrank"])
+@pytest.mark.parametrize("T", [700, 2000, 5000])
+def test_big_m4_fit_trace_and_separation(gpu, T, kind):
+    iters = 8
+    x, W, L, H = make_case(3, T, seed=T + 1, sigma_v=1.5, M=4, N=6, kind=kind)
+    r = fit(x, W, L, H, iters, "fp32")
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, iters)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL["fp32"], (rel.max(), int(rel.argmax()))
+    assert (r.bin_status == 0).all()
+    img_g = api.fastfca_separate(api.Spectrogram(x), r.params, precision="fp32")
+    img_o = oracle.separate(x, Wo, Lo, Ho)
+    for n in range(6):
+        assert rel_l2(img_g[n].f, img_o[n]) <= SEP_TOL["fp32"], n
+
+
+def test_big_m4_options_and_silent_bin(gpu, monkeypatch):
+    x, W, L, H = make_case(3, 2000, seed=31, sigma_v=1.5, M=4, N=6, kind="fullrank")
+    x[1] = 0.0  # a silent bin keeps its init (fastfca.cpp:165-170)
+    r = fit(x, W, L, H, 5, "fp32", normalize_scales=False)
+    _, _, _, nll_o, _, _ = oracle.fit(x, W, L, H, 5, normalize_scales=False)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL["fp32"]
+    assert np.array_equal(r.params.act[1], H[1]) and np.array_equal(r.params.decorr[1], W[1])
+    r2 = fit(x, W, L, H, 5, "fp32", record_trace=False, normalize_scales=False)
+    assert len(r2.nll) == 0
+    for a, b in zip(r2.params.act, r.params.act):
+        assert np.array_equal(a, b)
+    # the round-1 kernel (FFCA_NO_BIG) runs the same algorithm
+    r_big = fit(x, W, L, H, 6, "fp32")
+    monkeypatch.setenv("FFCA_NO_BIG", "1")
+    r_old = fit(x, W, L, H, 6, "fp32")
+    a, b = np.asarray(r_big.nll), np.asarray(r_old.nll)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
+
+
+def test_big_m4_ip_restart_matches_oracle(gpu):
+    x, W, L, H = make_case(2, 2000, seed=37, sigma_v=1.5, M=4, N=6)
+    W = W.copy()
+    W[1, :, 0] = 0.0
+    r = fit(x, W, L, H, 3, "fp32", record_trace=False, seed=7)
+    Wo, Lo, Ho, _, _, _ = oracle.fit(x, W, L, H, 3, record_trace=False, seed=7)
+    assert (r.bin_status == 0).all()
+    for f in range(2):
+        assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= 2e-3, f
+        assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= 2e-3, f
