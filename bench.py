@@ -239,6 +239,9 @@ def main() -> None:
     ap.add_argument("--config", default=os.environ.get("FFCA_BENCH_CONFIG", "c3"))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-separate", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: harness test on fewer GPUs than ranks (ranks share devices; the "
+                         "slot all-gather runs on host tensors)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -258,11 +261,16 @@ def main() -> None:
         return
 
     import torch
+    if args.dist_backend == "gloo":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2101_08563_b200 import _lib
 
     cfg, scaling = workload(cfg0, world, args.scaling)
@@ -272,6 +280,7 @@ def main() -> None:
     M, N, T, iters = cfg.M, cfg.N, cfg.T, cfg.iters
     x, W0, L0, H0 = build_inputs(cfg, lo, hi)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collectives' tensors
     fp64 = args.precision == "fp64"
     cdt = torch.complex128 if fp64 else torch.complex64
     rdt = torch.float64 if fp64 else torch.float32
@@ -329,7 +338,7 @@ def main() -> None:
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
     if dist:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     units = P * T * iters * args.steps
@@ -338,9 +347,9 @@ def main() -> None:
     # Trace assembly: all-gather the per-bin slots (NCCL), bin-order sums.
     st = status.cpu().numpy()
     bad = int((st >= 2).sum())
-    all_slots = gather_slots(slots, P, world, rank, dist)
+    all_slots = gather_slots(slots.to(cdev), P, world, rank, dist)
     if dist:
-        badt = torch.tensor([bad], device=dev)
+        badt = torch.tensor([bad], device=cdev)
         dist.all_reduce(badt)
         bad = int(badt.item())
     trace = bin_order_trace(all_slots, cfg.batch, cfg.F)  # [iters+1, batch]
@@ -367,26 +376,28 @@ def main() -> None:
                  "note": "record_trace=false (no per-iteration NLL), median of 10, this rank"}
 
     # Separation (fastfca_separate) of the fitted parameters, device path.
-    img = torch.empty((N, Pl, T, M), dtype=cdt, device=dev)
-    sep_ms = []
-    for i in range(3 + 5):
-        flush.fill_(i & 0xff)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        _lib.check(L_.ffca_separate_device(ctx.handle, Pl, M, N, T, prec, _lib.ptr(x_d),
-                                           _lib.ptr(W_d), _lib.ptr(L_d), _lib.ptr(H_d),
-                                           _lib.ptr(img), sp))
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if i >= 3:
-            sep_ms.append(e0.elapsed_time(e1))
-    sep_s = statistics.median(sep_ms) / 1e3
-    esz = 16 if fp64 else 8
-    sep_bytes = Pl * T * (esz * M + (esz // 2) * N + esz * N * M)
-    separate = {"ms": sep_s * 1e3, "bytes": int(sep_bytes), "GB_per_s": sep_bytes / sep_s / 1e9,
-                "frac_hbm": sep_bytes / sep_s / 1e9 / peaks()["hbm_gbs"],
-                "bytes_per_frame": "x read + H read + N images written"}
-    del img
+    separate = None
+    if not args.no_separate:
+        img = torch.empty((N, Pl, T, M), dtype=cdt, device=dev)
+        sep_ms = []
+        for i in range(3 + 5):
+            flush.fill_(i & 0xff)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _lib.check(L_.ffca_separate_device(ctx.handle, Pl, M, N, T, prec, _lib.ptr(x_d),
+                                               _lib.ptr(W_d), _lib.ptr(L_d), _lib.ptr(H_d),
+                                               _lib.ptr(img), sp))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                sep_ms.append(e0.elapsed_time(e1))
+        sep_s = statistics.median(sep_ms) / 1e3
+        esz = 16 if fp64 else 8
+        sep_bytes = Pl * T * (esz * M + (esz // 2) * N + esz * N * M)
+        separate = {"ms": sep_s * 1e3, "bytes": int(sep_bytes), "GB_per_s": sep_bytes / sep_s / 1e9,
+                    "frac_hbm": sep_bytes / sep_s / 1e9 / peaks()["hbm_gbs"],
+                    "bytes_per_frame": "x read + H read + N images written"}
+        del img
 
     # e2e through the reference-facing C-ABI with pinned host buffers.
     e2e = None
@@ -413,7 +424,7 @@ def main() -> None:
                 times.append(t1 - t0)
         et = sum(times)
         if dist:
-            t = torch.tensor([et], dtype=torch.float64, device=dev)
+            t = torch.tensor([et], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
         # whole-job bytes per step (all ranks' shards)

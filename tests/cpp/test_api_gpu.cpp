@@ -10,6 +10,7 @@
 #include <tuple>
 
 #include "fastfca/fastfca.hpp"
+#include "ffca.h"
 #include "oracle.hpp"
 
 namespace {
@@ -158,7 +159,9 @@ int main() {
   {
     const auto init = random_params(3, 4, 120, 3, rng);
     fastfca::GpuOptions one, two;
-    two.devices = {0, 0};
+    // two distinct GPUs when the node has them, else two contexts on device 0
+    two.devices = ffca_device_count() >= 2 ? std::vector<int>{0, 1} : std::vector<int>{0, 0};
+    std::printf("frequency sharding over devices {%d, %d}\n", two.devices[0], two.devices[1]);
     const auto a = fastfca::fastfca_fit(covs, init, fastfca::LhFlavor::em, 20, {}, {}, one);
     const auto b = fastfca::fastfca_fit(covs, init, fastfca::LhFlavor::em, 20, {}, {}, two);
     CHECK(a.nll == b.nll);
