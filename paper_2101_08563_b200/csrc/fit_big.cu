@@ -23,6 +23,18 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
   if (lay.total > dev_max) return FFCA_OK;
   *handled = true;
   if (fp.nprob == 0) return FFCA_OK;
+  if (big_incr<M, R, SLOTS>()) {
+    // U scratch [problem][T][M] (fit_big.cuh INCR): one allocation for the
+    // whole call, this launch's rows at work_first (concurrent chunks of the
+    // pipelined host fit must not share rows or regrow the buffer).
+    cudaError_t err;
+    const size_t per = size_t(fp.T) * M * sizeof(R);
+    const size_t nall = size_t(fp.work_total > 0 ? fp.work_total : fp.nprob);
+    char* base = static_cast<char*>(ctx->get(kU, nall * per, &err));
+    if (!base)
+      return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: U scratch alloc: ") + cudaGetErrorString(err));
+    fp.work = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
+  }
   if (C == 1) {
     auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
@@ -69,6 +81,12 @@ int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp
   // fit_kernel (one resident CTA in shared memory is cheaper there).
   if (M == 4 && fp.N == 6 && !fp64 && fp.T > 512)
     return launch_big_t<4, 6, float, 8, 256, 1, 3>(ctx, fp, st, handled);
+  // BASELINE config 4 (M = 3, N = 4, T = 626): 96 threads x 7 frame slots hold
+  // a 672-frame bin; 11 KB of H planes and 64 tensor-memory columns per bin,
+  // eight bins per SM, so the per-bin serial sections (N + 1 reductions, the
+  // IP, the balance) of one bin overlap the frame passes of seven others.
+  if (M == 3 && fp.N == 4 && !fp64 && fp.T > 192 && fp.T <= 672 && !getenv("FFCA_NO_BIG3"))
+    return launch_big_t<3, 4, float, 7, 96, 1, 8>(ctx, fp, st, handled);
   return FFCA_OK;
 }
 

@@ -61,12 +61,19 @@
 #include "ip_fast.cuh"
 #include "serial_math.cuh"
 
+#ifndef FFCA_BIG_INCR
+#define FFCA_BIG_INCR 1  // incremental mixture variances in the fp32 EM sweeps
+#endif
+#ifndef FFCA_BIG_FS
+#define FFCA_BIG_FS 2  // frame slots per trip of the incremental EM sweep (4: spills at M = 8)
+#endif
+
 namespace ffca {
 
 // Shared-memory carve-up of a big-bin CTA (byte offsets), computed on the host.
 struct BigLayout {
   int off_h, ps;  // H planes: ps 16-byte vectors per plane
-  int off_le, off_ld, off_hsc, off_hinv, off_linv, off_us, off_wsc, off_hsum, off_psum;
+  int off_le, off_ld, off_hsc, off_hinv, off_linv, off_lprev, off_us, off_wsc, off_hsum, off_psum;
   int off_wd, off_wr, off_ipscr, off_ldscr, off_red, off_cx, off_scal;
   int off_scr;                                    // reused scratch region:
   int off_gscr, off_ex, off_q, off_ipf, off_rng;  //   covariance tree, then the rest
@@ -77,6 +84,12 @@ struct BigLayout {
 template <typename R> struct Vec16;
 template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+
+// Incremental mixture variances in the fp32 EM sweeps (see big_fit_kernel).
+template <int M, typename R, int SLOTS>
+constexpr bool big_incr() {
+  return FFCA_BIG_INCR != 0 && sizeof(R) == 4 && SLOTS % FFCA_BIG_FS == 0 && M == 8;
+}
 
 constexpr int pow2_at_least(int n) {
   int p = 1;
@@ -92,14 +105,16 @@ struct BigCfg {
   static constexpr int TCAP = NTHR * SLOTS;        // frames per CTA
   static constexpr int D = M / 2;                  // cyclic product distances
   static constexpr int NP = 1 + 2 * D;             // reals per covariance lane
+  static constexpr int ML = pow2_at_least(M);      // lanes per frame in the M-lane passes
+  static constexpr int LES = ((M + VE - 1) / VE) * VE;  // stride of an effective-loading column
   static constexpr int MW = M / MS;                // weights per covariance lane
   static constexpr int KA = NP * MW;               // accumulators per covariance lane
-  static constexpr int GS = M * MS;                // covariance lanes per frame
+  static constexpr int GS = ML * MS;               // covariance lanes per frame (lanes >= M idle)
   static constexpr int KAP = ((KA + 32 / GS - 1) / (32 / GS)) * (32 / GS);  // padded so that the
                                                    // in-warp reduce-scatter halves evenly
   static constexpr int KRED = 2 * M + 1;           // EM sweep partials
   static constexpr int KQ = M * M * M;             // covariance totals
-  static constexpr int WPR = M * int(sizeof(R)) / 4;  // TMEM columns per record
+  static constexpr int WPR = pow2_at_least(M) * int(sizeof(R)) / 4;  // TMEM columns per record
   static constexpr int SCOL = 2 * WPR;             // columns per slot (U, Phi)
   static constexpr int WGROUPS = (NW + 3) / 4;     // warps sharing a TMEM lane quarter
   static constexpr int PW = pow2_at_least(NW);
@@ -111,7 +126,7 @@ struct BigCfg {
     while (c < SLOTS * SCOL * WGROUPS) c <<= 1;
     return c;
   }();
-  static_assert(32 % GS == 0 && 32 % M == 0, "lanes per frame must divide a warp");
+  static_assert(32 % GS == 0 && M % MS == 0, "lanes per frame must divide a warp");
   static_assert(NTHR % 32 == 0, "whole warps");
   static_assert(SLOTS * SCOL * WGROUPS <= 512, "tensor memory columns");
   static_assert(WPR == 4 || WPR == 8 || WPR == 16, "record width");
@@ -125,11 +140,12 @@ struct BigCfg {
     int o = 0;
     L.off_h = o; o = al(o + NHP * L.ps * 16);
     const int rs = int(sizeof(R));
-    L.off_le = o; o = al(o + N * M * rs);
+    L.off_le = o; o = al(o + N * LES * rs);
     L.off_ld = o; o = al(o + 2 * M * N * rs);
     L.off_hsc = o; o = al(o + 2 * N * rs);
     L.off_hinv = o; o = al(o + 2 * N * rs);
     L.off_linv = o; o = al(o + M * rs);
+    L.off_lprev = o; o = al(o + M * rs);
     L.off_us = o; o = al(o + M * rs);
     L.off_wsc = o; o = al(o + M * rs);
     L.off_hsum = o; o = al(o + N * rs);
@@ -255,7 +271,7 @@ __device__ __forceinline__ void words_to(const unsigned* w, R (&v)[M]) {
 // One record of M values in the compute type.
 template <int M, typename R>
 __device__ __forceinline__ void tm_load_rec(unsigned a, R (&v)[M]) {
-  constexpr int NWD = M * int(sizeof(R)) / 4;
+  constexpr int NWD = pow2_at_least(M) * int(sizeof(R)) / 4;
   unsigned w[NWD];
   tm_ld<NWD>(a, w);
   tm_wait_ld();
@@ -264,7 +280,7 @@ __device__ __forceinline__ void tm_load_rec(unsigned a, R (&v)[M]) {
 // Two adjacent records (U then Phi) in one transfer when they fit 16 words.
 template <int M, typename R>
 __device__ __forceinline__ void tm_load_rec2(unsigned a, R (&u)[M], R (&ph)[M]) {
-  constexpr int NWD = M * int(sizeof(R)) / 4;
+  constexpr int NWD = pow2_at_least(M) * int(sizeof(R)) / 4;
   if constexpr (2 * NWD <= 16) {
     unsigned w[2 * NWD];
     tm_ld<2 * NWD>(a, w);
@@ -278,8 +294,10 @@ __device__ __forceinline__ void tm_load_rec2(unsigned a, R (&u)[M], R (&ph)[M]) 
 }
 template <int M, typename R>
 __device__ __forceinline__ void tm_store_rec(unsigned a, const R (&v)[M]) {
-  constexpr int NWD = M * int(sizeof(R)) / 4;
+  constexpr int NWD = pow2_at_least(M) * int(sizeof(R)) / 4;
   unsigned w[NWD];
+#pragma unroll
+  for (int k = M * int(sizeof(R)) / 4; k < NWD; ++k) w[k] = 0u;  // record padding (odd M)
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     if constexpr (sizeof(R) == 4) {
@@ -290,6 +308,16 @@ __device__ __forceinline__ void tm_store_rec(unsigned a, const R (&v)[M]) {
     }
   }
   tm_st<NWD>(a, w);
+}
+
+// Two adjacent records in one transfer (fp32, 2 M <= 16 words).
+template <int M>
+__device__ __forceinline__ void tm_store_rec2(unsigned a, const float (&v0)[M], const float (&v1)[M]) {
+  static_assert(2 * M <= 16 && (M == 4 || M == 8), "two fp32 records per store");
+  unsigned w[2 * M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) w[m] = __float_as_uint(v0[m]), w[M + m] = __float_as_uint(v1[m]);
+  tm_st<2 * M>(a, w);
 }
 
 // Packed fp32 pairs (FFMA2 / FMUL2 on sm_100): the frame loops are issue
@@ -310,7 +338,16 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   constexpr int VE = Cfg::VE, NHP = Cfg::NHP, NW = Cfg::NW, PW = Cfg::PW, HW = Cfg::HW;
   constexpr int D = Cfg::D, NP = Cfg::NP, MW = Cfg::MW, KA = Cfg::KA, GS = Cfg::GS;
   constexpr int KRED = Cfg::KRED, KQ = Cfg::KQ, WPR = Cfg::WPR, SCOL = Cfg::SCOL, CNT = Cfg::CNT;
-  constexpr int KAP = Cfg::KAP, TMCOLS = Cfg::TMCOLS;
+  constexpr int KAP = Cfg::KAP, TMCOLS = Cfg::TMCOLS, ML = Cfg::ML, LES = Cfg::LES;
+  // fp32 path: the mixture variances sigma^2 = eps + L H live in tensor memory
+  // (where U used to be) and follow each EM sweep's row update incrementally
+  // (sigma^2 += L_new h_new - L_old h_old, 4M flops instead of the 2MN of a
+  // fresh sum); the variance pass A1 rebuilds them exactly every iteration.
+  // U, read-only during the sweeps, moves to an L2-resident global scratch.
+  // Measured: c3 (M = 8, N = 12) 97.0 -> 94.5 ms; at M = 4, N = 6 the fresh
+  // sum is only 12 packed FMAs per frame and the extra L2 reads cost more
+  // than they save (c2 4.54 -> 4.60 ms), so it stays on the exact path.
+  constexpr bool INCR = big_incr<M, R, SLOTS>();
   using B = R;
   using BM = SMath<B>;
   namespace cg = cooperative_groups;
@@ -334,7 +371,8 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   const int ps = lay.ps;
   // Frame slots in use: short bins skip the empty ones (an even count, the
   // fp32 EM sweep takes two slots per trip).
-  const int nsl = min(SLOTS, (((Tl + NTHR - 1) / NTHR) + 1) & ~1);
+  constexpr int SLQ = big_incr<M, R, SLOTS>() ? FFCA_BIG_FS : 2;
+  const int nsl = min(SLOTS, (((Tl + NTHR - 1) / NTHR) + SLQ - 1) / SLQ * SLQ);
   // Phase timing (diagnostics build, -DFFCA_PHASE_TIMING): thread 0 of each
   // CTA accumulates clock64 deltas; CTA rank 0 reports them per bin.
   // 0 U pass, 1 EM frames, 2 EM reduce/update, 3 balance, 4 A1, 5 A2 frames,
@@ -358,11 +396,12 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
 
   V* Hp = reinterpret_cast<V*>(smem + lay.off_h);
   R* Hs = reinterpret_cast<R*>(Hp);
-  R* Le = reinterpret_cast<R*>(smem + lay.off_le);  // [N][M]: column n at Le + n M
+  R* Le = reinterpret_cast<R*>(smem + lay.off_le);  // [N][LES]: column n at Le + n LES
   B* const Ld0 = reinterpret_cast<B*>(smem + lay.off_ld);
   B* const hsc0 = reinterpret_cast<B*>(smem + lay.off_hsc);
   B* const hinv0 = reinterpret_cast<B*>(smem + lay.off_hinv);
   R* Linv = reinterpret_cast<R*>(smem + lay.off_linv);
+  R* Lprev = reinterpret_cast<R*>(smem + lay.off_lprev);  // effective column n before its update
   B* us = reinterpret_cast<B*>(smem + lay.off_us);
   B* wsc = reinterpret_cast<B*>(smem + lay.off_wsc);
   B* hsumv = reinterpret_cast<B*>(smem + lay.off_hsum);
@@ -386,6 +425,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
 
   const C* xg = reinterpret_cast<const C*>(p.x) + (size_t(b) * T + t0g) * M;
   R* Hg = reinterpret_cast<R*>(p.H) + (size_t(b) * T + t0g) * N;
+  R* Ug = reinterpret_cast<R*>(p.work) + (size_t(b) * T + t0g) * M;  // INCR only
 
   // ---- tensor memory: TMCOLS columns (all 512 for the one-CTA-per-SM shapes).
   if (warp == 0) {
@@ -406,7 +446,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   for (int k = tid; k < M * N; k += NTHR) {
     const double l = p.L[size_t(b) * M * N + k];
     Ld[k] = narrow_pos<B>(l);
-    Le[k] = narrow_pos<R>(l);  // col-major m + n M == [n][m]
+    Le[(k % M) + (k / M) * LES] = narrow_pos<R>(l);  // [n][m], column stride LES
   }
   for (int k = tid; k < N; k += NTHR) hsc[k] = B(1), hinv[k] = B(1);
   for (int k = tid; k < M; k += NTHR) us[k] = B(1), wsc[k] = B(1);
@@ -450,23 +490,26 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   // re-read per frame from the broadcast bank instead of being hoisted into
   // 12 x M registers the frame loops cannot afford.
   auto load_le = [&](int k, R (&l)[M]) {
-    const unsigned a = unsigned(__cvta_generic_to_shared(Le + k * M));
+    const unsigned a = unsigned(__cvta_generic_to_shared(Le + k * LES));
+    R v[LES];
 #pragma unroll
-    for (int q = 0; q < M / VE; ++q) {
+    for (int q = 0; q < LES / VE; ++q) {
       if constexpr (VE == 4) {
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(l[q * 4]), "=f"(l[q * 4 + 1]), "=f"(l[q * 4 + 2]), "=f"(l[q * 4 + 3])
+                     : "=f"(v[q * 4]), "=f"(v[q * 4 + 1]), "=f"(v[q * 4 + 2]), "=f"(v[q * 4 + 3])
                      : "r"(a + 16 * q));
       } else {
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
-                     : "=d"(l[q * 2]), "=d"(l[q * 2 + 1])
+                     : "=d"(v[q * 2]), "=d"(v[q * 2 + 1])
                      : "r"(a + 16 * q));
       }
     }
+#pragma unroll
+    for (int m = 0; m < M; ++m) l[m] = v[m];
   };
   // Mixture variances sigma^2(m) = eps + sum_k Le(m,k) h_k.
   auto mix_var = [&](const R (&h)[NHP * VE], R (&lh)[M]) {
-    if constexpr (sizeof(R) == 4) {
+    if constexpr (sizeof(R) == 4 && M % 2 == 0) {
       float2 a[M / 2];
 #pragma unroll
       for (int q = 0; q < M / 2; ++q) a[q] = f2(eps, eps);
@@ -497,7 +540,31 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   // U(j, t) = |w_j^H x_t|^2: M lanes per frame, lane j owns column j of W;
   // the frame's owner lane gathers its M values and stores them to TMEM.
   auto u_pass = [&]() {
-    if constexpr (sizeof(R) == 4) {
+    if constexpr (sizeof(R) == 4 && M % 2 != 0) {
+      // fp32, odd M: one thread per frame, 8-byte loads, scalar complex algebra.
+#pragma unroll 1
+      for (int s = 0; s < nsl; ++s) {
+        const int t0 = frame_of(s, lane);
+        const int t = t0 < Tl ? t0 : 0;
+        C xc[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) xc[c] = __ldg(xg + size_t(t) * M + c);
+        R uo[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          R yr = R(0), yi = R(0);
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const C w = Wr[c + m * M];  // y_m = sum_c conj(W(c, m)) x_c
+            yr += w.x * xc[c].x + w.y * xc[c].y;
+            yi += w.x * xc[c].y - w.y * xc[c].x;
+          }
+          uo[m] = yr * yr + yi * yi;
+        }
+        tm_store_rec<M, R>(tm_u(s), uo);
+      }
+      tm_wait_st();
+    } else if constexpr (sizeof(R) == 4) {
       // fp32: one thread per frame (the owner loads its record, coalesced),
       // W columns from broadcast shared loads, packed FFMA2:
       // y_m = sum_c conj(W(c,m)) x_c = sum_c Re W(c,m) x_c + i sum_c Im W(c,m) (Im x_c, -Re x_c),
@@ -515,8 +582,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
           xc[2 * q + 1] = f2(v.z, v.w);
         }
         const unsigned ta = tm_u(s);
-#pragma unroll 2
-        for (int m = 0; m < M; ++m) {
+        auto u_of = [&](int m) -> float {
           float wc[2 * M];  // column m of W: (re, im) pairs
           const unsigned a = unsigned(__cvta_generic_to_shared(Wr + m * M));
 #pragma unroll
@@ -531,10 +597,24 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
             y2 = fma2s(xc[c], wc[2 * c + 1], y2);
           }
           const float yr = y1.x + y2.y, yi = y1.y - y2.x;
-          const float u = yr * yr + yi * yi;
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(ta + unsigned(m)),
-                       "r"(__float_as_uint(u))
-                       : "memory");
+          return yr * yr + yi * yi;
+        };
+        if constexpr (INCR) {
+          // U to the global scratch, four channels per 16-byte store.
+          float4* uw = reinterpret_cast<float4*>(Ug + size_t(t) * M);
+#pragma unroll 1
+          for (int q = 0; q < M / 4; ++q) {
+            const float4 v = make_float4(u_of(4 * q), u_of(4 * q + 1), u_of(4 * q + 2), u_of(4 * q + 3));
+            if (t0 < Tl) uw[q] = v;
+          }
+        } else {
+#pragma unroll 2
+          for (int m = 0; m < M; ++m) {
+            const float u = u_of(m);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(ta + unsigned(m)),
+                         "r"(__float_as_uint(u))
+                         : "memory");
+          }
         }
       }
       tm_wait_st();
@@ -611,7 +691,96 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
     R acc[KRED];
 #pragma unroll
     for (int k = 0; k < KRED; ++k) acc[k] = R(0);
-    if constexpr (sizeof(R) == 4 && SLOTS % 2 == 0 && M % 2 == 0) {
+    if constexpr (INCR) {
+      // fp32, incremental variances: sigma^2 (tensor memory) takes the row
+      // n-1 update as sigma^2 += L_new h_new - L_old h_old before it is used;
+      // U comes from the global scratch.  Two frame slots per trip.
+      constexpr int MP = M / 2;
+      float2 lc2[MP], li2[MP], ln2[MP], lo2[MP];
+      {
+        R lnw[M];
+        load_le(n > 0 ? n - 1 : 0, lnw);  // column n-1 after its update
+#pragma unroll
+        for (int q = 0; q < MP; ++q) {
+          lc2[q] = f2(lc[2 * q], lc[2 * q + 1]);
+          li2[q] = f2(linv[2 * q], linv[2 * q + 1]);
+          ln2[q] = f2(lnw[2 * q], lnw[2 * q + 1]);
+          lo2[q] = n > 0 ? f2(Lprev[2 * q], Lprev[2 * q + 1]) : f2(0.f, 0.f);
+        }
+      }
+      float2 a2[MP], p2[MP];
+#pragma unroll
+      for (int q = 0; q < MP; ++q) a2[q] = f2(0.f, 0.f), p2[q] = f2(0.f, 0.f);
+      float hacc = 0.f;
+      // FS frame slots per trip: independent dependency chains (tensor-memory
+      // and L2 loads, reciprocals, stores) in flight per warp.
+      constexpr int FS = FFCA_BIG_FS;
+      static_assert(SLOTS % FS == 0, "frame slots per trip");
+#pragma unroll 1
+      for (int s = 0; s < nsl; s += FS) {
+        int t[FS];
+        bool ok[FS];
+        float2 u[FS][MP], lh[FS][MP];
+#pragma unroll
+        for (int f = 0; f < FS; ++f) {
+          const int t0 = frame_of(s + f, lane);
+          ok[f] = t0 < Tl;
+          t[f] = ok[f] ? t0 : 0;
+          const float4* uw = reinterpret_cast<const float4*>(Ug + size_t(t[f]) * M);
+#pragma unroll
+          for (int q = 0; q < M / 4; ++q) {
+            const float4 v = __ldcg(uw + q);
+            u[f][2 * q] = f2(v.x, v.y), u[f][2 * q + 1] = f2(v.z, v.w);
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < FS; ++f) {
+          float sg[M], pp[M];
+          tm_load_rec2<M, R>(tm_u(s + f), sg, pp);
+#pragma unroll
+          for (int q = 0; q < MP; ++q) lh[f][q] = f2(sg[2 * q], sg[2 * q + 1]);
+          if (n > 0) {  // H row n-1 (fastfca.cpp:95-97), then its change in sigma^2
+            float2 s2 = fmul2(f2(pp[0], pp[1]), li2[0]);
+#pragma unroll
+            for (int q = 1; q < MP; ++q) s2 = fma2(f2(pp[2 * q], pp[2 * q + 1]), li2[q], s2);
+            float hn1 = (s2.x + s2.y) * (1.f / M);
+            hn1 = hn1 > tiny<R>() ? hn1 : tiny<R>();
+            const float hold = Hs[hidx(n - 1, t[f])];
+            if (ok[f]) Hs[hidx(n - 1, t[f])] = hn1;
+            hacc += ok[f] ? hn1 : 0.f;
+#pragma unroll
+            for (int q = 0; q < MP; ++q)
+              lh[f][q] = fma2s(ln2[q], hn1, fma2s(lo2[q], -hold, lh[f][q]));
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < FS; ++f) {
+          const float hn = Hs[hidx(n, t[f])];
+          const float ihn = ok[f] ? rcp_fast(hn) : 0.f;
+          const float okf = ok[f] ? 1.f : 0.f;
+          float v[M], sg[M];
+#pragma unroll
+          for (int q = 0; q < MP; ++q) {
+            const float2 ln = fmul2s(lc2[q], hn);                      // L_n H_n
+            const float2 rl = f2(rcp_fast(lh[f][q].x), rcp_fast(lh[f][q].y));
+            const float2 gg = fmul2(ln, rl);                           // G
+            const float2 w = fma2(gg, u[f][q], fneg2(ln));             // G U - L_n H_n
+            const float2 vv = fma2(gg, w, ln);                         // G^2 U + (1 - G) L_n H_n
+            v[2 * q] = vv.x, v[2 * q + 1] = vv.y;
+            sg[2 * q] = lh[f][q].x, sg[2 * q + 1] = lh[f][q].y;
+            a2[q] = fma2s(vv, ihn, a2[q]);
+            if (phis) p2[q] = fma2s(vv, okf, p2[q]);
+          }
+          tm_store_rec2<M>(tm_u(s + f), sg, v);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MP; ++q) {
+        acc[2 * q] = a2[q].x, acc[2 * q + 1] = a2[q].y;
+        acc[M + 1 + 2 * q] = p2[q].x, acc[M + 2 + 2 * q] = p2[q].y;
+      }
+      acc[M] = hacc;
+    } else if constexpr (sizeof(R) == 4 && SLOTS % 2 == 0 && M % 2 == 0) {
       // fp32: two frame slots per trip share the loading-column loads, and
       // the per-channel algebra runs on packed pairs (FFMA2 / FMUL2).  A slot
       // past the CTA's frames computes on frame 0; its H store is skipped and
@@ -778,6 +947,14 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
       const int t = ok ? t0 : 0;
       R u[M], php[M];
       tm_load_rec2<M, R>(tm_u(s), u, php);
+      if constexpr (INCR) {  // the U slot holds sigma^2: U comes from the global scratch
+        const float4* uw = reinterpret_cast<const float4*>(Ug + size_t(t) * M);
+#pragma unroll
+        for (int q = 0; q < M / 4; ++q) {
+          const float4 v = __ldcg(uw + q);
+          u[4 * q] = v.x, u[4 * q + 1] = v.y, u[4 * q + 2] = v.z, u[4 * q + 3] = v.w;
+        }
+      }
       if (finish) {
         R sum = php[0] * linv[0];
 #pragma unroll
@@ -798,7 +975,13 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
         lsum += flog2_ftz(lh[m]);
       }
       nacc[M] += ok ? lsum : R(0);
-      tm_store_rec<M, R>(tm_u(s), r);
+      if constexpr (INCR) {
+        // exact sigma^2 for the next iteration's sweeps, 1/sigma^2 (the
+        // covariance weights) over the spent posterior
+        tm_store_rec2<M>(tm_u(s), lh, r);
+      } else {
+        tm_store_rec<M, R>(tm_u(s), r);
+      }
     }
     tm_wait_st();
   };
@@ -811,18 +994,19 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   // layout the IP reads) and nll_tot.
   auto a2_pass = [&](bool want_q, const R (&nacc)[M + 1], double (&nll_tot)[M + 1]) {
     constexpr int FPB = 32 / GS;  // frames per batch
-    const int a = lane % M, mh = (lane / M) % MS, g = lane / GS;
+    const int a = lane % ML, mh = (lane / ML) % MS, g = lane / GS;
+    const bool live = a < M;  // odd M: the padding lane of each frame group idles
     R acc[KAP];  // [jj * MW + mm], zero padding up to KAP
 #pragma unroll
     for (int k = 0; k < KAP; ++k) acc[k] = R(0);
     int coff[D + 1];
 #pragma unroll
-    for (int d = 0; d <= D; ++d) coff[d] = (a + d) % M;
+    for (int d = 0; d <= D; ++d) coff[d] = live ? (a + d) % M : 0;
     if (want_q) {
 #pragma unroll 1
       for (int s = 0; s < nsl; ++s) {
         R ro[M];  // this lane's own frame weights 1/sigma^2
-        tm_load_rec<M, R>(tm_u(s), ro);
+        tm_load_rec<M, R>(INCR ? tm_phi(s) : tm_u(s), ro);
 #pragma unroll 2
         for (int bb = 0; bb < 32 / FPB; ++bb) {
           const int owner = bb * FPB + g;
@@ -851,7 +1035,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
               const R r1 = __shfl_sync(0xffffffffu, ro[MW + mm], owner);
               rm = mh == 0 ? r0 : r1;
             }
-            rw[mm] = ok ? rm : R(0);
+            rw[mm] = (ok && live) ? rm : R(0);
           }
           if constexpr (sizeof(R) == 4 && MW % 2 == 0) {
             // acc pairs (jj, mm), (jj, mm + 1): weights packed, product broadcast
@@ -918,7 +1102,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
     // (a < c: Re at a*M+c, Im at c*M+a; diagonal at a*M+a), then the NLL.
     if (warp == 0) {
       if (want_q) {
-        const int ra = lane % M, rmh = (lane / M) % MS;
+        const int ra = lane % ML, rmh = (lane / ML) % MS;
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
           const int k = base + i;
@@ -926,7 +1110,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
           const int m = rmh * MW + mm;
           int idx = -1;
           double val = double(acc[i]);
-          if (k >= KA) {
+          if (k >= KA || ra >= M) {
             idx = -1;  // padding
           } else if (j == 0) {
             idx = ra * M + ra;
@@ -1023,7 +1207,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
       l = (l0 > B(0) && !(l > B(0))) ? tiny<B>() : l;
       Ldn[k] = l;
       const B le = l * hscn[n];
-      Le[k] = R((l > B(0) && !(le > B(0))) ? tiny<B>() : le);
+      Le[m + n * LES] = R((l > B(0) && !(le > B(0))) ? tiny<B>() : le);
     }
     __syncwarp();
 #pragma unroll
@@ -1118,6 +1302,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
       auto em_step = [&](int n) {
         const bool phis = bal && n == N - 1;
         R* rd = red + (n & 1) * NW * KRED;
+        const R lold = lane < M ? Le[lane + n * LES] : R(0);  // effective column n before its update
         em_sweep(n, phis, rd);
         FFCA_BTIC(1);
         const int K = phis ? KRED : M + 1;
@@ -1129,7 +1314,8 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
           const B l = fmax(B(tot) * B(invT) * hinv[n], tiny<B>());  // fastfca.cpp:92-94
           const R lr = R(l);
           Ld[m + n * M] = l;
-          if (!phis) Le[m + n * M] = lr;
+          if (!phis) Le[m + n * LES] = lr;
+          if constexpr (INCR) Lprev[m] = lold;
           Linv[m] = rcp_fast(lr);
           if (phis) psum[m] = B(pss);
         }

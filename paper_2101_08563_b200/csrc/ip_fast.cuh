@@ -48,23 +48,29 @@ __device__ __forceinline__ cplx_t<SR> shfl_c(cplx_t<SR> v, int src, int width) {
 //   warp  M/SEG     : applies the pending balance column scales to W, saves W,
 //                     V = (W^H)^{-1} and log|det W|^2.
 // The caller synchronises the CTA afterwards.
+// Lane segments are ML = pow2ceil(M) wide; for M not a power of two the
+// systems are padded with identity rows / columns (block-diagonal, so the
+// M x M blocks of the inverses are the inverses of the blocks).
 template <int M, typename SR, typename B>
 __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, const double* qraw,
                              double invT, IpFastScratch<M, SR>* sc) {
   using SC = cplx_t<SR>;
-  static_assert(32 % M == 0, "segments");
-  constexpr int SEG = 32 / M;                  // matrices per warp
+  constexpr int ML = Pow2Ceil<M>::value;
+  static_assert(32 % ML == 0, "segments");
+  constexpr int SEG = 32 / ML;                 // matrices per warp
   constexpr int QW = (M + SEG - 1) / SEG;      // warps inverting Q
-  const int r = lane % M;                      // row of this lane
+  const int r = lane % ML;                     // row of this lane (rows >= M: padding)
   if (warp < QW) {
-    const int m = warp * SEG + lane / M;
+    const int m = warp * SEG + lane / ML;
     const bool act = m < M;
     const double* q = qraw + (act ? m : 0) * M * M;
-    SC row[2 * M];
+    SC row[2 * ML];
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
+    for (int c = 0; c < ML; ++c) {
       SR re, im;
-      if (c == r) {
+      if (r >= M || c >= M) {
+        re = (c == r) ? SR(1) : SR(0), im = SR(0);
+      } else if (c == r) {
         re = SR(q[r * M + r] * invT), im = SR(0);
       } else if (r < c) {
         re = SR(q[r * M + c] * invT), im = SR(q[c * M + r] * invT);
@@ -72,31 +78,31 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
         re = SR(q[c * M + r] * invT), im = SR(-q[r * M + c] * invT);
       }
       row[c] = mkc<SR>(re, im);
-      row[M + c] = mkc<SR>(c == r ? SR(1) : SR(0), SR(0));
+      row[ML + c] = mkc<SR>(c == r ? SR(1) : SR(0), SR(0));
     }
     // Gauss-Jordan without pivoting (Q_m Hermitian positive definite).
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-      SC pk[2 * M];
+      SC pk[2 * ML];
 #pragma unroll
-      for (int c = k; c < 2 * M; ++c) pk[c] = shfl_c<SR>(row[c], k, M);
+      for (int c = k; c < 2 * ML; ++c) pk[c] = shfl_c<SR>(row[c], k, ML);
       const SR pm = cabs2(pk[k]);
       const SR s = SMath<SR>::rcp(pm);
       const SC ipiv = mkc<SR>(pk[k].x * s, -pk[k].y * s);
 #pragma unroll
-      for (int c = k + 1; c < 2 * M; ++c) pk[c] = cmul(pk[c], ipiv);
+      for (int c = k + 1; c < 2 * ML; ++c) pk[c] = cmul(pk[c], ipiv);
       if (r == k) {
 #pragma unroll
-        for (int c = k + 1; c < 2 * M; ++c) row[c] = pk[c];
+        for (int c = k + 1; c < 2 * ML; ++c) row[c] = pk[c];
       } else {
         const SC f = row[k];
 #pragma unroll
-        for (int c = k + 1; c < 2 * M; ++c) row[c] = csub(row[c], cmul(f, pk[c]));
+        for (int c = k + 1; c < 2 * ML; ++c) row[c] = csub(row[c], cmul(f, pk[c]));
       }
     }
-    if (act) {
+    if (act && r < M) {
 #pragma unroll
-      for (int c = 0; c < M; ++c) sc->qinv[m][r * M + c] = row[M + c];
+      for (int c = 0; c < M; ++c) sc->qinv[m][r * M + c] = row[ML + c];
     }
   } else if (warp == QW) {
     // Pending balance scales on the fp64 master (fastfca.cpp:139-141), saved
@@ -113,14 +119,20 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
     // V = (W^H)^{-1}: Gauss-Jordan with partial pivoting on lanes [0, M)
     // (row r of W^H = conj of column r of W), rows chosen in place.
     const bool act = lane < M;
-    SC row[2 * M];
+    SC row[2 * ML];
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
-      const double2 w = Wd[c + r * M];
-      row[c] = mkc<SR>(SR(w.x), SR(-w.y));
-      row[M + c] = mkc<SR>(c == r ? SR(1) : SR(0), SR(0));
+    for (int c = 0; c < ML; ++c) {
+      if (r < M && c < M) {
+        const double2 w = Wd[c + r * M];
+        row[c] = mkc<SR>(SR(w.x), SR(-w.y));
+      } else {
+        row[c] = mkc<SR>(c == r ? SR(1) : SR(0), SR(0));
+      }
+      row[ML + c] = mkc<SR>(c == r ? SR(1) : SR(0), SR(0));
     }
-    bool used = false;  // lanes >= M run duplicate copies in their own segments
+    // Padding rows never compete for a pivot (their columns < M are zero and
+    // the steps stop at M); lanes >= ML run duplicate copies in their segments.
+    bool used = r >= M;
     int step = -1;  // the step at which this row was the pivot
     double ld = 0.0;
     bool ok = true;
@@ -129,37 +141,37 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
       SR best = used ? SR(-1) : cabs2(row[k]);
       int bl = lane;
 #pragma unroll
-      for (int o = M / 2; o > 0; o >>= 1) {
-        const SR ob = __shfl_xor_sync(0xffffffffu, best, o, M);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o, M);
+      for (int o = ML / 2; o > 0; o >>= 1) {
+        const SR ob = __shfl_xor_sync(0xffffffffu, best, o, ML);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o, ML);
         if (ob > best || (ob == best && ol < bl)) best = ob, bl = ol;
       }
-      const int pl = bl % M;
-      SC pk[2 * M];
+      const int pl = bl % ML;
+      SC pk[2 * ML];
 #pragma unroll
-      for (int c = k; c < 2 * M; ++c) pk[c] = shfl_c<SR>(row[c], pl, M);
+      for (int c = k; c < 2 * ML; ++c) pk[c] = shfl_c<SR>(row[c], pl, ML);
       const SR pm = cabs2(pk[k]);
       if (!(pm > SR(0)) || !isfinite(pm)) ok = false;
       ld += SMath<SR>::log_d(pm);
       const SR s = SMath<SR>::rcp(pm);
       const SC ipiv = mkc<SR>(pk[k].x * s, -pk[k].y * s);
 #pragma unroll
-      for (int c = k + 1; c < 2 * M; ++c) pk[c] = cmul(pk[c], ipiv);
+      for (int c = k + 1; c < 2 * ML; ++c) pk[c] = cmul(pk[c], ipiv);
       if (r == pl) {
 #pragma unroll
-        for (int c = k + 1; c < 2 * M; ++c) row[c] = pk[c];
+        for (int c = k + 1; c < 2 * ML; ++c) row[c] = pk[c];
         used = true;
         step = k;
       } else {
         const SC f = row[k];
 #pragma unroll
-        for (int c = k + 1; c < 2 * M; ++c) row[c] = csub(row[c], cmul(f, pk[c]));
+        for (int c = k + 1; c < 2 * ML; ++c) row[c] = csub(row[c], cmul(f, pk[c]));
       }
     }
     // Row chosen at step k carries row k of the inverse in its right half.
     if (act && step >= 0) {
 #pragma unroll
-      for (int c = 0; c < M; ++c) sc->V[step * M + c] = row[M + c];
+      for (int c = 0; c < M; ++c) sc->V[step * M + c] = row[ML + c];
     }
     if (lane == 0) {
       sc->logdet_old = ld;
@@ -174,7 +186,9 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
 template <int M, typename SR>
 __device__ bool ip_fast_sweep(int lane, double2* Wd, IpFastScratch<M, SR>* sc, double& logdet_new) {
   using SC = cplx_t<SR>;
-  const int j = lane % M;
+  constexpr int ML = Pow2Ceil<M>::value;
+  const int j = lane % ML < M ? lane % ML : 0;  // padding lanes shadow row / column 0
+  const bool live = lane % ML < M;
   SC vcol[M];  // column j of V
 #pragma unroll
   for (int i = 0; i < M; ++i) vcol[i] = sc->V[i * M + j];
@@ -184,7 +198,7 @@ __device__ bool ip_fast_sweep(int lane, double2* Wd, IpFastScratch<M, SR>* sc, d
   for (int m = 0; m < M; ++m) {
     SC vm[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) vm[i] = shfl_c<SR>(vcol[i], m, M);
+    for (int i = 0; i < M; ++i) vm[i] = shfl_c<SR>(vcol[i], m, ML);
     // lane i: w_i = sum_c Q_m^{-1}(i, c) v_m(c)
     const SC* qi = sc->qinv[m] + j * M;
     SC w = mkc<SR>(SR(0), SR(0));
@@ -195,9 +209,9 @@ __device__ bool ip_fast_sweep(int lane, double2* Wd, IpFastScratch<M, SR>* sc, d
 #pragma unroll
     for (int i = 1; i < M; ++i)
       if (i == j) vj = vm[i];
-    SR e = w.x * vj.x + w.y * vj.y;
+    SR e = live ? w.x * vj.x + w.y * vj.y : SR(0);
 #pragma unroll
-    for (int o = M / 2; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o, M);
+    for (int o = ML / 2; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o, ML);
     const bool good = isfinite(e) && e > SR(0) && isfinite(w.x) && isfinite(w.y);
     ok = ok && __all_sync(0xffffffffu, good);
     const SR is = SMath<SR>::rsq(e);
@@ -207,7 +221,7 @@ __device__ bool ip_fast_sweep(int lane, double2* Wd, IpFastScratch<M, SR>* sc, d
     // r_j = w_new^H v_j ; V(:, j) -= v_m (r_j - [j == m]) / s
     SC wp[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) wp[i] = shfl_c<SR>(wn, i, M);
+    for (int i = 0; i < M; ++i) wp[i] = shfl_c<SR>(wn, i, ML);
     SC rj = mkc<SR>(SR(0), SR(0));
 #pragma unroll
     for (int i = 0; i < M; ++i) rj = cadd(rj, cmulc(wp[i], vcol[i]));

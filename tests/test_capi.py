@@ -10,7 +10,7 @@ from conftest import HAS_GPU, ROOT
 
 def header_symbols():
     text = (ROOT / "include" / "ffca.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|void|long long|const char\*)\s+(ffca_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void\*?|long long|const char\*)\s+(ffca_\w+)\s*\(", text, re.M)))
 
 
 def test_header_matches_binding_exports():

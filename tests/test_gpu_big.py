@@ -165,3 +165,52 @@ def test_big_m4_ip_restart_matches_oracle(gpu):
     for f in range(2):
         assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= 2e-3, f
         assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= 2e-3, f
+
+
+# ---- M = 3, N = 4 (BASELINE config 4's shape): 96 threads x 7 frame slots per
+# bin, eight bins per SM; odd M exercises the padded tensor-memory records, the
+# idle fourth lane of the covariance pass and the reference-order IP.
+@pytest.mark.parametrize("T", [200, 626, 672])
+def test_big_m3_fit_trace_and_separation(gpu, T):
+    iters = 10
+    x, W, L, H = make_case(5, T, seed=T + 2, sigma_v=1.5, M=3, N=4)
+    r = fit(x, W, L, H, iters, "fp32")
+    Wo, Lo, Ho, nll_o, _, _ = oracle.fit(x, W, L, H, iters)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL["fp32"], (rel.max(), int(rel.argmax()))
+    assert (r.bin_status == 0).all()
+    img_g = api.fastfca_separate(api.Spectrogram(x), r.params, precision="fp32")
+    img_o = oracle.separate(x, Wo, Lo, Ho)
+    for n in range(4):
+        assert rel_l2(img_g[n].f, img_o[n]) <= SEP_TOL["fp32"], n
+
+
+def test_big_m3_options_silent_bin_and_old_kernel(gpu, monkeypatch):
+    x, W, L, H = make_case(4, 626, seed=41, sigma_v=1.5, M=3, N=4)
+    x[2] = 0.0
+    r = fit(x, W, L, H, 6, "fp32", normalize_scales=False)
+    _, _, _, nll_o, _, _ = oracle.fit(x, W, L, H, 6, normalize_scales=False)
+    rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+    assert rel.max() <= NLL_TOL["fp32"]
+    assert np.array_equal(r.params.act[2], H[2]) and np.array_equal(r.params.decorr[2], W[2])
+    r2 = fit(x, W, L, H, 6, "fp32", record_trace=False, normalize_scales=False)
+    assert len(r2.nll) == 0
+    for a, b in zip(r2.params.act, r.params.act):
+        assert np.array_equal(a, b)
+    r_big = fit(x, W, L, H, 6, "fp32")
+    monkeypatch.setenv("FFCA_NO_BIG", "1")
+    r_old = fit(x, W, L, H, 6, "fp32")
+    a, b = np.asarray(r_big.nll), np.asarray(r_old.nll)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
+
+
+def test_big_m3_ip_restart_matches_oracle(gpu):
+    x, W, L, H = make_case(2, 626, seed=43, sigma_v=1.5, M=3, N=4)
+    W = W.copy()
+    W[1, :, 0] = 0.0
+    r = fit(x, W, L, H, 3, "fp32", record_trace=False, seed=7)
+    Wo, Lo, Ho, _, _, _ = oracle.fit(x, W, L, H, 3, record_trace=False, seed=7)
+    assert (r.bin_status == 0).all()
+    for f in range(2):
+        assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= 2e-3, f
+        assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= 2e-3, f
