@@ -10,19 +10,31 @@ namespace ffca {
 
 namespace {
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS, int MINB = 1>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, int MINB = 1, bool AUXG = false>
 int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
-  using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
+  using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS, AUXG>;
   *handled = false;
   int dev_max = 0;
   cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   if (dev_max <= 0) dev_max = 227 * 1024;
   const int C = (fp.T + Cfg::TCAP - 1) / Cfg::TCAP;
   if (C < 1 || C > 16) return FFCA_OK;  // not handled: the streaming kernel takes it
-  const BigLayout lay = Cfg::layout(C);
+  const BigLayout lay = Cfg::layout(C, fp.T);
   if (lay.total > dev_max) return FFCA_OK;
   *handled = true;
   if (fp.nprob == 0) return FFCA_OK;
+  if (AUXG) {
+    // Cold-path scratch (restart generator, saved W, reference-order IP
+    // matrices) in global memory: AUX_BYTES per CTA of the CALL (concurrent chunks of the
+    // pipelined host fit take disjoint rows).
+    cudaError_t err;
+    const size_t per = size_t(C) * Cfg::AUX_BYTES;
+    const size_t nall = size_t(fp.work_total > 0 ? fp.work_total : fp.nprob);
+    char* base = static_cast<char*>(ctx->get(kAux, nall * per, &err));
+    if (!base)
+      return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: aux scratch alloc: ") + cudaGetErrorString(err));
+    fp.aux = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
+  }
   if (big_incr<M, R, SLOTS>()) {
     // U scratch [problem][T][M] (fit_big.cuh INCR): one allocation for the
     // whole call, this launch's rows at work_first (concurrent chunks of the
@@ -36,11 +48,11 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
     fp.work = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
   }
   if (C == 1) {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB, AUXG>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     kern<<<fp.nprob, NTHR, lay.total, st>>>(fp, lay);
   } else {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true, MINB>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true, MINB, AUXG>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
@@ -72,7 +84,13 @@ int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp
   if (fp.blk || fp.flavor != 0 || fp.fix_loadings) return FFCA_OK;
   if (M == 8 && fp.N == 12) {
     if (fp64) return launch_big_t<8, 12, double, 4, 448, 2>(ctx, fp, st, handled);
-    return launch_big_t<8, 12, float, 8, 512, 1>(ctx, fp, st, handled);
+    // fp32: 256 threads x 8 slots = 2048 frames per CTA and TWO CTAs per SM
+    // (111 KB of shared memory and 256 tensor-memory columns each): a c3 bin
+    // is a 4-CTA cluster, and every SM hosts slices of two bins, so one bin's
+    // reductions, cluster barriers and IP overlap the other's frame passes.
+    // FFCA_BIG_WIDE=1: the 512-thread, one-CTA-per-SM shape (2-CTA clusters).
+    if (getenv("FFCA_BIG_WIDE")) return launch_big_t<8, 12, float, 8, 512, 1>(ctx, fp, st, handled);
+    return launch_big_t<8, 12, float, 8, 256, 1, 2, true>(ctx, fp, st, handled);
   }
   // BASELINE config 2 (M = 4, N = 6, T = 2000): 256 threads x 8 frame slots
   // hold a 2048-frame bin in one CTA; three CTAs (three bins) share an SM

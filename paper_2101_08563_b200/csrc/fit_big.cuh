@@ -97,7 +97,7 @@ constexpr int pow2_at_least(int n) {
   return p;
 }
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool AUXG = false>
 struct BigCfg {
   static constexpr int VE = Vec16<R>::n;           // reals per 16-byte vector
   static constexpr int NHP = (N + VE - 1) / VE;    // H planes
@@ -132,11 +132,21 @@ struct BigCfg {
   static_assert(WPR == 4 || WPR == 8 || WPR == 16, "record width");
 
   static int al(int v) { return (v + 15) & ~15; }
-  static BigLayout layout(int csize) {
+  // Cold-path scratch of a CTA in global memory (FitParams::aux): the restart
+  // generator, the saved W and the two small matrices of the reference-order
+  // IP / log-det -- kept out of shared memory so that two CTAs share an SM.
+  static constexpr int AUX_RNG = 0;
+  static constexpr int AUX_WSAVE = (int(sizeof(RestartRng)) + 15) & ~15;
+  static constexpr int AUX_IPSCR = AUX_WSAVE + M * M * 16;
+  static constexpr int AUX_LDSCR = AUX_IPSCR + ((M * M * 2 * int(sizeof(R)) + 15) & ~15);
+  static constexpr int AUX_BYTES = (AUX_LDSCR + M * (M + 1) * 2 * int(sizeof(R)) + 255) & ~255;
+
+  static BigLayout layout(int csize, int T) {
     BigLayout L{};
     L.csize = csize;
     L.tcap = TCAP;
-    L.ps = TCAP + 4;  // planes start 16 banks apart
+    const int tloc = (T + csize - 1) / csize;     // frames of the largest CTA
+    L.ps = ((tloc + 3) & ~3) + 4;  // planes start 16 banks apart
     int o = 0;
     L.off_h = o; o = al(o + NHP * L.ps * 16);
     const int rs = int(sizeof(R));
@@ -152,8 +162,8 @@ struct BigCfg {
     L.off_psum = o; o = al(o + M * rs);
     L.off_wd = o; o = al(o + M * M * 16);
     L.off_wr = o; o = al(o + M * M * 2 * rs);
-    L.off_ipscr = o; o = al(o + M * M * 2 * rs);
-    L.off_ldscr = o; o = al(o + M * (M + 1) * 2 * rs);
+    L.off_ipscr = o; if (!AUXG) o = al(o + M * M * 2 * rs);  // AUXG: global (aux)
+    L.off_ldscr = o; if (!AUXG) o = al(o + M * (M + 1) * 2 * rs);
     L.off_red = o; o = al(o + 2 * NW * KRED * rs);
     L.off_cx = o; o = al(o + 2 * csize * KRED * 8);
     L.off_scal = o; o = al(o + 128);
@@ -167,7 +177,7 @@ struct BigCfg {
     int e = al(o + (KQ + 2 * (M + 1)) * 8);
     L.off_q = e; e = al(e + KQ * 8);
     L.off_ipf = e; e = al(e + int(sizeof(IpFastScratch<M, R>)));
-    L.off_rng = e; e = al(e + int(sizeof(RestartRng)));
+    L.off_rng = e; if (!AUXG) e = al(e + AUX_IPSCR);  // restart generator + saved W
     o = al(o + gscr) > e ? al(o + gscr) : e;
     L.total = o;
     return L;
@@ -330,9 +340,9 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(
 __device__ __forceinline__ float2 fmul2s(float2 a, float s) { return __fmul2_rn(a, f2(s, s)); }
 __device__ __forceinline__ float2 fneg2(float2 a) { return f2(-a.x, -a.y); }
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL, int MINB = 1>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL, int MINB = 1, bool AUXG = false>
 __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLayout lay) {
-  using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS>;
+  using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS, AUXG>;
   using C = cplx_t<R>;
   using V = typename Vec16<R>::type;
   constexpr int VE = Cfg::VE, NHP = Cfg::NHP, NW = Cfg::NW, PW = Cfg::PW, HW = Cfg::HW;
@@ -408,8 +418,11 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   B* psum = reinterpret_cast<B*>(smem + lay.off_psum);
   double2* Wd = reinterpret_cast<double2*>(smem + lay.off_wd);
   C* Wr = reinterpret_cast<C*>(smem + lay.off_wr);
-  C* ipscr = reinterpret_cast<C*>(smem + lay.off_ipscr);
-  C* ldscr = reinterpret_cast<C*>(smem + lay.off_ldscr);
+  // Cold-path scratch: shared memory, or (AUXG) this CTA's slice of FitParams::aux.
+  unsigned char* aux = AUXG ? reinterpret_cast<unsigned char*>(p.aux) + size_t(blockIdx.x) * Cfg::AUX_BYTES
+                            : smem + lay.off_rng;
+  C* ipscr = AUXG ? reinterpret_cast<C*>(aux + Cfg::AUX_IPSCR) : reinterpret_cast<C*>(smem + lay.off_ipscr);
+  C* ldscr = AUXG ? reinterpret_cast<C*>(aux + Cfg::AUX_LDSCR) : reinterpret_cast<C*>(smem + lay.off_ldscr);
   R* red = reinterpret_cast<R*>(smem + lay.off_red);
   double* cx = reinterpret_cast<double*>(smem + lay.off_cx);
   BigScalars* sc = reinterpret_cast<BigScalars*>(smem + lay.off_scal);
@@ -417,7 +430,8 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   double* ex = reinterpret_cast<double*>(smem + lay.off_ex);
   double* qraw = reinterpret_cast<double*>(smem + lay.off_q);
   IpFastScratch<M, R>* ipf = reinterpret_cast<IpFastScratch<M, R>*>(smem + lay.off_ipf);
-  RestartRng* rng = reinterpret_cast<RestartRng*>(smem + lay.off_rng);
+  RestartRng* rng = reinterpret_cast<RestartRng*>(aux + Cfg::AUX_RNG);
+  double2* wsave = reinterpret_cast<double2*>(aux + Cfg::AUX_WSAVE);
   B* Ld = Ld0;
   B* hsc = hsc0;
   B* hinv = hinv0;
@@ -1227,7 +1241,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   // restart) from the saved W.  Leaves log|det W|^2 of the result in
   // sc->logdet0 / sc->ldok for the next trace entry.
   auto run_ip = [&](unsigned long long seed) {
-    ip_fast_prep<M, R, B>(warp, lane, Wd, wsc, qraw, invT, ipf);
+    ip_fast_prep<M, R, B>(warp, lane, Wd, wsc, qraw, invT, ipf, wsave);
     __syncthreads();
     if (warp == 0) {
       double ldn = 0.0;
@@ -1238,7 +1252,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
           sc->ldok = 1;
         }
       } else {
-        for (int k = lane; k < M * M; k += 32) Wd[k] = ipf->wsave[k];
+        for (int k = lane; k < M * M; k += 32) Wd[k] = wsave[k];
         __syncwarp();
         int bad = -1;
         const bool ok = ip_update_warp_reg<M, R>(Wd, qraw, invT, seed, bin_index, rng, ipscr, lane, bad);

@@ -85,6 +85,7 @@ struct FitParams {
   int nc;           // MM: sources per L-reduction chunk
   int tloc;         // frames held per CTA (= T, or ceil(T/C) for a C-CTA cluster)
   int blk;          // x holds packed block covariances [nprob][T][M*M] (T = blocks)
+  void* aux;        // large-bin kernel: cold-path global scratch, AUX_BYTES per CTA
   int work_total, work_first;  // host: scratch rows of the whole call and this launch's first
                                // row (pipelined chunks share one allocation); 0, 0 = nprob rows
   unsigned long long* timing;  // optional per-problem phase cycle counters [nprob][16]

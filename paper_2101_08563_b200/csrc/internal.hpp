@@ -49,7 +49,7 @@ struct ffca_ctx {
 
 namespace ffca {
 
-enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kWave, kSpec, kFrames, kSepRec, kNumSlots };
+enum Slot { kX = 0, kXs, kH, kHs, kW, kL, kPow, kNll, kStat, kU, kImg, kWave, kSpec, kFrames, kSepRec, kAux, kNumSlots };
 
 // Threads per fit CTA: about 4 frames per thread, capped at the kernel's
 // launch bound; a multiple of 32*M when the weighted-covariance pass is split

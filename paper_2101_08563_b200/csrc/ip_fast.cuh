@@ -32,7 +32,6 @@ template <int M, typename SR>
 struct IpFastScratch {
   cplx_t<SR> qinv[M][M * M];  // row-major Q_m^{-1}
   cplx_t<SR> V[M * M];        // row-major (W^H)^{-1}
-  double2 wsave[M * M];       // W at the start of the sweep (fallback input)
   double logdet_old;
   int ok;
 };
@@ -53,7 +52,7 @@ __device__ __forceinline__ cplx_t<SR> shfl_c(cplx_t<SR> v, int src, int width) {
 // M x M blocks of the inverses are the inverses of the blocks).
 template <int M, typename SR, typename B>
 __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, const double* qraw,
-                             double invT, IpFastScratch<M, SR>* sc) {
+                             double invT, IpFastScratch<M, SR>* sc, double2* wsave) {
   using SC = cplx_t<SR>;
   constexpr int ML = Pow2Ceil<M>::value;
   static_assert(32 % ML == 0, "segments");
@@ -113,7 +112,7 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
       w.x *= c;
       w.y *= c;
       Wd[k] = w;
-      sc->wsave[k] = w;
+      wsave[k] = w;  // W at the start of the sweep: the fallback's input
     }
     __syncwarp();
     // V = (W^H)^{-1}: Gauss-Jordan with partial pivoting on lanes [0, M)
@@ -182,7 +181,7 @@ __device__ void ip_fast_prep(int warp, int lane, double2* Wd, const B* wsc, cons
 
 // The sequential sweep (one warp; lanes [0, M) active).  Writes the new
 // columns into Wd and returns false on a failed acceptance test (Wd then
-// holds partial results: the caller restores sc->wsave).
+// holds partial results: the caller restores the saved W).
 template <int M, typename SR>
 __device__ bool ip_fast_sweep(int lane, double2* Wd, IpFastScratch<M, SR>* sc, double& logdet_new) {
   using SC = cplx_t<SR>;
