@@ -1,8 +1,6 @@
 // fastfca.hpp -- the FastFCA fit / separate entry points, B200 backend
-// (drop-in for reference proj/include/fastfca/fastfca.hpp:16-66 and :76-81;
-// not provided: fastfca_mwf :60-61, ajd_cost :68-71, reconstruct_scms :83-84
-// -- explicit filter matrices and diagnostics outside the fit/separate path,
-// SURVEY section 8 out of scope).
+// (drop-in for reference proj/include/fastfca/fastfca.hpp:16-84: every
+// function the reference header declares).
 //
 // Same names, argument order, defaults and error behaviour as the reference:
 // std::invalid_argument on shape mismatch, NumericalError on a singular IP
@@ -90,6 +88,19 @@ FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
 // Block-stationary statistics; block_size == 1 reproduces sample_covs
 // (fastfca.hpp:80-81, fastfca.cpp:266-268).
 SampleCovSet piecewise_prepare(const Spectrogram& spec, int block_size);
+
+// Decomposed Wiener filter W^-H diag(gains) W^H at one (i, j, n)
+// (fastfca.hpp:60-61, fastfca.cpp:193-203).
+CMat fastfca_mwf(const FastFcaParams& params, int i, int j, int n);
+
+// Joint-diagonality cost sum_j alpha_j D_LD(W^H Xhat_j W | ddiag(...))
+// (fastfca.hpp:68-71, fastfca.cpp:225-239).  Empty weights mean alpha_j = 1;
+// needs the block covariances (`mats`) and throws NumericalError when a
+// transformed covariance is not positive definite.
+double ajd_cost(const CMat& w, const SampleCovSet& covs, int i, const RVec& weights = RVec());
+
+// R_in = W^-H Lambda_n W^-1 (fastfca.hpp:83-84, fastfca.cpp:270-282).
+std::vector<std::vector<CMat>> reconstruct_scms(const FastFcaParams& params);
 
 // Decomposed multichannel Wiener filter (fastfca.cpp:205-223).
 std::vector<Spectrogram> fastfca_separate(const Spectrogram& spec, const FastFcaParams& params);

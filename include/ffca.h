@@ -263,6 +263,23 @@ int ffca_ip_update_w(ffca_ctx* ctx, int dim, int sources, int blocks, int is_blo
  * ("singular decorrelation matrix") when a pivot is zero or non-finite. */
 int ffca_log_abs_det2(ffca_ctx* ctx, int dim, const double* w, double* out);
 
+/* fastfca_mwf (fastfca.cpp:193-203): out [dim*dim] complex col-major =
+ * W^-H diag(gains) W^H for source n at one frame; act_col = H(:, j). */
+int ffca_mwf(ffca_ctx* ctx, int dim, int sources, const double* w, const double* loading,
+             const double* act_col, int n, double* out);
+
+/* reconstruct_scms (fastfca.cpp:270-282): out [bins][sources][dim*dim] complex
+ * col-major, R_in = W^-H Lambda_n W^-1. */
+int ffca_reconstruct_scms(ffca_ctx* ctx, int bins, int dim, int sources, const double* W,
+                          const double* L, double* out);
+
+/* ajd_cost (fastfca.cpp:225-239): *out = sum_j alpha_j D_LD(W^H X_j W |
+ * ddiag(.)) over one bin's block covariances mats [blocks][dim*dim]; weights
+ * (nullable) [blocks].  FFCA_NUMERICAL when a transformed covariance is not
+ * positive definite (hermitian.hpp:93-94). */
+int ffca_ajd_cost(ffca_ctx* ctx, int dim, int blocks, const double* mats, const double* w,
+                  const double* weights, double* out);
+
 /* source_gain (fastfca.cpp:74-78): gain [dim x frames] col-major =
  * L(:,n) H(n,:) / floor_positive(L H). */
 int ffca_source_gain(ffca_ctx* ctx, int dim, int sources, int frames, const double* loading,

@@ -663,6 +663,55 @@ void mm_update_lh(const RMat& u, RMat& loading, RMat& act, bool update_loading, 
                           loading.data(), act.data(), update_loading ? 1 : 0, eps));
 }
 
+CMat fastfca_mwf(const FastFcaParams& params, int i, int j, int n) {
+  if (i < 0 || i >= params.bins || j < 0 || j >= params.frames || n < 0 || n >= params.sources)
+    throw std::invalid_argument("fastfca_mwf: index out of range");
+  const int M = params.dim, N = params.sources;
+  std::vector<double> col(N);
+  for (int q = 0; q < N; ++q) col[q] = params.act[i](q, j);
+  CMat out(M, M);
+  raise(ffca_mwf(context(0), M, N, reinterpret_cast<const double*>(params.decorr[i].data()),
+                 params.loading[i].data(), col.data(), n, reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
+double ajd_cost(const CMat& w, const SampleCovSet& covs, int i, const RVec& weights) {
+  if (weights.size() != 0 && weights.size() != covs.blocks)
+    throw std::invalid_argument("ajd_cost: weight count mismatch");  // fastfca.cpp:227-228
+  if (i < 0 || i >= covs.bins || int(covs.mats.size()) != covs.bins ||
+      int(covs.mats[i].size()) != covs.blocks)
+    throw std::invalid_argument("ajd_cost: needs the block covariances (SampleCovSet::mats)");
+  const int M = covs.dim, J = covs.blocks;
+  if (w.rows() != M || w.cols() != M) throw std::invalid_argument("ajd_cost: W shape mismatch");
+  std::vector<double> x(size_t(J) * M * M * 2);
+  for (int j = 0; j < J; ++j)
+    std::memcpy(x.data() + size_t(j) * M * M * 2, covs.mats[i][j].data(), sizeof(double) * M * M * 2);
+  double out = 0.0;
+  raise(ffca_ajd_cost(context(0), M, J, x.data(), reinterpret_cast<const double*>(w.data()),
+                      weights.size() ? weights.data() : nullptr, &out));
+  return out;
+}
+
+std::vector<std::vector<CMat>> reconstruct_scms(const FastFcaParams& params) {
+  const int F = params.bins, M = params.dim, N = params.sources;
+  std::vector<std::vector<CMat>> scms(F);
+  if (F == 0) return scms;
+  std::vector<double> W(size_t(F) * M * M * 2), L(size_t(F) * M * N), out(size_t(F) * N * M * M * 2);
+  for (int i = 0; i < F; ++i) {
+    std::memcpy(W.data() + size_t(i) * M * M * 2, params.decorr[i].data(), sizeof(double) * M * M * 2);
+    std::memcpy(L.data() + size_t(i) * M * N, params.loading[i].data(), sizeof(double) * M * N);
+  }
+  raise(ffca_reconstruct_scms(context(0), F, M, N, W.data(), L.data(), out.data()));
+  for (int i = 0; i < F; ++i)
+    for (int n = 0; n < N; ++n) {
+      CMat r(M, M);
+      std::memcpy(static_cast<void*>(r.data()), out.data() + (size_t(i) * N + n) * M * M * 2,
+                  sizeof(double) * M * M * 2);
+      scms[i].push_back(r);
+    }
+  return scms;
+}
+
 double log_abs_det2(const CMat& w) {
   if (w.rows() != w.cols() || w.rows() < 1) throw std::invalid_argument("log_abs_det2: not square");
   double out = 0.0;

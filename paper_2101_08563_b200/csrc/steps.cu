@@ -241,6 +241,147 @@ __global__ void __launch_bounds__(kStepThreads)
   for (int k = threadIdx.x; k < M * N; k += kStepThreads) L[k] = ls[k];
 }
 
+// ---- small dense helpers for the diagnostics below (one thread, fp64) ----
+constexpr int kMaxDim = 8;
+
+// Solve A X = B in place (B <- X) by Gauss-Jordan with partial pivoting
+// (largest modulus, lowest row on ties -- Eigen::PartialPivLU's choice).
+// A, B: M x M column-major.  Returns false on a zero / non-finite pivot.
+__device__ bool gj_solve(double2* A, double2* B, int M) {
+  for (int k = 0; k < M; ++k) {
+    int piv = k;
+    double best = cabs2(A[k + k * M]);
+    for (int r = k + 1; r < M; ++r) {
+      const double v = cabs2(A[r + k * M]);
+      if (v > best) best = v, piv = r;
+    }
+    if (!(best > 0.0) || !isfinite(best)) return false;
+    if (piv != k)
+      for (int c = 0; c < M; ++c) {
+        double2 t = A[k + c * M]; A[k + c * M] = A[piv + c * M]; A[piv + c * M] = t;
+        t = B[k + c * M]; B[k + c * M] = B[piv + c * M]; B[piv + c * M] = t;
+      }
+    const double2 d = A[k + k * M];
+    for (int c = 0; c < M; ++c) {
+      A[k + c * M] = cdiv(A[k + c * M], d);
+      B[k + c * M] = cdiv(B[k + c * M], d);
+    }
+    for (int r = 0; r < M; ++r) {
+      if (r == k) continue;
+      const double2 f = A[r + k * M];
+      for (int c = 0; c < M; ++c) {
+        A[r + c * M] = csub(A[r + c * M], cmul(f, A[k + c * M]));
+        B[r + c * M] = csub(B[r + c * M], cmul(f, B[k + c * M]));
+      }
+    }
+  }
+  return true;
+}
+
+// fastfca_mwf (fastfca.cpp:193-203): W^-H diag(gains) W^H at one (i, j, n).
+__global__ void step_mwf_kernel(const double2* W, const double* L, const double* hcol, int M, int N,
+                                int n, double2* out, int* status) {
+  if (threadIdx.x != 0) return;
+  double2 a[kMaxDim * kMaxDim], b[kMaxDim * kMaxDim];
+  for (int r = 0; r < M; ++r)
+    for (int c = 0; c < M; ++c) {
+      const double2 w = W[c + r * M];
+      a[r + c * M] = make_double2(w.x, -w.y);  // a = W^H
+    }
+  for (int k = 0; k < M; ++k) {
+    double mix = 0.0;
+    for (int q = 0; q < N; ++q) mix += L[k + q * M] * hcol[q];
+    mix = fmax(mix, 1e-300);
+    const double g = L[k + n * M] * hcol[n] / mix;
+    for (int c = 0; c < M; ++c) b[k + c * M] = make_double2(g * a[k + c * M].x, g * a[k + c * M].y);
+  }
+  const bool ok = gj_solve(a, b, M);
+  for (int k = 0; k < M * M; ++k) out[k] = b[k];
+  *status = ok ? kStatusOk : kStatusSingularW;
+}
+
+// reconstruct_scms (fastfca.cpp:270-282): R_in = W^-H Lambda_n W^-1, one
+// thread per bin.
+__global__ void step_scms_kernel(const double2* W, const double* L, int P, int M, int N,
+                                 double2* out, int* status) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double2 a[kMaxDim * kMaxDim], winv[kMaxDim * kMaxDim];
+  for (int k = 0; k < M * M; ++k) {
+    a[k] = W[size_t(p) * M * M + k];
+    winv[k] = make_double2((k % M) == (k / M) ? 1.0 : 0.0, 0.0);
+  }
+  const bool ok = gj_solve(a, winv, M);
+  if (!ok) atomicMax(status, kStatusSingularW);
+  for (int n = 0; n < N; ++n)
+    for (int r = 0; r < M; ++r)
+      for (int c = 0; c < M; ++c) {
+        double2 acc = make_double2(0.0, 0.0);  // sum_k conj(winv(k, r)) lam_k winv(k, c)
+        for (int k = 0; k < M; ++k) {
+          const double lam = L[size_t(p) * M * N + k + n * M];
+          const double2 u = winv[k + r * M], v = winv[k + c * M];
+          acc.x += lam * (u.x * v.x + u.y * v.y);
+          acc.y += lam * (u.x * v.y - u.y * v.x);
+        }
+        out[(size_t(p) * N + n) * M * M + r + c * M] = acc;
+      }
+}
+
+// ajd_cost terms (fastfca.cpp:225-239, hermitian.hpp:85-102): per block j,
+// t = W^H X_j W and D_LD(t | ddiag(t)) = max(0, sum_k log Re t_kk - logdet
+// sym(t)) (tr(ddiag(t)^-1 t) = M exactly); Cholesky decides positive
+// definiteness.  One thread per block; the weighted sum runs in block order on
+// the host side of the ABI call.
+__global__ void step_ajd_kernel(const double2* X, const double2* W, int M, int J, double* terms,
+                                int* status) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double2 xw[kMaxDim * kMaxDim], t[kMaxDim * kMaxDim];
+  const double2* Xj = X + size_t(j) * M * M;
+  for (int r = 0; r < M; ++r)
+    for (int c = 0; c < M; ++c) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) acc = cadd(acc, cmul(Xj[r + k * M], W[k + c * M]));
+      xw[r + c * M] = acc;
+    }
+  for (int r = 0; r < M; ++r)
+    for (int c = 0; c < M; ++c) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) acc = cadd(acc, cmulc(W[k + r * M], xw[k + c * M]));
+      t[r + c * M] = acc;
+    }
+  // symmetrize, then Cholesky (lower), logdet = 2 sum log l_kk
+  double2 s[kMaxDim * kMaxDim];
+  for (int r = 0; r < M; ++r)
+    for (int c = 0; c < M; ++c)
+      s[r + c * M] = make_double2(0.5 * (t[r + c * M].x + t[c + r * M].x),
+                                  0.5 * (t[r + c * M].y - t[c + r * M].y));
+  bool pd = true;
+  double logdet_a = 0.0, logdet_b = 0.0;
+  for (int k = 0; k < M && pd; ++k) {
+    double d = s[k + k * M].x;
+    for (int q = 0; q < k; ++q) d -= cabs2(s[k + q * M]);
+    if (!(d > 0.0) || !isfinite(d)) { pd = false; break; }
+    const double l = sqrt(d);
+    s[k + k * M] = make_double2(l, 0.0);
+    logdet_a += 2.0 * log(l);
+    for (int r = k + 1; r < M; ++r) {
+      double2 v = s[r + k * M];
+      for (int q = 0; q < k; ++q) v = csub(v, cmul(s[r + q * M], make_double2(s[k + q * M].x, -s[k + q * M].y)));
+      s[r + k * M] = make_double2(v.x / l, v.y / l);
+    }
+    const double dk = t[k + k * M].x;
+    if (!(dk > 0.0) || !isfinite(dk)) { pd = false; break; }
+    logdet_b += log(dk);
+  }
+  if (!pd) {
+    atomicMax(status, 1);
+    terms[j] = 0.0;
+    return;
+  }
+  terms[j] = fmax(0.0, logdet_b - logdet_a);
+}
+
 struct DevBuf {  // call-scoped device memory (these entry points are not hot)
   void* p = nullptr;
   ~DevBuf() {
@@ -432,6 +573,98 @@ int ffca_log_abs_det2(ffca_ctx* ctx, int dim, const double* w, double* out) {
   FFCA_CUDA(cudaMemcpyAsync(out, O, 8, cudaMemcpyDeviceToHost, st));
   FFCA_CUDA(cudaStreamSynchronize(st));
   if (status == kStatusSingularW) return ffca_set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
+  return FFCA_OK;
+}
+
+int ffca_mwf(ffca_ctx* ctx, int dim, int sources, const double* w, const double* loading,
+             const double* act_col, int n, double* out) {
+  if (!ctx || !w || !loading || !act_col || !out)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_mwf: null argument");
+  if (dim < 1 || dim > kMaxDim || sources < 1 || n < 0 || n >= sources)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_mwf: bad shape or source index");
+  ctx->launches = 0;
+  DeviceScope g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int M = dim, N = sources;
+  DevBuf dw, dl, dh, dout, dstat;
+  if (dw.alloc(size_t(M) * M * 16) || dl.alloc(size_t(M) * N * 8) || dh.alloc(size_t(N) * 8) ||
+      dout.alloc(size_t(M) * M * 16) || dstat.alloc(4))
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca_mwf: device alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dw.p, w, size_t(M) * M * 16, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemcpyAsync(dl.p, loading, size_t(M) * N * 8, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemcpyAsync(dh.p, act_col, size_t(N) * 8, cudaMemcpyHostToDevice, st));
+  step_mwf_kernel<<<1, 32, 0, st>>>(dw.as<double2>(), dl.as<double>(), dh.as<double>(), M, N, n,
+                                    dout.as<double2>(), dstat.as<int>());
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  int status = 0;
+  FFCA_CUDA(cudaMemcpyAsync(&status, dstat.p, 4, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaMemcpyAsync(out, dout.p, size_t(M) * M * 16, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  if (status != kStatusOk) return ffca_set_err(FFCA_NUMERICAL, "fastfca_mwf: singular decorrelation matrix");
+  return FFCA_OK;
+}
+
+int ffca_reconstruct_scms(ffca_ctx* ctx, int bins, int dim, int sources, const double* W,
+                          const double* L, double* out) {
+  if (!ctx || !W || !L || !out)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_reconstruct_scms: null argument");
+  if (bins < 1 || dim < 1 || dim > kMaxDim || sources < 1)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_reconstruct_scms: bad shape");
+  ctx->launches = 0;
+  DeviceScope g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t M = dim, N = sources, P = bins;
+  DevBuf dw, dl, dout, dstat;
+  if (dw.alloc(P * M * M * 16) || dl.alloc(P * M * N * 8) || dout.alloc(P * N * M * M * 16) ||
+      dstat.alloc(4))
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca_reconstruct_scms: device alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dw.p, W, P * M * M * 16, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemcpyAsync(dl.p, L, P * M * N * 8, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemsetAsync(dstat.p, 0, 4, st));
+  step_scms_kernel<<<(bins + 63) / 64, 64, 0, st>>>(dw.as<double2>(), dl.as<double>(), bins, dim,
+                                                     sources, dout.as<double2>(), dstat.as<int>());
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  int status = 0;
+  FFCA_CUDA(cudaMemcpyAsync(&status, dstat.p, 4, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaMemcpyAsync(out, dout.p, P * N * M * M * 16, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  if (status != kStatusOk)
+    return ffca_set_err(FFCA_NUMERICAL, "reconstruct_scms: singular decorrelation matrix");
+  return FFCA_OK;
+}
+
+int ffca_ajd_cost(ffca_ctx* ctx, int dim, int blocks, const double* mats, const double* w,
+                  const double* weights, double* out) {
+  if (!ctx || !mats || !w || !out)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_ajd_cost: null argument");
+  if (dim < 1 || dim > kMaxDim || blocks < 1)
+    return ffca_set_err(FFCA_INVALID_ARGUMENT, "ffca_ajd_cost: bad shape");
+  ctx->launches = 0;
+  DeviceScope g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t M = dim, J = blocks;
+  DevBuf dx, dw, dt, dstat;
+  if (dx.alloc(J * M * M * 16) || dw.alloc(M * M * 16) || dt.alloc(J * 8) || dstat.alloc(4))
+    return ffca_set_err(FFCA_CUDA_ERROR, "ffca_ajd_cost: device alloc failed");
+  FFCA_CUDA(cudaMemcpyAsync(dx.p, mats, J * M * M * 16, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemcpyAsync(dw.p, w, M * M * 16, cudaMemcpyHostToDevice, st));
+  FFCA_CUDA(cudaMemsetAsync(dstat.p, 0, 4, st));
+  step_ajd_kernel<<<(blocks + 63) / 64, 64, 0, st>>>(dx.as<double2>(), dw.as<double2>(), dim, blocks,
+                                                      dt.as<double>(), dstat.as<int>());
+  ctx->launches++;
+  FFCA_CUDA(cudaGetLastError());
+  std::vector<double> terms(J);
+  int status = 0;
+  FFCA_CUDA(cudaMemcpyAsync(&status, dstat.p, 4, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaMemcpyAsync(terms.data(), dt.p, J * 8, cudaMemcpyDeviceToHost, st));
+  FFCA_CUDA(cudaStreamSynchronize(st));
+  if (status != 0)
+    return ffca_set_err(FFCA_NUMERICAL, "logdet_divergence: argument not positive definite");
+  double acc = 0.0;  // block order, as the reference's loop (fastfca.cpp:231-237)
+  for (size_t j = 0; j < J; ++j) acc += (weights ? weights[j] : 1.0) * terms[j];
+  *out = acc;
   return FFCA_OK;
 }
 

@@ -419,6 +419,78 @@ int main() {
     }
     CHECK(numerical);
   }
+  // ---- fastfca_mwf (fastfca.cpp:193-203), reconstruct_scms (:270-282),
+  // ajd_cost (:225-239) against the oracle; the filters of all sources sum to
+  // the identity (test_fastfca.cpp:342-359's partition, filter form)
+  {
+    std::mt19937 rng(72);
+    FastFcaParams p = random_params(3, 2, 6, 4, rng);
+    oracle::FastFcaParams po;
+    po.dim = 3, po.bins = 2, po.frames = 6, po.sources = 4;
+    for (int i = 0; i < 2; ++i) {
+      po.decorr.push_back(to_o(p.decorr[i]));
+      po.loading.push_back(to_o(p.loading[i]));
+      po.act.push_back(to_o(p.act[i]));
+    }
+    for (int i = 0; i < 2; ++i)
+      for (int j : {0, 5}) {
+        CMat total = CMat::Zero(3, 3);
+        for (int n = 0; n < 4; ++n) {
+          const CMat f = fastfca_mwf(p, i, j, n);
+          CHECK(rel_diff(f, oracle::fastfca_mwf(po, i, j, n)) <= 1e-12);
+          for (long k = 0; k < total.size(); ++k) total(k) += f(k);
+        }
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) CHECK(std::abs(total(r, c) - Complex(r == c ? 1.0 : 0.0)) < 1e-10);
+      }
+    const auto scms = reconstruct_scms(p);
+    const auto scms_o = oracle::reconstruct_scms(po);
+    CHECK(scms.size() == 2 && scms[0].size() == 4);
+    for (int i = 0; i < 2; ++i)
+      for (int n = 0; n < 4; ++n) {
+        CHECK(rel_diff(scms[i][n], scms_o[i][n]) <= 1e-12);
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c)  // Hermitian
+            CHECK(std::abs(scms[i][n](r, c) - std::conj(scms[i][n](c, r))) <= 1e-12 * (1.0 + std::abs(scms[i][n](r, c))));
+      }
+    // ajd_cost on block covariances
+    Spectrogram s = Spectrogram::zero(3, 2, 40);
+    for (int i = 0; i < 2; ++i) s.f[i] = random_complex(3, 40, rng);
+    const SampleCovSet cb = piecewise_prepare(s, 5);
+    std::vector<Complex> xflat(size_t(2) * 40 * 3);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 40; ++j)
+        for (int k = 0; k < 3; ++k) xflat[(size_t(i) * 40 + j) * 3 + k] = s.f[i](k, j);
+    const oracle::SampleCovSet cbo = oracle::piecewise_prepare(3, 2, 40, xflat.data(), 5);
+    RVec wts(cb.blocks);
+    for (int j = 0; j < cb.blocks; ++j) wts(j) = 0.5 + 0.25 * j;
+    std::vector<double> wts_o(wts.data(), wts.data() + cb.blocks);
+    for (int i = 0; i < 2; ++i) {
+      const double a = ajd_cost(p.decorr[i], cb, i);
+      const double ao = oracle::ajd_cost(to_o(p.decorr[i]), cbo, i, {});
+      CHECK(std::abs(a - ao) <= 1e-10 * (1.0 + std::abs(ao)));
+      const double b = ajd_cost(p.decorr[i], cb, i, wts);
+      const double bo = oracle::ajd_cost(to_o(p.decorr[i]), cbo, i, wts_o);
+      CHECK(std::abs(b - bo) <= 1e-10 * (1.0 + std::abs(bo)));
+      CHECK(a >= 0.0);
+    }
+    bool numerical = false;  // a zero block is not positive definite (hermitian.hpp:93-94)
+    SampleCovSet bad = cb;
+    bad.mats[0][1] = CMat::Zero(3, 3);
+    try {
+      ajd_cost(p.decorr[0], bad, 0);
+    } catch (const NumericalError&) {
+      numerical = true;
+    }
+    CHECK(numerical);
+    bool invalid = false;
+    try {
+      ajd_cost(p.decorr[0], cb, 0, RVec(3));
+    } catch (const std::invalid_argument&) {
+      invalid = true;
+    }
+    CHECK(invalid);
+  }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
