@@ -214,3 +214,21 @@ def test_big_m3_ip_restart_matches_oracle(gpu):
     for f in range(2):
         assert rel_l2(np.asarray(r.params.decorr[f]), Wo[f]) <= 2e-3, f
         assert rel_l2(np.asarray(r.params.act[f]), Ho[f]) <= 2e-3, f
+
+
+# The pipelined host fit (bin chunks on their own streams, concurrently) with
+# the large-bin kernel: each chunk works in its own rows of the U scratch and
+# of the cold-path scratch, so chunked and single-launch fits agree bit for bit.
+@pytest.mark.parametrize("shape", [(8, 12, 3000), (4, 6, 2000), (3, 4, 626)])
+def test_big_chunked_host_fit_is_bit_equal(gpu, monkeypatch, shape):
+    M, N, T = shape
+    x, W, L, H = make_case(7, T, seed=51 + M, sigma_v=1.5, M=M, N=N)
+    monkeypatch.setenv("FFCA_FIT_CHUNKS", "1")
+    r1 = fit(x, W, L, H, 4, "fp32")
+    monkeypatch.setenv("FFCA_FIT_CHUNKS", "3")
+    r3 = fit(x, W, L, H, 4, "fp32")
+    assert np.array_equal(np.asarray(r1.nll), np.asarray(r3.nll))
+    for a, b in zip(r1.params.act, r3.params.act):
+        assert np.array_equal(a, b)
+    for a, b in zip(r1.params.decorr, r3.params.decorr):
+        assert np.array_equal(a, b)
