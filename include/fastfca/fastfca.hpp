@@ -81,6 +81,7 @@ std::vector<FastFcaFitResult> fastfca_fit_batch(const std::vector<SampleCovSet>&
 // the GPU), then IP+MM with the loadings fixed.
 FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
                               const std::vector<CMat>& w_init, const FitOptions& fit = {});
+// gpu.precision is ignored here: the ICA mode always computes in fp64.
 FastFcaFitResult ica_mode_fit(const SampleCovSet& covs, int sources, int iters,
                               const std::vector<CMat>& w_init, const FitOptions& fit,
                               const GpuOptions& gpu);

@@ -100,7 +100,8 @@ void* ffca_pinned_buffer(ffca_ctx* ctx, int slot, size_t bytes);
  * (sample_covs, sigmodel.cpp:17-48).  nll: [batch][iters+1] trace (bin-order
  * sums of the per-bin slots, fastfca.cpp:186-189), required when
  * record_trace; nll_slots (nullable): [batch][iters+1][bins]; bin_status
- * (nullable): [batch][bins]. */
+ * (nullable): [batch][bins].  On FFCA_NUMERICAL the contents of W, L, H are
+ * unspecified (the pipelined path has copied partial results back by then). */
 int ffca_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts, const double* x,
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status);

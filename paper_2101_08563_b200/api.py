@@ -316,7 +316,10 @@ def ica_mode_fit(covs: SampleCovSet, sources: int, iters: int, w_init: np.ndarra
                  fit: FitOptions | None = None, *, precision: str = "fp32",
                  device: int | None = None) -> FastFcaFitResult:
     """fastfca.cpp:241-264 on the GPU: determined ICA mode (L = identity, H =
-    floored decorrelated powers of w_init, IP+MM with the loadings fixed)."""
+    floored decorrelated powers of w_init, IP+MM with the loadings fixed).
+    `precision` is accepted for symmetry with fastfca_fit, but this mode always
+    computes in fp64 (ffca.h, ffca_ica_fit: at its fixed point H tracks
+    |w^H x|^2 and the 1/H weights amplify fp32 cancellation)."""
     fit = fit or FitOptions()
     if sources != covs.dim:
         raise InvalidArgument("ica_mode_fit: requires as many sources as channels")

@@ -64,6 +64,9 @@
 #ifndef FFCA_BIG_INCR
 #define FFCA_BIG_INCR 1  // incremental mixture variances in the fp32 EM sweeps
 #endif
+#ifndef FFCA_BIG_PREFETCH
+#define FFCA_BIG_PREFETCH 0  // prefetch the next EM trip's U into registers (measured: no gain)
+#endif
 #ifndef FFCA_BIG_FS
 #define FFCA_BIG_FS 2  // frame slots per trip of the incremental EM sweep (4: spills at M = 8)
 #endif
@@ -730,6 +733,19 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
       // and L2 loads, reciprocals, stores) in flight per warp.
       constexpr int FS = FFCA_BIG_FS;
       static_assert(SLOTS % FS == 0, "frame slots per trip");
+#if FFCA_BIG_PREFETCH
+      float4 un[FS][M / 4];  // the next trip's U, fetched (L2) while this trip computes
+      auto fetch_u = [&](int s) {
+#pragma unroll
+        for (int f = 0; f < FS; ++f) {
+          const int t0 = frame_of(s + f, lane);
+          const float4* uw = reinterpret_cast<const float4*>(Ug + size_t(t0 < Tl ? t0 : 0) * M);
+#pragma unroll
+          for (int q = 0; q < M / 4; ++q) un[f][q] = __ldcg(uw + q);
+        }
+      };
+      fetch_u(0);
+#endif
 #pragma unroll 1
       for (int s = 0; s < nsl; s += FS) {
         int t[FS];
@@ -740,13 +756,22 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
           const int t0 = frame_of(s + f, lane);
           ok[f] = t0 < Tl;
           t[f] = ok[f] ? t0 : 0;
+#if FFCA_BIG_PREFETCH
+#pragma unroll
+          for (int q = 0; q < M / 4; ++q)
+            u[f][2 * q] = f2(un[f][q].x, un[f][q].y), u[f][2 * q + 1] = f2(un[f][q].z, un[f][q].w);
+#else
           const float4* uw = reinterpret_cast<const float4*>(Ug + size_t(t[f]) * M);
 #pragma unroll
           for (int q = 0; q < M / 4; ++q) {
             const float4 v = __ldcg(uw + q);
             u[f][2 * q] = f2(v.x, v.y), u[f][2 * q + 1] = f2(v.z, v.w);
           }
+#endif
         }
+#if FFCA_BIG_PREFETCH
+        if (s + FS < nsl) fetch_u(s + FS);
+#endif
 #pragma unroll
         for (int f = 0; f < FS; ++f) {
           float sg[M], pp[M];
