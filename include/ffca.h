@@ -106,6 +106,21 @@ int ffca_fit(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts, co
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status);
 
+/* ffca_fit on PER-BIN host buffers -- what a caller holding the reference's
+ * containers has (one allocation per bin: Spectrogram::f[i],
+ * FastFcaParams::decorr[i] / loading[i] / act[i]).  x_bins, W_in, L_in, H_in,
+ * W_out, L_out, H_out: arrays of batch*bins pointers, each bin in the layout
+ * of ffca_fit (in and out may alias).  The library gathers bin chunks into
+ * page-locked staging on `host_threads` host threads (<= 0: hardware
+ * concurrency, at most 16) and pipelines gather / H2D / fit / D2H / scatter
+ * over the chunks.  Results equal ffca_fit's bit for bit.  On FFCA_NUMERICAL
+ * the outputs are unspecified. */
+int ffca_fit_bins(ffca_ctx* ctx, const ffca_dims* dims, const ffca_fit_opts* opts,
+                  const double* const* x_bins, const double* power, const double* const* W_in,
+                  const double* const* L_in, const double* const* H_in, double* const* W_out,
+                  double* const* L_out, double* const* H_out, double* nll, double* nll_slots,
+                  int32_t* bin_status, int host_threads);
+
 /* ica_mode_fit (fastfca.hpp:76-78, fastfca.cpp:241-264): determined ICA mode.
  * dims->sources must equal dims->dim (else FFCA_INVALID_ARGUMENT with the
  * reference's message).  W: w_init on entry, the fitted W on return; L, H are

@@ -33,6 +33,7 @@ EXPORTS = (
     "ffca_weighted_cov", "ffca_ip_update_w", "ffca_source_gain", "ffca_em_update_lh",
     "ffca_mm_update_lh", "ffca_log_abs_det2", "ffca_debug_restart_draws",
     "ffca_pinned_buffer", "ffca_mwf", "ffca_reconstruct_scms", "ffca_ajd_cost",
+    "ffca_fit_bins",
 )
 STFT_CENTERED, STFT_FULL_FRAMES = 0, 1
 
@@ -119,6 +120,7 @@ def lib() -> C.CDLL:
         L.ffca_em_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
         L.ffca_mm_update_lh.argtypes = [P, i, i, i, P, P, P, i, C.c_double]
         L.ffca_log_abs_det2.argtypes = [P, i, P, P]
+        L.ffca_fit_bins.argtypes = [P, C.POINTER(Dims), C.POINTER(FitOpts)] + [P] * 11 + [i]
         L.ffca_mwf.argtypes = [P, i, i, P, P, P, i, P]
         L.ffca_reconstruct_scms.argtypes = [P, i, i, i, P, P, P]
         L.ffca_ajd_cost.argtypes = [P, i, i, P, P, P, P]

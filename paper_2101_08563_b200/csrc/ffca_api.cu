@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "aux_kernels.cuh"
@@ -405,6 +406,178 @@ int fit_host_chunked(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, 
   return FFCA_OK;
 }
 
+// fn(i) for i in [0, count) on nt host threads (contiguous ranges).
+template <typename Fn>
+static void host_parallel(int count, int nt, Fn fn) {
+  if (nt <= 1 || count < 2) {
+    for (int i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  nt = std::min(nt, count);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([=] {
+      const int lo = int((long long)count * t / nt), hi = int((long long)count * (t + 1) / nt);
+      for (int i = lo; i < hi; ++i) fn(i);
+    });
+  for (auto& t : th) t.join();
+}
+
+// The host fit on PER-BIN buffers (ffca_fit_bins): what a caller holding the
+// reference's containers has -- one allocation per bin for x, W, L, H.  The
+// library gathers bin chunks into page-locked staging on host threads and
+// runs the chunks depth-first on their own streams, so the gather of chunk
+// c+1 overlaps the transfer and fit of chunk c, and the scatter of chunk c's
+// results overlaps the fits of the later chunks.  Snapshot input only.
+template <typename R>
+int fit_host_gather(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o,
+                    const double* const* x_bins, const double* power, const double* const* W_in,
+                    const double* const* L_in, const double* const* H_in, double* const* W_out,
+                    double* const* L_out, double* const* H_out, double* nll, double* nll_slots,
+                    int32_t* bin_status, int host_threads, int K) {
+  const int P = d->batch * d->bins, M = d->dim, N = d->sources, T = d->frames;
+  const int iters = o->iters;
+  const bool record = o->record_trace != 0;
+  cudaError_t err;
+  const size_t nx = size_t(P) * T * M * 2, nh = size_t(P) * T * N;
+  const size_t nw = size_t(P) * M * M * 2, nl = size_t(P) * M * N;
+  double* px = static_cast<double*>(ffca_pinned_buffer(ctx, 2, nx * 8));
+  double* ph = static_cast<double*>(ffca_pinned_buffer(ctx, 3, nh * 8));
+  double* pw = static_cast<double*>(ffca_pinned_buffer(ctx, 4, nw * 8));
+  double* pl = static_cast<double*>(ffca_pinned_buffer(ctx, 5, nl * 8));
+  int* pstat = static_cast<int*>(ffca_pinned_buffer(ctx, 6, size_t(P) * 4));
+  if (!px || !ph || !pw || !pl || !pstat)
+    return set_err(FFCA_CUDA_ERROR, "ffca: pinned staging alloc failed");
+  double* dx = static_cast<double*>(ctx->get(kX, nx * 8, &err));
+  R* xs = sizeof(R) == 8 ? reinterpret_cast<R*>(dx) : static_cast<R*>(ctx->get(kXs, nx * sizeof(R), &err));
+  double* dh = static_cast<double*>(ctx->get(kH, nh * 8, &err));
+  R* hs = static_cast<R*>(ctx->get(kHs, nh * sizeof(R), &err));
+  double* dW = static_cast<double*>(ctx->get(kW, nw * 8, &err));
+  double* dL = static_cast<double*>(ctx->get(kL, nl * 8, &err));
+  double* dpow = static_cast<double*>(ctx->get(kPow, size_t(P) * 8, &err));
+  double* dnll = static_cast<double*>(ctx->get(kNll, size_t(iters + 1) * P * 8, &err));
+  int* dstat = static_cast<int*>(ctx->get(kStat, size_t(P) * 4, &err));
+  if (!dx || !xs || !dh || !hs || !dW || !dL || !dpow || !dnll || !dstat)
+    return set_err(FFCA_CUDA_ERROR, "ffca: alloc failed");
+  for (int c = 0; c < K; ++c)
+    if (!ctx->cstream[c]) FFCA_CUDA(cudaStreamCreateWithFlags(&ctx->cstream[c], cudaStreamNonBlocking));
+  auto range = [&](int c, int& lo, int& n) {
+    lo = int((long long)P * c / K);
+    n = int((long long)P * (c + 1) / K) - lo;
+  };
+  const size_t bx = size_t(T) * M * 2, bh = size_t(T) * N, bw = size_t(M) * M * 2, bl = size_t(M) * N;
+  for (int c = 0; c < K; ++c) {
+    int lo, n;
+    range(c, lo, n);
+    if (n == 0) continue;
+    host_parallel(n, host_threads, [&, lo](int j) {
+      const size_t p = size_t(lo + j);
+      std::memcpy(px + p * bx, x_bins[p], bx * 8);
+      std::memcpy(ph + p * bh, H_in[p], bh * 8);
+      std::memcpy(pw + p * bw, W_in[p], bw * 8);
+      std::memcpy(pl + p * bl, L_in[p], bl * 8);
+    });
+    cudaStream_t s = ctx->cstream[c];
+    const size_t xo = size_t(lo) * bx, ho = size_t(lo) * bh;
+    FFCA_CUDA(cudaMemcpyAsync(dx + xo, px + xo, size_t(n) * bx * 8, cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dh + ho, ph + ho, size_t(n) * bh * 8, cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dW + size_t(lo) * bw, pw + size_t(lo) * bw, size_t(n) * bw * 8,
+                              cudaMemcpyHostToDevice, s));
+    FFCA_CUDA(cudaMemcpyAsync(dL + size_t(lo) * bl, pl + size_t(lo) * bl, size_t(n) * bl * 8,
+                              cudaMemcpyHostToDevice, s));
+    if (power)
+      FFCA_CUDA(cudaMemcpyAsync(dpow + lo, power + lo, size_t(n) * 8, cudaMemcpyHostToDevice, s));
+    stage_kernel<R><<<n, 256, 0, s>>>(reinterpret_cast<const double2*>(dx + xo),
+                                      reinterpret_cast<cplx_t<R>*>(xs + xo), dh + ho, hs + ho,
+                                      power ? nullptr : dpow + lo, M, N, T);
+    ctx->launches++;
+    FFCA_CUDA(cudaGetLastError());
+    FitParams fp{};
+    fp.nprob = n;
+    fp.N = N;
+    fp.T = T;
+    fp.F = d->mixture_bins > 0 ? d->mixture_bins : d->bins;
+    fp.seed_bin0 = d->first_bin + lo;
+    fp.prob_offset = lo;
+    fp.work_total = P;
+    fp.work_first = lo;
+    fp.x = xs + xo;
+    fp.H = hs + ho;
+    fp.W = reinterpret_cast<double2*>(dW) + size_t(lo) * M * M;
+    fp.L = dL + size_t(lo) * bl;
+    fp.power = dpow + lo;
+    fp.nll = dnll;
+    fp.nll_stride = P;
+    fp.status = dstat + lo;
+    fp.iters = iters;
+    fp.flavor = o->flavor;
+    fp.record = record ? 1 : 0;
+    fp.normalize = o->normalize_scales;
+    fp.fix_loadings = o->fix_loadings;
+    fp.seed = o->seed;
+    int rc = launch_fit<R>(ctx, M, fp, s);
+    if (rc) return rc;
+    FFCA_CUDA(cudaMemcpyAsync(pstat + lo, dstat + lo, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+    if (iters > 0) {
+      const size_t hn = size_t(n) * bh;
+      unpack_h_kernel<R><<<grid_for(hn, 256), 256, 0, s>>>(hs + ho, dh + ho, dstat + lo,
+                                                            size_t(T) * N, hn);
+      ctx->launches++;
+      FFCA_CUDA(cudaGetLastError());
+      FFCA_CUDA(cudaMemcpyAsync(ph + ho, dh + ho, hn * 8, cudaMemcpyDeviceToHost, s));
+      FFCA_CUDA(cudaMemcpyAsync(pw + size_t(lo) * bw, dW + size_t(lo) * bw, size_t(n) * bw * 8,
+                                cudaMemcpyDeviceToHost, s));
+      FFCA_CUDA(cudaMemcpyAsync(pl + size_t(lo) * bl, dL + size_t(lo) * bl, size_t(n) * bl * 8,
+                                cudaMemcpyDeviceToHost, s));
+    }
+  }
+  // Scatter each chunk as it completes (the later chunks still compute).  A
+  // numerical failure stops the scatter: the outputs are then unspecified.
+  int rc_num = FFCA_OK;
+  for (int c = 0; c < K; ++c) {
+    int lo, n;
+    range(c, lo, n);
+    if (n == 0) continue;
+    FFCA_CUDA(cudaStreamSynchronize(ctx->cstream[c]));
+    for (int p = lo; p < lo + n && rc_num == FFCA_OK; ++p) {
+      const int st = pstat[p] & 0xff;
+      if (st == kStatusIpSingular)
+        rc_num = set_err(FFCA_NUMERICAL, "ip_update_w: singular system for column " +
+                                             std::to_string(pstat[p] >> 8));
+      else if (st == kStatusSingularW)
+        rc_num = set_err(FFCA_NUMERICAL, "singular decorrelation matrix");
+    }
+    if (rc_num == FFCA_OK && iters > 0)
+      host_parallel(n, host_threads, [&, lo](int j) {
+        const size_t p = size_t(lo + j);
+        std::memcpy(H_out[p], ph + p * bh, bh * 8);
+        std::memcpy(W_out[p], pw + p * bw, bw * 8);
+        std::memcpy(L_out[p], pl + p * bl, bl * 8);
+      });
+  }
+  if (rc_num != FFCA_OK) return rc_num;
+  const int* stat_p = pstat;
+  std::vector<double> slots;
+  if (record) {
+    slots.resize(size_t(iters + 1) * P);
+    FFCA_CUDA(cudaMemcpy(slots.data(), dnll, slots.size() * 8, cudaMemcpyDeviceToHost));
+  }
+  if (bin_status) std::memcpy(bin_status, stat_p, size_t(P) * 4);
+  if (record) {
+    const int F = d->bins;
+    for (int b = 0; b < d->batch; ++b)
+      for (int t = 0; t <= iters; ++t) {
+        double sum = 0.0;  // bin order, fastfca.cpp:188
+        for (int i = 0; i < F; ++i) sum += slots[size_t(t) * P + size_t(b) * F + i];
+        if (nll) nll[size_t(b) * (iters + 1) + t] = sum;
+        if (nll_slots)
+          for (int i = 0; i < F; ++i)
+            nll_slots[(size_t(b) * (iters + 1) + t) * F + i] = slots[size_t(t) * P + size_t(b) * F + i];
+      }
+  }
+  return FFCA_OK;
+}
+
 // Chunks for the pipelined host fit: one per ~128 bins, at most kMaxChunks;
 // 1 (the plain path) below 256 bins.
 inline int fit_chunks(int P) {
@@ -532,6 +705,37 @@ int ffca_fit(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const do
              const double* power, double* W, double* L, double* H, double* nll,
              double* nll_slots, int32_t* bin_status) {
   return fit_entry(ctx, d, o, x, power, W, L, H, nll, nll_slots, bin_status, false, false);
+}
+
+int ffca_fit_bins(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o,
+                  const double* const* x_bins, const double* power, const double* const* W_in,
+                  const double* const* L_in, const double* const* H_in, double* const* W_out,
+                  double* const* L_out, double* const* H_out, double* nll, double* nll_slots,
+                  int32_t* bin_status, int host_threads) {
+  if (!ctx || !d || !o || !x_bins || !W_in || !L_in || !H_in || !W_out || !L_out || !H_out)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_bins: null argument");
+  if (d->batch < 1 || d->bins < 1) return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_bins: empty shape");
+  int rc = check_dims((long long)d->batch * d->bins, d->dim, d->sources, d->frames);
+  if (rc) return rc;
+  if (o->iters < 0) return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: negative iteration count");
+  if (o->flavor != FFCA_FLAVOR_EM && o->flavor != FFCA_FLAVOR_MM)
+    return set_err(FFCA_INVALID_ARGUMENT, "fastfca_fit: unknown flavor");
+  if (o->record_trace && !nll && !nll_slots)
+    return set_err(FFCA_INVALID_ARGUMENT, "ffca_fit_bins: record_trace needs an nll buffer");
+  ctx->launches = 0;
+  DeviceGuard g(ctx->device);
+  const int P = d->batch * d->bins;
+  if (o->iters == 0 && !o->record_trace) {
+    if (bin_status) std::memset(bin_status, 0, sizeof(int32_t) * P);
+    return FFCA_OK;  // the outputs already hold the init (the caller's copy)
+  }
+  if (host_threads < 1) host_threads = int(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+  const int K = std::max(1, std::min(kMaxChunks, std::max(fit_chunks(P), std::min(P, 4))));
+  return o->precision == FFCA_PREC_FP64
+             ? fit_host_gather<double>(ctx, d, o, x_bins, power, W_in, L_in, H_in, W_out, L_out,
+                                       H_out, nll, nll_slots, bin_status, host_threads, K)
+             : fit_host_gather<float>(ctx, d, o, x_bins, power, W_in, L_in, H_in, W_out, L_out,
+                                      H_out, nll, nll_slots, bin_status, host_threads, K);
 }
 
 int ffca_fit_covs(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o, const double* mats,

@@ -487,16 +487,38 @@ FastFcaFitResult fastfca_fit(const SampleCovSet& covs, const FastFcaParams& init
   const ffca_fit_opts o = fit_opts(flavor, iters, fit, opts, gpu);
   std::vector<double> slots(fit.record_trace ? size_t(iters + 1) * F : 0);
   over_devices(gpu.devices, F, [&](int dev, int lo, int hi) {
-    Packed pk;
     const int n = hi - lo;
     const int nt = host_threads(gpu, n);
-    pack_bins(covs, init, lo, hi, pk, context(dev), nt);
     std::vector<double> sl(fit.record_trace ? size_t(iters + 1) * n : 0);
     ffca_dims d{1, n, covs.dim, init.sources, covs.blocks, lo, F};
-    raise((pk.snap ? ffca_fit : ffca_fit_covs)(context(dev), &d, &o, pk.x.data(), pk.pw(),
-                                               pk.W.data(), pk.L.data(), pk.H.data(), nullptr,
-                                               fit.record_trace ? sl.data() : nullptr, nullptr));
-    if (iters > 0) unpack_bins(pk, lo, hi, result.params, 0, nt);
+    if (covs.has_snapshots()) {
+      // Per-bin pointers straight into the containers: the library gathers bin
+      // chunks into pinned staging on host threads and pipelines gather / H2D /
+      // fit / D2H / scatter (ffca_fit_bins).  result.params already holds the
+      // init, so the outputs alias the inputs.
+      FastFcaParams& rp = result.params;
+      std::vector<const double*> xb(n), wi(n), li(n), hi_(n);
+      std::vector<double*> wo(n), lo_(n), ho(n);
+      std::vector<double> pw(n);
+      for (int k = 0; k < n; ++k) {
+        const int i = lo + k;
+        xb[k] = reinterpret_cast<const double*>(covs.snapshots[i].data());
+        wo[k] = reinterpret_cast<double*>(rp.decorr[i].data());
+        lo_[k] = rp.loading[i].data();
+        ho[k] = rp.act[i].data();
+        wi[k] = wo[k], li[k] = lo_[k], hi_[k] = ho[k];
+        pw[k] = covs.power_scale(i);
+      }
+      raise(ffca_fit_bins(context(dev), &d, &o, xb.data(), pw.data(), wi.data(), li.data(),
+                          hi_.data(), wo.data(), lo_.data(), ho.data(), nullptr,
+                          fit.record_trace ? sl.data() : nullptr, nullptr, nt));
+    } else {
+      Packed pk;
+      pack_bins(covs, init, lo, hi, pk, context(dev), nt);
+      raise(ffca_fit_covs(context(dev), &d, &o, pk.x.data(), pk.pw(), pk.W.data(), pk.L.data(),
+                          pk.H.data(), nullptr, fit.record_trace ? sl.data() : nullptr, nullptr));
+      if (iters > 0) unpack_bins(pk, lo, hi, result.params, 0, nt);
+    }
     for (int t = 0; fit.record_trace && t <= iters; ++t)
       for (int k = 0; k < n; ++k) slots[size_t(t) * F + lo + k] = sl[size_t(t) * n + k];
   });

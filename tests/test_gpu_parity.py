@@ -259,3 +259,39 @@ def test_streaming_bins_chunked_match_oracle(gpu, precision, monkeypatch):
         assert e <= tol, (f, e)
     # a chunked bin equals the same bin fitted alone, bit for bit
     assert np.array_equal(np.asarray(r.params.act[0]), np.asarray(r1.params.act[0]))
+
+
+# ffca_fit_bins: the fit on per-bin host buffers (the reference's containers),
+# gathered into pinned staging on host threads and pipelined over bin chunks --
+# the same bits as ffca_fit on the contiguous buffers.
+@pytest.mark.parametrize("shape", [(2, 3, 9, 300), (8, 12, 6, 2500)])
+def test_fit_bins_matches_contiguous_fit(gpu, shape):
+    import ctypes as C
+    from paper_2101_08563_b200 import _lib
+    M, N, F, T = shape
+    x, W, L, H = make_case(M, N, F, T, seed=61)
+    x[1] = 0.0  # a silent bin keeps its init
+    iters = 4
+    r = gpu_fit(x, W, L, H, iters, "fp32")
+    xb = [np.ascontiguousarray(x[f].T, np.complex128) for f in range(F)]          # [T][M]
+    Wb = [np.ascontiguousarray(W[f].T, np.complex128) for f in range(F)]          # col-major
+    Lb = [np.ascontiguousarray(L[f].T, np.float64) for f in range(F)]
+    Hb = [np.ascontiguousarray(H[f].T, np.float64) for f in range(F)]            # [T][N]
+    power = np.array([np.mean(np.abs(x[f]) ** 2) for f in range(F)])
+
+    def ptrs(arrs):
+        return (C.c_void_p * F)(*[a.ctypes.data for a in arrs])
+    nll = np.zeros(iters + 1)
+    status = np.zeros(F, np.int32)
+    d = _lib.Dims(1, F, M, N, T)
+    o = _lib.FitOpts(_lib.FLAVOR_EM, iters, 1, 0, 1, 0, _lib.PREC_FP32)
+    pw, pl, ph = ptrs(Wb), ptrs(Lb), ptrs(Hb)
+    _lib.check(_lib.lib().ffca_fit_bins(gpu.handle, d, o, ptrs(xb), None, pw, pl, ph, pw, pl, ph,
+                                        _lib.ptr(nll), None, _lib.ptr(status), 3))
+    assert np.array_equal(nll, np.asarray(r.nll))
+    assert np.array_equal(status, r.bin_status)
+    for f in range(F):
+        assert np.array_equal(Hb[f].T, np.asarray(r.params.act[f])), f
+        assert np.array_equal(Wb[f].T, np.asarray(r.params.decorr[f])), f
+        assert np.array_equal(Lb[f].T, np.asarray(r.params.loading[f])), f
+    del power
