@@ -10,7 +10,8 @@ namespace ffca {
 
 namespace {
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS, int MINB = 1, bool AUXG = false>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, int MINB = 1, bool AUXG = false,
+          bool EXACTVAR = false>
 int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
   using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS, AUXG>;
   *handled = false;
@@ -35,7 +36,7 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
       return ffca_set_err(FFCA_CUDA_ERROR, std::string("ffca: aux scratch alloc: ") + cudaGetErrorString(err));
     fp.aux = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
   }
-  if (big_incr<M, R, SLOTS>()) {
+  if (big_incr<M, R, SLOTS>() && !EXACTVAR) {
     // U scratch [problem][T][M] (fit_big.cuh INCR): one allocation for the
     // whole call, this launch's rows at work_first (concurrent chunks of the
     // pipelined host fit must not share rows or regrow the buffer).
@@ -48,11 +49,11 @@ int launch_big_t(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, bool* handled) {
     fp.work = base + size_t(fp.work_total > 0 ? fp.work_first : 0) * per;
   }
   if (C == 1) {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB, AUXG>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, false, MINB, AUXG, EXACTVAR>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     kern<<<fp.nprob, NTHR, lay.total, st>>>(fp, lay);
   } else {
-    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true, MINB, AUXG>;
+    auto kern = big_fit_kernel<M, N, R, SLOTS, NTHR, MS, true, MINB, AUXG, EXACTVAR>;
     FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total));
     if (C > 8) FFCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
@@ -89,6 +90,10 @@ int launch_fit_big(ffca_ctx* ctx, FitParams& fp, cudaStream_t st, int M, bool fp
     // is a 4-CTA cluster, and every SM hosts slices of two bins, so one bin's
     // reductions, cluster barriers and IP overlap the other's frame passes.
     // FFCA_BIG_WIDE=1: the 512-thread, one-CTA-per-SM shape (2-CTA clusters).
+    // FFCA_EXACT_VARIANCES=1: the mixture variances are summed afresh in
+    // every EM sweep instead of being updated incrementally (~5 % slower).
+    if (getenv("FFCA_EXACT_VARIANCES"))
+      return launch_big_t<8, 12, float, 8, 256, 1, 2, true, true>(ctx, fp, st, handled);
     if (getenv("FFCA_BIG_WIDE")) return launch_big_t<8, 12, float, 8, 512, 1>(ctx, fp, st, handled);
     return launch_big_t<8, 12, float, 8, 256, 1, 2, true>(ctx, fp, st, handled);
   }

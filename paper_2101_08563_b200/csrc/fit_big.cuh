@@ -343,7 +343,8 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(
 __device__ __forceinline__ float2 fmul2s(float2 a, float s) { return __fmul2_rn(a, f2(s, s)); }
 __device__ __forceinline__ float2 fneg2(float2 a) { return f2(-a.x, -a.y); }
 
-template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL, int MINB = 1, bool AUXG = false>
+template <int M, int N, typename R, int SLOTS, int NTHR, int MS, bool CL, int MINB = 1, bool AUXG = false,
+          bool EXACTVAR = false>
 __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLayout lay) {
   using Cfg = BigCfg<M, N, R, SLOTS, NTHR, MS, AUXG>;
   using C = cplx_t<R>;
@@ -360,7 +361,8 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   // Measured: c3 (M = 8, N = 12) 97.0 -> 94.5 ms; at M = 4, N = 6 the fresh
   // sum is only 12 packed FMAs per frame and the extra L2 reads cost more
   // than they save (c2 4.54 -> 4.60 ms), so it stays on the exact path.
-  constexpr bool INCR = big_incr<M, R, SLOTS>();
+  // EXACTVAR (FFCA_EXACT_VARIANCES=1 at run time) keeps the fresh sum.
+  constexpr bool INCR = big_incr<M, R, SLOTS>() && !EXACTVAR;
   using B = R;
   using BM = SMath<B>;
   namespace cg = cooperative_groups;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
   const int ps = lay.ps;
   // Frame slots in use: short bins skip the empty ones (an even count, the
   // fp32 EM sweep takes two slots per trip).
-  constexpr int SLQ = big_incr<M, R, SLOTS>() ? FFCA_BIG_FS : 2;
+  constexpr int SLQ = (big_incr<M, R, SLOTS>() && !EXACTVAR) ? FFCA_BIG_FS : 2;
   const int nsl = min(SLOTS, (((Tl + NTHR - 1) / NTHR) + SLQ - 1) / SLQ * SLQ);
   // Phase timing (diagnostics build, -DFFCA_PHASE_TIMING): thread 0 of each
   // CTA accumulates clock64 deltas; CTA rank 0 reports them per bin.

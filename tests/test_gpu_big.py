@@ -232,3 +232,20 @@ def test_big_chunked_host_fit_is_bit_equal(gpu, monkeypatch, shape):
         assert np.array_equal(a, b)
     for a, b in zip(r1.params.decorr, r3.params.decorr):
         assert np.array_equal(a, b)
+
+
+def test_big_exact_variances_switch(gpu, monkeypatch):
+    """FFCA_EXACT_VARIANCES=1 selects the c3 kernel that sums the mixture
+    variances afresh in every EM sweep; the default (incremental within an
+    iteration, rebuilt exactly by the variance pass) stays within the fp32
+    parity tolerance of it and of the oracle."""
+    x, W, L, H = make_case(2, 5000, seed=71)
+    r_incr = fit(x, W, L, H, 10, "fp32")
+    monkeypatch.setenv("FFCA_EXACT_VARIANCES", "1")
+    r_exact = fit(x, W, L, H, 10, "fp32")
+    _, _, _, nll_o, _, _ = oracle.fit(x, W, L, H, 10)
+    for r in (r_incr, r_exact):
+        rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
+        assert rel.max() <= NLL_TOL["fp32"], rel.max()
+    a, b = np.asarray(r_incr.nll), np.asarray(r_exact.nll)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-6
