@@ -56,6 +56,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "fit_kernel.cuh"
 #include "ip_fast.cuh"
@@ -66,6 +68,9 @@
 #endif
 #ifndef FFCA_BIG_PREFETCH
 #define FFCA_BIG_PREFETCH 0  // prefetch the next EM trip's U into registers (measured: no gain)
+#endif
+#ifndef FFCA_BIG_PACK_ODD
+#define FFCA_BIG_PACK_ODD 0  // packed EM sweep for odd M (padded channel): measured slower at M = 3
 #endif
 #ifndef FFCA_BIG_FS
 #define FFCA_BIG_FS 2  // frame slots per trip of the incremental EM sweep (4: spills at M = 8)
@@ -462,6 +467,10 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
     Wd[k] = w;
     Wr[k] = mkc<R>(R(w.x), R(w.y));
   }
+  if constexpr (LES != M) {  // zero the column padding (odd M)
+    for (int k = tid; k < N * LES; k += NTHR) Le[k] = R(0);
+    __syncthreads();
+  }
   for (int k = tid; k < M * N; k += NTHR) {
     const double l = p.L[size_t(b) * M * N + k];
     Ld[k] = narrow_pos<B>(l);
@@ -525,6 +534,26 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) l[m] = v[m];
+  };
+  // The first MC = M rounded up to even entries of column k (entries >= M are
+  // the zero padding written at start-up).
+  auto load_le_pad = [&](int k, R (&l)[(M + 1) & ~1]) {
+    const unsigned a = unsigned(__cvta_generic_to_shared(Le + k * LES));
+    R v[LES];
+#pragma unroll
+    for (int q = 0; q < LES / VE; ++q) {
+      if constexpr (VE == 4) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v[q * 4]), "=f"(v[q * 4 + 1]), "=f"(v[q * 4 + 2]), "=f"(v[q * 4 + 3])
+                     : "r"(a + 16 * q));
+      } else {
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(v[q * 2]), "=d"(v[q * 2 + 1])
+                     : "r"(a + 16 * q));
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < ((M + 1) & ~1); ++m) l[m] = v[m];
   };
   // Mixture variances sigma^2(m) = eps + sum_k Le(m,k) h_k.
   auto mix_var = [&](const R (&h)[NHP * VE], R (&lh)[M]) {
@@ -821,34 +850,47 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
         acc[M + 1 + 2 * q] = p2[q].x, acc[M + 2 + 2 * q] = p2[q].y;
       }
       acc[M] = hacc;
-    } else if constexpr (sizeof(R) == 4 && SLOTS % 2 == 0 && M % 2 == 0) {
+    } else if constexpr (sizeof(R) == 4 && (M % 2 == 0 || FFCA_BIG_PACK_ODD != 0)) {
       // fp32: two frame slots per trip share the loading-column loads, and
-      // the per-channel algebra runs on packed pairs (FFMA2 / FMUL2).  A slot
+      // the per-channel algebra runs on packed pairs (FFMA2 / FMUL2); an odd
+      // slot count ends with a one-slot trip.  Odd M is padded to MC = M + 1
+      // channels whose loadings, posteriors and powers are zero (their
+      // variance is eps, so every padded quantity is an exact 0).  A slot
       // past the CTA's frames computes on frame 0; its H store is skipped and
       // its contributions are zeroed through the weights (okf, ihn = 0).
-      constexpr int MP = M / 2;
+      constexpr int MC = (M + 1) & ~1, MP = MC / 2;
       float2 lc2[MP], li2[MP];
+      {
+        float lcp[MC];
+        load_le_pad(n, lcp);
 #pragma unroll
-      for (int q = 0; q < MP; ++q) lc2[q] = f2(lc[2 * q], lc[2 * q + 1]), li2[q] = f2(linv[2 * q], linv[2 * q + 1]);
+        for (int q = 0; q < MP; ++q) {
+          lc2[q] = f2(lcp[2 * q], lcp[2 * q + 1]);
+          li2[q] = f2(linv[2 * q], (2 * q + 1 < M) ? linv[(2 * q + 1 < M) ? 2 * q + 1 : 0] : 0.f);
+        }
+      }
       float2 a2[MP], p2[MP];
 #pragma unroll
       for (int q = 0; q < MP; ++q) a2[q] = f2(0.f, 0.f), p2[q] = f2(0.f, 0.f);
       float hacc = 0.f;
-#pragma unroll 1
-      for (int s = 0; s < nsl; s += 2) {
-        int t[2];
-        bool ok[2];
-        float2 u[2][MP], ph[2][MP], lh[2][MP];
-        float h[2][NHP * VE];
+      auto trip = [&](auto fsc, int s) {
+        constexpr int FS = decltype(fsc)::value;
+        int t[FS];
+        bool ok[FS];
+        float2 u[FS][MP], ph[FS][MP], lh[FS][MP];
+        float h[FS][NHP * VE];
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
+        for (int f = 0; f < FS; ++f) {
           const int t0 = frame_of(s + f, lane);
           ok[f] = t0 < Tl;
           t[f] = ok[f] ? t0 : 0;
           float uu[M], pp[M];
           tm_load_rec2<M, R>(tm_u(s + f), uu, pp);
 #pragma unroll
-          for (int q = 0; q < MP; ++q) u[f][q] = f2(uu[2 * q], uu[2 * q + 1]), ph[f][q] = f2(pp[2 * q], pp[2 * q + 1]);
+          for (int q = 0; q < MP; ++q) {
+            u[f][q] = f2(uu[2 * q], (2 * q + 1 < M) ? uu[(2 * q + 1 < M) ? 2 * q + 1 : 0] : 0.f);
+            ph[f][q] = f2(pp[2 * q], (2 * q + 1 < M) ? pp[(2 * q + 1 < M) ? 2 * q + 1 : 0] : 0.f);
+          }
           if (n > 0) {  // H row n-1 (fastfca.cpp:95-97), stored before the row is read
             float2 s2 = fmul2(ph[f][0], li2[0]);
 #pragma unroll
@@ -864,17 +906,17 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          R l[M];
-          load_le(k, l);
+          float l[MC];
+          load_le_pad(k, l);
 #pragma unroll
           for (int q = 0; q < MP; ++q) {
             const float2 lq = f2(l[2 * q], l[2 * q + 1]);
-            lh[0][q] = fma2s(lq, h[0][k], lh[0][q]);
-            lh[1][q] = fma2s(lq, h[1][k], lh[1][q]);
+#pragma unroll
+            for (int f = 0; f < FS; ++f) lh[f][q] = fma2s(lq, h[f][k], lh[f][q]);
           }
         }
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
+        for (int f = 0; f < FS; ++f) {
           const float hn = Hs[hidx(n, t[f])];
           const float ihn = ok[f] ? rcp_fast(hn) : 0.f;
           const float okf = ok[f] ? 1.f : 0.f;
@@ -886,17 +928,28 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
             const float2 gg = fmul2(ln, rl);                           // G
             const float2 w = fma2(gg, u[f][q], fneg2(ln));             // G U - L_n H_n
             const float2 vv = fma2(gg, w, ln);                         // G^2 U + (1 - G) L_n H_n
-            v[2 * q] = vv.x, v[2 * q + 1] = vv.y;
+            v[2 * q] = vv.x;
+            if (2 * q + 1 < M) v[(2 * q + 1 < M) ? 2 * q + 1 : 0] = vv.y;
             a2[q] = fma2s(vv, ihn, a2[q]);
             if (phis) p2[q] = fma2s(vv, okf, p2[q]);
           }
           tm_store_rec<M, R>(tm_phi(s + f), v);
         }
+      };
+      {
+        int s = 0;
+#pragma unroll 1
+        for (; s + 2 <= nsl; s += 2) trip(std::integral_constant<int, 2>{}, s);
+        if (s < nsl) trip(std::integral_constant<int, 1>{}, s);
       }
 #pragma unroll
       for (int q = 0; q < MP; ++q) {
-        acc[2 * q] = a2[q].x, acc[2 * q + 1] = a2[q].y;
-        acc[M + 1 + 2 * q] = p2[q].x, acc[M + 2 + 2 * q] = p2[q].y;
+        acc[2 * q] = a2[q].x;
+        acc[M + 1 + 2 * q] = p2[q].x;
+        if (2 * q + 1 < M) {
+          acc[(2 * q + 1 < M) ? 2 * q + 1 : 0] = a2[q].y;
+          acc[(2 * q + 1 < M) ? M + 2 + 2 * q : 0] = p2[q].y;
+        }
       }
       acc[M] = hacc;
     } else {
