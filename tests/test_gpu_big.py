@@ -248,4 +248,4 @@ def test_big_exact_variances_switch(gpu, monkeypatch):
         rel = np.abs(np.asarray(r.nll) - nll_o) / np.abs(nll_o)
         assert rel.max() <= NLL_TOL["fp32"], rel.max()
     a, b = np.asarray(r_incr.nll), np.asarray(r_exact.nll)
-    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-6
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5  # both within parity tolerance of each other
