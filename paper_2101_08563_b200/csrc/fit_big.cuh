@@ -72,6 +72,9 @@
 #ifndef FFCA_BIG_PACK_ODD
 #define FFCA_BIG_PACK_ODD 0  // packed EM sweep for odd M (padded channel): measured slower at M = 3
 #endif
+#ifndef FFCA_BIG_A2_SCALAR
+#define FFCA_BIG_A2_SCALAR 0  // scalar FFMA instead of FFMA2 in the covariance pass (experiment)
+#endif
 #ifndef FFCA_BIG_FS
 #define FFCA_BIG_FS 2  // frame slots per trip of the incremental EM sweep (4: spills at M = 8)
 #endif
@@ -1131,7 +1134,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
             }
             rw[mm] = (ok && live) ? rm : R(0);
           }
-          if constexpr (sizeof(R) == 4 && MW % 2 == 0) {
+          if constexpr (sizeof(R) == 4 && MW % 2 == 0 && FFCA_BIG_A2_SCALAR == 0) {
             // acc pairs (jj, mm), (jj, mm + 1): weights packed, product broadcast
 #pragma unroll
             for (int jj = 0; jj < NP; ++jj)
