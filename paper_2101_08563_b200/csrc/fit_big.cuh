@@ -75,11 +75,16 @@
 #ifndef FFCA_BIG_A2_SCALAR
 #define FFCA_BIG_A2_SCALAR 0  // scalar FFMA instead of FFMA2 in the covariance pass (experiment)
 #endif
+#ifndef FFCA_BIG_A2_UNROLL
+#define FFCA_BIG_A2_UNROLL 8  // frame batches of the covariance pass unrolled together (8 = all)
+#endif
 #ifndef FFCA_BIG_FS
 #define FFCA_BIG_FS 2  // frame slots per trip of the incremental EM sweep (4: spills at M = 8)
 #endif
 
 namespace ffca {
+
+constexpr int kA2Unroll = FFCA_BIG_A2_UNROLL;
 
 // Shared-memory carve-up of a big-bin CTA (byte offsets), computed on the host.
 struct BigLayout {
@@ -1104,7 +1109,7 @@ __global__ void __launch_bounds__(NTHR, MINB) big_fit_kernel(FitParams p, BigLay
       for (int s = 0; s < nsl; ++s) {
         R ro[M];  // this lane's own frame weights 1/sigma^2
         tm_load_rec<M, R>(INCR ? tm_phi(s) : tm_u(s), ro);
-#pragma unroll 2
+#pragma unroll(kA2Unroll)
         for (int bb = 0; bb < 32 / FPB; ++bb) {
           const int owner = bb * FPB + g;
           const int t0 = frame_of(s, owner);
