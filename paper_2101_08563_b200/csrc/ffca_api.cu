@@ -580,9 +580,10 @@ int fit_host_gather(ffca_ctx* ctx, const ffca_dims* d, const ffca_fit_opts* o,
 
 // Chunks for the pipelined host fit: one per ~128 bins, at most kMaxChunks;
 // 1 (the plain path) below 256 bins.
+constexpr int kDefaultMaxChunks = 16;
 inline int fit_chunks(int P) {
   if (const char* e = getenv("FFCA_FIT_CHUNKS")) return std::max(1, std::min(kMaxChunks, atoi(e)));
-  return P < 256 ? 1 : std::min(kMaxChunks, P / 128);
+  return P < 256 ? 1 : std::min(kDefaultMaxChunks, P / 128);
 }
 
 // ffca_fit / ffca_ica_fit and their block-covariance variants.

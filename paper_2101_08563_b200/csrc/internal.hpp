@@ -18,12 +18,12 @@ int ffca_set_err(int code, const std::string& msg);
       return ffca_set_err(FFCA_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kMaxChunks = 8;
+constexpr int kMaxChunks = 16;
 
 struct ffca_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t cstream[8] = {};  // host-fit chunk pipeline (kMaxChunks)
+  cudaStream_t cstream[16] = {};  // host-fit chunk pipeline (kMaxChunks)
   int launches = 0;
   unsigned long long* timing = nullptr;  // diagnostics: per-problem phase counters
   struct Buf {
